@@ -1,0 +1,288 @@
+#!/usr/bin/env python
+"""bench.py -- trace records/s into the cuThermo heat map on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload sgemm]
+                    [--impl ours|reference] [--dedup auto|sort|hash]
+
+One step = one pass of the whole hot path over one
+synthetic trace: thermo_reset + thermo_ingest_trace + thermo_build_heatmap +
+thermo_classify, inputs resident in HBM.  The default workload is BJ
+configs[1], the naive SGEMM 1024x1024 trace (K = 128: 270,532,608 records, G19).
+Inputs (4.3 GB) are larger than L2 (126 MB), so no explicit flush is needed.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+Multi-GPU (torchrun): each rank reduces its own independent trace of the
+workload (replicas; weak scaling) and the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace records/sec into heat map (1/2/4/8 B200) and achieved HBM GB/s vs peak"
+UNIT = "records/s"
+ALGO_BYTES = {  # 16 N + 16 U + 4 (words + sectors), per config
+    "sgemm": dict(N=270532608, U=22020096, cells=9 * 163840),
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_trace(workload: str, device: str, rank: int = 0):
+    import tracegen as tg
+    if workload == "sgemm":
+        return tg.gemm(1024, 1024, 128, "v00", device=device)
+    if workload == "stencil":
+        return tg.stencil(8192, device=device)
+    if workload == "tiny":
+        return tg.tiny("B", device=device)
+    if workload == "spmv":
+        return tg.spmv(24, 16, device=device)
+    raise SystemExit(f"unknown workload {workload}")
+
+
+def cpu_baseline(workload: str, budget_s: float = 12.0):
+    """The oracle as it stands, single-threaded on a host core, on a bounded
+    prefix sample of the same trace (records/s)."""
+    import oracle
+    import tracegen as tg
+    if workload == "sgemm":   # a prefix of whole warps: ~10 s of oracle work
+        n_total = 270532608
+        warps = max(64, int(2048 * budget_s / 10.0))
+        t = tg.gemm(1024, 1024, 128, "v00", device="cpu", warp_limit=warps)
+    else:
+        t = make_trace(workload, "cpu")
+        n_total = t.n
+    recs = t.records
+    o = oracle.Oracle([x[:4] for x in t.objects])
+    chunk = 1 << 22
+    done, t0 = 0, time.perf_counter()
+    while done < recs.shape[0] and time.perf_counter() - t0 < 3 * budget_s:
+        o.ingest(recs[done:done + chunk])
+        done += min(chunk, recs.shape[0] - done)
+    o.build()
+    o.classify()
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {done} of {n_total} records of the {workload} trace (ingest + build + classify, "
+                      f"single-threaded std::set oracle, {el:.1f} s)"}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return ws, rank, local
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    base = cpu_baseline(args.workload, budget_s=min(20.0, 4.0 + 2.0 * args.steps))
+    v = base["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.workload, "records": None},
+            "cpu_baseline": base, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="sgemm")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2507_18729_b200 import BOTH, Thermo
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t = make_trace(args.workload, str(dev), rank)
+    n = t.n
+    stream = torch.cuda.current_stream(dev)
+    dedup = {"auto": 0, "sort": 1, "hash": 2}[args.dedup]
+    th = Thermo(device=local, stream=stream.cuda_stream, max_launches=max(1, int(t.meta.get("launches", 1))),
+                max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), dedup=dedup)
+    th.register_objects(t.objects)
+
+    def step(recs):
+        th.reset()
+        th.ingest(recs)
+        th.build(BOTH)
+        return th.classify()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(3, args.warmup)):
+        step(t.records)
+    st0 = th.stats()
+    launches0 = st0["kernel_launches"]
+    dec_ms, phase = [], {k: [] for k in ("ms_decode", "ms_dedup", "ms_count", "ms_hist", "ms_pc", "ms_indicators")}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(t.records)
+            s = th.stats()
+            for k in phase:
+                phase[k].append(s[k])
+        e1.record(stream)
+        barrier()
+    ms_total = e0.elapsed_time(e1)
+    ms = ms_total / args.steps
+    launches = th.stats()["kernel_launches"] - launches0
+    if ws > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = n * ws / (ms / 1e3)
+    st = th.stats()
+    clocks = clk.summary()
+
+    # ---- e2e: same step through the C ABI with a pinned HOST trace ----
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty_like(t.records, device="cpu").pin_memory()
+        host.copy_(t.records)
+        step(host)
+        barrier()
+        t0 = time.perf_counter()
+        k2 = max(1, min(3, args.steps))
+        for _ in range(k2):
+            res = step(host)
+        barrier()
+        el = (time.perf_counter() - t0) / k2
+        d2h = len(res) * 136
+        e2e = {"value": n * ws / el, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": d2h,
+               "ms_per_step": el * 1e3}
+        del host
+
+    # ---- roofline of the dominant kernel (decode: a2 + a3) ----
+    peak, peak_kind = peaks()
+    dec = statistics.mean(phase["ms_decode"])
+    ph_mean = {k: statistics.mean(v) for k, v in phase.items()}
+    dominant = max(ph_mean, key=ph_mean.get)
+    achieved = 16.0 * n / (dec / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload)
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "kernel": "decode_kernel (a2+a3)", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": 16 * n, "ms_per_launch": dec}
+    pipe = None
+    if args.workload in ALGO_BYTES:
+        a = ALGO_BYTES[args.workload]
+        b = 16 * a["N"] + 16 * a["U"] + 4 * a["cells"]
+        pipe = {"algorithmic_bytes": b, "achieved_GBps": b / (ms / 1e3) / 1e9,
+                "frac": b / (ms / 1e3) / 1e9 / peak}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.workload, "records": n, "objects": len(t.objects),
+                       "dedup": {1: "sort", 2: "hash"}.get(st["dedup_used"], "?"),
+                       "l2": "inputs larger than L2 (16 B x records >> 126 MB), no flush",
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single"},
+            "roofline": roof, "pipeline_roofline": pipe, "phase_ms": ph_mean, "dominant_phase": dominant,
+            "clocks": clocks, "gpu_launches": launches,
+            "stats": {k: st[k] for k in ("keys_emitted", "pc_keys_emitted", "distinct_pairs", "distinct_pc_pairs",
+                                          "n_pcs")},
+            "e2e": e2e}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.workload)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

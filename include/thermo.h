@@ -1,0 +1,293 @@
+/*
+ * thermo.h -- C ABI of libthermo, a B200-native (sm_100a) implementation of the
+ * data-parallel hot path of cuThermo (arXiv 2507.18729): the reduction of a
+ * GPU memory-access trace into the paper's word-sector heat map of distinct
+ * warp counts, heat-level histograms per object and per PC, and the sharing /
+ * inefficiency indicators the paper's five patterns are read from.
+ *
+ * Citation keys: P:n = PAPER.md line n (section named alongside);
+ *                S:n = SPEC.md line n;  G# = DESIGN.md "Readings" entry.
+ *
+ * General conventions
+ *   - Every entry point returns a thermo_status; no exception crosses the ABI.
+ *     CUDA / NCCL failures are sticky: once a context has returned
+ *     THERMO_ECUDA or THERMO_ENCCL every later call returns the same code.
+ *     thermo_last_error() gives a per-context message for the last failure.
+ *   - A context is bound to one device and one CUDA stream and is NOT
+ *     thread-safe; distinct contexts are independent.
+ *   - All device work is stream-ordered on the context stream.  Queries are
+ *     synchronous (they copy small results to caller-owned HOST buffers).
+ *   - State machine: create -> register_objects (exactly once) -> ingest_trace*
+ *     -> build_heatmap -> query_* / classify.  build_heatmap may be repeated
+ *     (e.g. with another launch filter); ingest after build invalidates the
+ *     build (queries then return THERMO_ESTATE until the next build).
+ *     Out-of-order calls return THERMO_ESTATE.
+ */
+#ifndef THERMO_H_
+#define THERMO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define THERMO_ABI_VERSION 1u
+#define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
+#define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
+#define THERMO_MAX_OBJECTS 1024
+
+/*
+ * One lane's memory access: the paper's per-instruction record (P:283-292,
+ * §IV-B1: pc, address[32], size, active_mask, access_flags, warp_id,
+ * block_id) flattened to one 16-byte record per active lane.  16-byte aligned,
+ * little-endian.
+ *
+ *   addr_flags bits [0,48)  byte address (G5)
+ *              bits [48,51) log2(access size): 0..4 = 1,2,4,8,16 bytes (G4)
+ *              bits [51,53) kind: 0 load, 1 store, 2 atomic (G7: all count)
+ *              bits [53,55) space: 0 global, 1 shared, 2 local
+ *              bit  55      instr_start: first record of a warp instruction (G24)
+ *              bits [56,64) reserved, must be 0
+ *   warp       global warp id within its launch
+ *              (= linear_block_id * warps_per_block + warp_in_block; G1)
+ *   site       bits [0,20) pc >> 4 (SASS instructions are 16 B), bits [20,32) launch id
+ *
+ * A record is INVALID (skipped and counted, never fatal) if log2size > 4,
+ * kind > 2, space > 2, reserved != 0, or addr + size > 2^48.
+ * An instruction (for the misalignment indicator) is a run of
+ * records starting at a record with instr_start = 1 or at the first record of
+ * an ingest call, of at most 32 records (32 lane addresses); a longer
+ * run is split every 32 records (G24).
+ */
+typedef struct {
+  uint64_t addr_flags;
+  uint32_t warp;
+  uint32_t site;
+} thermo_record;
+
+/*
+ * A registered data object ("memory registration"; P:329 region
+ * config).  base must be 32-byte aligned (G9), len > 0, base + len <= 2^48, and
+ * objects of one space must not overlap.  id is the caller's handle
+ * used by the queries; ids must be unique.
+ * A word (4 B) belongs to the object iff its first byte lies in [base, base+len);
+ * n_words = ceil(len/4), n_sectors = ceil(len/32).
+ */
+typedef struct {
+  uint64_t base;
+  uint64_t len;
+  uint32_t space;
+  uint32_t id;
+} thermo_object;
+
+typedef enum { THERMO_WORD = 1, THERMO_SECTOR = 2, THERMO_BOTH = 3 } thermo_granularity;
+
+typedef enum {
+  THERMO_OK = 0,
+  THERMO_EINVAL = -1,  /* bad argument / malformed object table           */
+  THERMO_ENOMEM = -2,  /* device or pinned-host allocation failed          */
+  THERMO_ERANGE = -3,  /* key width overflow, id out of declared range, cap too small */
+  THERMO_ESTATE = -4,  /* call out of order                                */
+  THERMO_ECUDA = -5,   /* CUDA error (sticky)                              */
+  THERMO_ENCCL = -6    /* NCCL error (sticky)                              */
+} thermo_status;
+
+typedef enum { THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2 } thermo_dedup;
+
+/*
+ * Context configuration.  max_launches / max_warps_per_launch fix the bit
+ * widths L, W of the (sector, launch, warp) key; records whose launch or warp
+ * id exceeds them are counted in stats.out_of_range and make build return
+ * THERMO_ERANGE.  max_pcs bounds the number of distinct (launch, pc) pairs.
+ */
+typedef struct {
+  uint32_t max_launches;          /* >= 1; launch ids < max_launches (<= 4096)      */
+  uint32_t max_warps_per_launch;  /* >= 1; warp ids < this                           */
+  uint32_t max_pcs;               /* >= 1; distinct (launch, pc) pairs (<= 65536)    */
+  uint32_t dedup;                 /* thermo_dedup                                    */
+  uint32_t track_pc;              /* 1: maintain per-PC histograms (G11)             */
+  uint32_t reserved0;
+  uint64_t expected_pairs;        /* hash sizing hint: distinct (sector,warp) pairs; 0 = auto */
+} thermo_config;
+
+/*
+ * Pattern-rule parameters as exact rationals (SPEC PatternParams; G12).
+ * Defaults (thermo_default_params): theta_hot 16, alpha 5/4, beta 4/1, fs_min 4,
+ * smem_cap 1, smem_cov 9/10, gamma 1/2, strided_min_sectors 4, dom 3/4,
+ * hot_frac 1/2, fs_frac 1/4, mis_frac 1/10, cv 1/2.
+ */
+typedef struct {
+  uint64_t theta_hot, alpha_num, alpha_den, beta_num, beta_den, fs_min;
+  uint64_t smem_cap, smem_cov_num, smem_cov_den, gamma_num, gamma_den;
+  uint64_t strided_min_sectors, dom_num, dom_den, hot_frac_num, hot_frac_den;
+  uint64_t fs_frac_num, fs_frac_den, mis_frac_num, mis_frac_den, cv_num, cv_den;
+} thermo_params;
+
+/* label bits of thermo_indicators.labels (§IV-C) */
+#define THERMO_LABEL_HOT 1u
+#define THERMO_LABEL_RANDOM_HOT 2u               /* P:404 random variant */
+#define THERMO_LABEL_FALSE_SHARING 4u
+#define THERMO_LABEL_SMEM_THREAD_LOCAL 8u
+#define THERMO_LABEL_SMEM_WARP_PRIVATE 16u
+#define THERMO_LABEL_MISALIGNED 32u
+#define THERMO_LABEL_STRIDED 64u
+
+/* Per-object indicator sums and labels. */
+typedef struct {
+  uint32_t object_id;
+  uint32_t labels;             /* THERMO_LABEL_* bits                         */
+  uint64_t n_words, n_sectors;
+  uint64_t touched_sectors;    /* T: sectors with count >= 1                   */
+  uint64_t touched_words;      /* TW: words with count >= 1                    */
+  uint64_t hot_sectors;        /* c >= theta_hot and alpha_den*c <= alpha_num*max_word */
+  uint64_t fs_sectors;         /* beta_den*c >= beta_num*max_word and c >= fs_min */
+  uint64_t sum_x;              /* sum of nonzero word counts                   */
+  uint64_t sum_x2_lo, sum_x2_hi;  /* 128-bit sum of squares of word counts      */
+  uint64_t le1_words;          /* touched words with count <= smem_cap         */
+  uint64_t max_sector_count;
+  uint64_t instrs, misaligned_instrs;  /* instructions attributed to the object (G24) */
+  uint64_t gaps;               /* TW - 1 (gaps between consecutive touched words) */
+  uint64_t dom_gap, dom_count; /* gap value holding a strict majority of gaps, else 0,0 */
+} thermo_indicators;
+
+/* Per-PC heat-level histogram row (G11): distinct (launch, pc, word) pairs
+ * binned by the word's level (THERMO_WORD) or distinct (launch, pc, sector)
+ * pairs binned by the sector's level (THERMO_SECTOR). */
+typedef struct {
+  uint32_t launch;
+  uint32_t pc;                 /* byte pc (site field << 4) */
+  uint64_t hist[THERMO_LEVELS];
+} thermo_pc_hist;
+
+typedef struct {
+  uint64_t records;            /* records ingested (all calls)                */
+  uint64_t invalid;            /* invalid records (skipped)                   */
+  uint64_t out_of_range;       /* launch/warp id beyond the declared widths   */
+  uint64_t unmapped_words;     /* word accesses outside every object (G8), launch-filtered */
+  uint64_t mapped_word_accesses; /* word accesses inside objects, launch-filtered */
+  uint64_t keys_emitted;       /* (sector, launch, warp) keys after pre-dedup  */
+  uint64_t pc_keys_emitted;    /* (pc, sector) keys after pre-dedup            */
+  uint64_t distinct_pairs;     /* distinct (sector, launch, warp) = sum of sector counts */
+  uint64_t distinct_pc_pairs;  /* distinct (launch, pc, sector)                */
+  uint64_t n_pcs;              /* distinct (launch, pc) pairs seen             */
+  uint32_t dedup_used;         /* THERMO_DEDUP_SORT or THERMO_DEDUP_HASH       */
+  uint32_t reserved0;
+  double ms_ingest, ms_build, ms_classify;  /* device time of the last calls   */
+  /* device time (CUDA events on the context stream) of the phases of the last
+   * ingest / build / classify: decode kernel (a2+a3), main-key dedup (a4),
+   * segmented count (a5), object histograms (a6), per-pc dedup + histograms
+   * (a4+a6), indicators (a7) */
+  double ms_decode, ms_dedup, ms_count, ms_hist, ms_pc, ms_indicators;
+  uint64_t kernel_launches;    /* libthermo kernels launched since create      */
+} thermo_stats;
+
+typedef struct thermo_ctx thermo_ctx;
+
+/* Defaults: max_launches 1, max_warps_per_launch 2^20, max_pcs 4096, AUTO, track_pc 1. */
+void thermo_default_config(thermo_config *cfg);
+void thermo_default_params(thermo_params *p);
+uint32_t thermo_abi_version(void);
+
+/*
+ * Create a context on `device` using CUDA stream `stream` (a cudaStream_t
+ * passed as void*, NULL = a new stream owned by the context).  cfg NULL =
+ * defaults.  Ownership: the context owns every device buffer it allocates.
+ * Errors: EINVAL (bad cfg), ECUDA, ENOMEM.
+ */
+thermo_status thermo_create(thermo_ctx **out, int device, void *stream, const thermo_config *cfg);
+
+/*
+ * Multi-GPU (address-sharded) context: rank `rank` of `nranks`.  nccl_id is a
+ * 128-byte ncclUniqueId produced by rank 0 and broadcast by the caller (e.g.
+ * over a torch process group).  Every rank must issue the same sequence of
+ * calls (collective semantics).  Each rank owns the sectors g with
+ * (g >> 12) % nranks == rank.  Errors additionally: ENCCL.
+ */
+thermo_status thermo_create_dist(thermo_ctx **out, int device, void *stream, const thermo_config *cfg,
+                                 const void *nccl_id, int rank, int nranks);
+/* Writes a fresh 128-byte ncclUniqueId into out (rank 0 only). */
+thermo_status thermo_nccl_unique_id(void *out128);
+
+thermo_status thermo_destroy(thermo_ctx *ctx);
+
+/*
+ * Drop everything ingested (keys, counters, pc ids) and return to the
+ * "registered" state, keeping the object table and all allocations -- for
+ * repeated runs over new traces of the same objects.  Errors: ESTATE.
+ */
+thermo_status thermo_reset(thermo_ctx *ctx);
+
+/*
+ * Register the data objects.  Called exactly once, before any
+ * ingest.  objs is a HOST array of n objects (copied).  Errors: EINVAL
+ * (len == 0, base not 32-aligned, base+len > 2^48, space > 2, overlap within a
+ * space, duplicate id, n == 0 or n > THERMO_MAX_OBJECTS), ERANGE (total sectors
+ * do not fit the key together with the declared launch/warp widths), ESTATE.
+ */
+thermo_status thermo_register_objects(thermo_ctx *ctx, const thermo_object *objs, size_t n);
+
+/*
+ * Ingest n records (the analyzer consumes the collector's
+ * buffers).  recs may be a DEVICE pointer (fast path; must stay valid until
+ * the context stream passes this call) or a HOST pointer (pinned or pageable;
+ * staged through pinned chunks with copies overlapped with decoding; the call
+ * returns when the host buffer may be reused).  The first record starts an
+ * instruction.  n == 0 is a no-op.  Errors: EINVAL (recs NULL with n > 0,
+ * misaligned), ESTATE, ENOMEM, ECUDA.
+ */
+thermo_status thermo_ingest_trace(thermo_ctx *ctx, const thermo_record *recs, size_t n);
+
+/*
+ * Reduce everything ingested so far into the heat map (the
+ * popcount flush): dense per-object word and sector distinct-warp counts,
+ * level histograms per object and per PC.  launch_filter selects one launch
+ * (the paper's per-kernel heat map, G2) or THERMO_ALL_LAUNCHES (launch-
+ * qualified warps of all launches).  g selects which histograms are computed;
+ * counts are always produced for both granularities.  Errors: ESTATE, ERANGE
+ * (out-of-range records were ingested, or too many distinct pcs), ECUDA.
+ */
+thermo_status thermo_build_heatmap(thermo_ctx *ctx, thermo_granularity g, uint32_t launch_filter);
+
+/*
+ * Dense heat-map rows of object `object_id` into the HOST buffer out:
+ *   THERMO_WORD   n_words   u32 word counts
+ *   THERMO_SECTOR n_sectors u32 sector counts
+ *   THERMO_BOTH   9*n_sectors u32: per sector its 8 word counts (0 past n_words)
+ *                 then the sector count (the paper's 9-cell row)
+ * *n_out receives the element count; ERANGE (with *n_out set) if cap is too
+ * small.  Errors: EINVAL (unknown id), ESTATE.
+ */
+thermo_status thermo_query_heatmap(thermo_ctx *ctx, uint32_t object_id, thermo_granularity g,
+                                   uint32_t *out, size_t cap, size_t *n_out);
+
+/* Level histogram (THERMO_LEVELS bins, HOST buffer) of one object over all its
+ * n_words words (THERMO_WORD) or n_sectors sectors (THERMO_SECTOR); level-0
+ * counts untouched ones.  Errors: EINVAL, ESTATE. */
+thermo_status thermo_query_histogram(thermo_ctx *ctx, uint32_t object_id, thermo_granularity g,
+                                     uint64_t hist[THERMO_LEVELS]);
+
+/* Per-PC histograms in ascending (launch, pc) order into HOST out[cap].
+ * ERANGE (with *n_out set) if cap is too small; ESTATE if track_pc == 0. */
+thermo_status thermo_query_per_pc(thermo_ctx *ctx, thermo_granularity g, thermo_pc_hist *out,
+                                  size_t cap, size_t *n_out);
+
+/*
+ * Pattern indicators and labels per object (rules S:356-409 as
+ * exact integer inequalities).  params NULL = defaults.
+ * out[cap] HOST, one row per object in registration order.  Errors: ESTATE,
+ * ERANGE (cap < number of objects), ECUDA.
+ */
+thermo_status thermo_classify(thermo_ctx *ctx, const thermo_params *params, thermo_indicators *out,
+                              size_t cap, size_t *n_out);
+
+thermo_status thermo_get_stats(thermo_ctx *ctx, thermo_stats *out);
+
+/* Per-context message of the last failure ("" if none).  Valid until the next call. */
+const char *thermo_last_error(const thermo_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* THERMO_H_ */

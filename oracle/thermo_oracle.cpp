@@ -134,10 +134,14 @@ struct Oracle {
       }
       in_instr = false; has_valid = false; i_obj = -1; i_sectors.clear();
     };
+    size_t pos = 0;  // record position within the current instruction
     for (size_t k = 0; k < n; ++k) {
       Rec r = parse(recs + 16 * k);
       ++n_records;
-      if (k == 0 || r.instr_start) { close_instr(); in_instr = true; }
+      // an instruction has at most 32 lane records ("32-element array");
+      // a longer run without instr_start is split every 32 records (G24)
+      if (k == 0 || r.instr_start || pos == 32) { close_instr(); in_instr = true; pos = 0; }
+      ++pos;
       if (!r.valid) { ++n_invalid; continue; }
       // ---- instruction extent (Fig.6) ----
       uint64_t lo = (uint64_t(r.space) << 48) | r.addr;

@@ -1,0 +1,786 @@
+// thermo_api.cu -- the C ABI of libthermo (include/thermo.h) and the host-side
+// orchestration of the hot path: object staging (a1), ingest
+// (a2/a3 kernels), build (a4/a5/a6 kernels), classify (a7 kernels), queries.
+// Host code only launches kernels and moves small results; every step of the
+// reduction runs in the kernels of decode.cu, sort.cu, count.cu, indicators.cu.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "thermo_internal.cuh"
+
+using namespace thermo;
+
+namespace {
+
+constexpr ull kRangeLen = 2048;          // records per decode work range
+constexpr ull kHostChunk = 1ull << 24;   // records per staged host chunk
+constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors)
+
+int bit_width(ull x) { return x ? 64 - __builtin_clzll(x) : 0; }
+ull next_pow2(ull x) {
+  ull p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct thermo_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;
+  thermo_config cfg{};
+  int num_sms = 148;
+  int state = 0;  // 0 created, 1 registered, 2 ingested, 3 built
+  thermo_status sticky = THERMO_OK;
+  std::string err;
+  int rank = 0, nranks = 1;
+
+  // objects
+  std::vector<thermo_object> reg;
+  std::vector<uint32_t> sorted_to_reg, reg_to_sorted;
+  std::unordered_map<uint32_t, uint32_t> id_to_reg;
+  std::vector<ull> h_lo, h_hi, h_soff, h_nwords;
+  std::vector<uint32_t> h_space;
+  ull S_tot = 0;
+  KeyLayout kl{};
+  uint32_t n_tiles = 0;
+
+  // device buffers
+  ull *d_lo = nullptr, *d_hi = nullptr, *d_soff = nullptr, *d_nwords = nullptr;
+  uint32_t* d_space = nullptr;
+  uint32_t *d_wc = nullptr, *d_sc = nullptr;
+  ull* d_keys = nullptr;
+  size_t keys_cap = 0;
+  ull* d_pckeys = nullptr;
+  size_t pckeys_cap = 0;
+  ull n_keys = 0, n_pckeys = 0;
+  DevCounters* d_ctr = nullptr;
+  ull* d_pc_keys_tab = nullptr;
+  uint32_t* d_pc_vals = nullptr;
+  uint32_t* d_site_of = nullptr;
+  uint32_t pc_cap = 0;
+  ull* d_instr = nullptr;
+  ull* d_launch_ctr = nullptr;
+  ull* d_hist = nullptr;
+  ull* d_pchist = nullptr;
+  ull* d_ind = nullptr;
+  ull *d_tile_obj = nullptr, *d_tile_first = nullptr, *d_tile_end = nullptr;
+  ull* d_tile_info = nullptr;
+  ull* d_tile_prev = nullptr;  // followed by obj_tile0 (u32[n+1])
+  ull* d_heads = nullptr;
+  size_t heads_cap = 0;
+  ull* d_table = nullptr;
+  size_t table_cap = 0;
+  ull* d_pctable = nullptr;
+  size_t pctable_cap = 0;
+  SortWorkspace sw, swpc;
+  // host staging
+  void* h_pinned[2] = {nullptr, nullptr};
+  uint4* d_stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evp[8] = {};  // phase timers
+  ull launches = 0;         // kernels launched
+  float ms_phase[6] = {0, 0, 0, 0, 0, 0};  // decode, dedup, count, hist, pc, indicators
+
+  uint32_t built_filter = THERMO_ALL_LAUNCHES;
+  uint32_t built_gran = THERMO_BOTH;
+  uint32_t dedup_used = THERMO_DEDUP_SORT;
+  ull records = 0;
+  float ms_ingest = 0, ms_build = 0, ms_classify = 0;
+  bool hist_valid = false;
+};
+
+namespace {
+
+thermo_status fail(thermo_ctx* c, thermo_status st, const std::string& msg) {
+  if (c) {
+    c->err = msg;
+    if (st == THERMO_ECUDA || st == THERMO_ENCCL) c->sticky = st;
+  }
+  return st;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(ctx, THERMO_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+ObjTable obj_table(thermo_ctx* c) { return ObjTable{c->d_lo, c->d_hi, c->d_soff, (uint32_t)c->reg.size()}; }
+
+thermo_status pre(thermo_ctx* ctx) {
+  if (!ctx) return THERMO_EINVAL;
+  if (ctx->sticky != THERMO_OK) return ctx->sticky;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return fail(ctx, THERMO_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  ctx->err.clear();
+  return THERMO_OK;
+}
+
+// grow a device key buffer to hold `need` keys, preserving `keep` keys
+thermo_status grow_keys(thermo_ctx* ctx, ull** buf, size_t* cap, ull need, ull keep) {
+  if (need <= *cap) return THERMO_OK;
+  size_t ncap = std::max<size_t>(need, *cap + *cap / 2);
+  ull* nb = nullptr;
+  if (cudaMalloc(&nb, ncap * sizeof(ull)) != cudaSuccess) {
+    cudaGetLastError();
+    ncap = need;
+    if (cudaMalloc(&nb, ncap * sizeof(ull)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, THERMO_ENOMEM, "key buffer allocation failed");
+    }
+  }
+  if (keep) CK(cudaMemcpyAsync(nb, *buf, keep * sizeof(ull), cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  dfree(*buf);
+  *buf = nb;
+  *cap = ncap;
+  return THERMO_OK;
+}
+
+// decode one device-resident call (records[0] starts an instruction)
+thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
+  if (n == 0) return THERMO_OK;
+  const ull n_ranges = (n + kRangeLen - 1) / kRangeLen;
+  if (ctx->heads_cap < n_ranges + 1) {
+    dfree(ctx->d_heads);
+    ctx->heads_cap = n_ranges + 1 + 1024;
+    CK(dalloc(&ctx->d_heads, ctx->heads_cap));
+  }
+  CK(cudaEventRecord(ctx->evp[6], ctx->stream));
+  launch_find_heads(recs, n, kRangeLen, (uint32_t)n_ranges, ctx->d_heads, ctx->stream);
+  DecodeArgs a{};
+  a.recs = recs;
+  a.n = n;
+  a.heads = ctx->d_heads;
+  a.n_ranges = (uint32_t)n_ranges;
+  a.obj = obj_table(ctx);
+  a.kl = ctx->kl;
+  a.max_launches = ctx->cfg.max_launches;
+  a.max_warps = ctx->cfg.max_warps_per_launch;
+  a.track_pc = ctx->cfg.track_pc ? 1 : 0;
+  a.pcmap = PcMap{ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of, ctx->pc_cap - 1, ctx->cfg.max_pcs};
+  a.keys = ctx->d_keys;
+  a.pckeys = ctx->d_pckeys;
+  a.ctr = ctx->d_ctr;
+  a.instr_ctr = ctx->d_instr;
+  a.launch_ctr = ctx->d_launch_ctr;
+  launch_decode(a, ctx->num_sms, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evp[7], ctx->stream));
+  ctx->launches += 2;
+  return THERMO_OK;
+}
+
+thermo_status sync_counts(thermo_ctx* ctx) {
+  ull v[2];
+  CK(cudaMemcpyAsync(v, ctx->d_ctr, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->n_keys = v[0];
+  ctx->n_pckeys = v[1];
+  return THERMO_OK;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+void thermo_default_config(thermo_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->max_launches = 1;
+  cfg->max_warps_per_launch = 1u << 20;
+  cfg->max_pcs = 4096;
+  cfg->dedup = THERMO_DEDUP_AUTO;
+  cfg->track_pc = 1;
+}
+
+void thermo_default_params(thermo_params* p) {
+  if (!p) return;
+  *p = thermo_params{16, 5, 4, 4, 1, 4, 1, 9, 10, 1, 2, 4, 3, 4, 1, 2, 1, 4, 1, 10, 1, 2};
+}
+
+uint32_t thermo_abi_version(void) { return THERMO_ABI_VERSION; }
+
+thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const thermo_config* cfg) {
+  if (!out) return THERMO_EINVAL;
+  *out = nullptr;
+  thermo_config c;
+  if (cfg) c = *cfg; else thermo_default_config(&c);
+  if (c.max_launches < 1 || c.max_launches > 4096 || c.max_warps_per_launch < 1 || c.max_pcs < 1 ||
+      c.max_pcs > 65536 || c.dedup > THERMO_DEDUP_HASH)
+    return THERMO_EINVAL;
+  thermo_ctx* ctx = new thermo_ctx();
+  ctx->device = device;
+  ctx->cfg = c;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { delete ctx; return THERMO_ECUDA; }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return THERMO_ECUDA; }
+    ctx->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) {
+    delete ctx;
+    return THERMO_ECUDA;
+  }
+  for (int i = 0; i < 8; ++i)
+    if (cudaEventCreate(&ctx->evp[i]) != cudaSuccess) {
+    delete ctx;
+    return THERMO_ECUDA;
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_used[i], cudaEventDisableTiming);
+  }
+  if (dalloc(&ctx->d_ctr, 1) != cudaSuccess) { delete ctx; return THERMO_ENOMEM; }
+  cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), ctx->stream);
+  *out = ctx;
+  return THERMO_OK;
+}
+
+thermo_status thermo_create_dist(thermo_ctx** out, int device, void* stream, const thermo_config* cfg,
+                                 const void* nccl_id, int rank, int nranks) {
+  if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks) return THERMO_EINVAL;
+  if (nranks == 1) return thermo_create(out, device, stream, cfg);
+  *out = nullptr;
+  return THERMO_ESTATE;  // address-sharded mode: see DESIGN.md "Multi-GPU" (next row)
+}
+
+thermo_status thermo_nccl_unique_id(void* out128) {
+  if (!out128) return THERMO_EINVAL;
+  std::memset(out128, 0, 128);
+  return THERMO_ESTATE;
+}
+
+thermo_status thermo_destroy(thermo_ctx* ctx) {
+  if (!ctx) return THERMO_EINVAL;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  void* bufs[] = {ctx->d_lo, ctx->d_hi, ctx->d_soff, ctx->d_nwords, ctx->d_space, ctx->d_wc, ctx->d_sc,
+                  ctx->d_keys, ctx->d_pckeys, ctx->d_ctr, ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of,
+                  ctx->d_instr, ctx->d_launch_ctr, ctx->d_hist, ctx->d_pchist, ctx->d_ind, ctx->d_tile_obj,
+                  ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
+                  ctx->d_table, ctx->d_pctable, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
+                  ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->d_stage[0],
+                  ctx->d_stage[1]};
+  for (void* b : bufs) dfree(b);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->h_pinned[i]) cudaFreeHost(ctx->h_pinned[i]);
+    if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
+    if (ctx->ev_used[i]) cudaEventDestroy(ctx->ev_used[i]);
+  }
+  for (int i = 0; i < 8; ++i)
+    if (ctx->evp[i]) cudaEventDestroy(ctx->evp[i]);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return THERMO_OK;
+}
+
+thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs, size_t n) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 0) return fail(ctx, THERMO_ESTATE, "objects already registered");
+  if (!objs || n == 0 || n > THERMO_MAX_OBJECTS) return fail(ctx, THERMO_EINVAL, "need 1..1024 objects");
+  std::vector<uint32_t> order(n);
+  std::unordered_map<uint32_t, uint32_t> ids;
+  for (size_t i = 0; i < n; ++i) {
+    const thermo_object& o = objs[i];
+    if (o.len == 0 || (o.base & 31) || o.space > 2 || o.base + o.len > (1ull << 48) || o.base + o.len < o.base)
+      return fail(ctx, THERMO_EINVAL, "object " + std::to_string(i) + ": need len > 0, base % 32 == 0, space <= 2, base+len <= 2^48");
+    if (!ids.emplace(o.id, (uint32_t)i).second) return fail(ctx, THERMO_EINVAL, "duplicate object id");
+    order[i] = (uint32_t)i;
+  }
+  auto key = [&](uint32_t i) { return ((ull)objs[i].space << 48) | objs[i].base; };
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+  for (size_t j = 1; j < n; ++j) {
+    const thermo_object &a = objs[order[j - 1]], &b = objs[order[j]];
+    if (a.space == b.space && a.base + a.len > b.base) return fail(ctx, THERMO_EINVAL, "objects overlap");
+  }
+  ctx->reg.assign(objs, objs + n);
+  ctx->id_to_reg = ids;
+  ctx->sorted_to_reg = order;
+  ctx->reg_to_sorted.assign(n, 0);
+  ctx->h_lo.resize(n); ctx->h_hi.resize(n); ctx->h_soff.resize(n + 1); ctx->h_nwords.resize(n);
+  ctx->h_space.resize(n);
+  ull soff = 0;
+  std::vector<ull> tile_obj, tile_first, tile_end;
+  std::vector<uint32_t> obj_tile0(n + 1, 0);
+  for (size_t j = 0; j < n; ++j) {
+    const thermo_object& o = objs[order[j]];
+    ctx->reg_to_sorted[order[j]] = (uint32_t)j;
+    ctx->h_lo[j] = ((ull)o.space << 48) | o.base;
+    ctx->h_hi[j] = ctx->h_lo[j] + o.len;
+    ctx->h_soff[j] = soff;
+    ctx->h_nwords[j] = (o.len + 3) / 4;
+    ctx->h_space[j] = o.space;
+    const ull ns = (o.len + 31) / 32;
+    obj_tile0[j] = (uint32_t)tile_obj.size();
+    for (ull t = 0; t < ns; t += kTileSectors) {
+      tile_obj.push_back(j);
+      tile_first.push_back(soff + t);
+      tile_end.push_back(soff + std::min(ns, t + kTileSectors));
+    }
+    soff += ns;
+  }
+  obj_tile0[n] = (uint32_t)tile_obj.size();
+  ctx->h_soff[n] = soff;
+  ctx->S_tot = soff;
+  ctx->n_tiles = (uint32_t)tile_obj.size();
+  const thermo_config& c = ctx->cfg;
+  KeyLayout kl;
+  kl.S = std::max(1, bit_width(soff - 1));
+  kl.L = bit_width(c.max_launches - 1);
+  kl.W = bit_width(c.max_warps_per_launch - 1);
+  kl.P = bit_width(c.max_pcs - 1);
+  if (kl.S + kl.L + kl.W > 56 || kl.P + kl.S > 56)
+    return fail(ctx, THERMO_ERANGE, "sector/launch/warp key widths exceed 56 bits");
+  ctx->kl = kl;
+  // ---- device tables ----
+  CK(dalloc(&ctx->d_lo, n)); CK(dalloc(&ctx->d_hi, n)); CK(dalloc(&ctx->d_soff, n + 1));
+  CK(dalloc(&ctx->d_nwords, n)); CK(dalloc(&ctx->d_space, n));
+  CK(cudaMemcpy(ctx->d_lo, ctx->h_lo.data(), n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_hi, ctx->h_hi.data(), n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_soff, ctx->h_soff.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_nwords, ctx->h_nwords.data(), n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_space, ctx->h_space.data(), n * 4, cudaMemcpyHostToDevice));
+  if (dalloc(&ctx->d_wc, 8 * soff) != cudaSuccess || dalloc(&ctx->d_sc, soff) != cudaSuccess)
+    return fail(ctx, THERMO_ENOMEM, "dense heat-map arrays");
+  CK(dalloc(&ctx->d_instr, (size_t)c.max_launches * n * 2));
+  CK(dalloc(&ctx->d_launch_ctr, (size_t)c.max_launches * 2));
+  CK(dalloc(&ctx->d_hist, n * 2 * kLevels));
+  CK(dalloc(&ctx->d_pchist, (size_t)c.max_pcs * 2 * kLevels));
+  CK(dalloc(&ctx->d_ind, n * kIndFields));
+  const size_t nt = std::max<size_t>(1, ctx->n_tiles);
+  CK(dalloc(&ctx->d_tile_obj, nt)); CK(dalloc(&ctx->d_tile_first, nt)); CK(dalloc(&ctx->d_tile_end, nt));
+  CK(dalloc(&ctx->d_tile_info, nt * 4));
+  CK(dalloc(&ctx->d_tile_prev, nt + (n + 2) / 2 + 1));
+  if (ctx->n_tiles) {
+    CK(cudaMemcpy(ctx->d_tile_obj, tile_obj.data(), ctx->n_tiles * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_tile_first, tile_first.data(), ctx->n_tiles * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->d_tile_end, tile_end.data(), ctx->n_tiles * 8, cudaMemcpyHostToDevice));
+  }
+  CK(cudaMemcpy(ctx->d_tile_prev + ctx->n_tiles, obj_tile0.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  ctx->pc_cap = (uint32_t)next_pow2(std::max<ull>(64, 4ull * c.max_pcs));
+  CK(dalloc(&ctx->d_pc_keys_tab, ctx->pc_cap));
+  CK(dalloc(&ctx->d_pc_vals, ctx->pc_cap));
+  CK(dalloc(&ctx->d_site_of, c.max_pcs));
+  ctx->state = 1;
+  return thermo_reset(ctx);
+}
+
+thermo_status thermo_reset(thermo_ctx* ctx) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state < 1) return fail(ctx, THERMO_ESTATE, "register objects first");
+  const size_t n = ctx->reg.size();
+  CK(cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_instr, 0, (size_t)ctx->cfg.max_launches * n * 2 * 8, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_launch_ctr, 0, (size_t)ctx->cfg.max_launches * 2 * 8, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_pc_keys_tab, 0, (size_t)ctx->pc_cap * 8, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_pc_vals, 0xFF, (size_t)ctx->pc_cap * 4, ctx->stream));
+  ctx->n_keys = ctx->n_pckeys = 0;
+  ctx->records = 0;
+  ctx->state = 1;
+  ctx->hist_valid = false;
+  return THERMO_OK;
+}
+
+thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, size_t n) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state < 1) return fail(ctx, THERMO_ESTATE, "register objects first");
+  if (n == 0) return THERMO_OK;
+  if (!recs) return fail(ctx, THERMO_EINVAL, "recs is NULL");
+  if (reinterpret_cast<uintptr_t>(recs) & 15) return fail(ctx, THERMO_EINVAL, "recs must be 16-byte aligned");
+  cudaPointerAttributes attr;
+  bool on_device = false, pinned = false;
+  if (cudaPointerGetAttributes(&attr, recs) == cudaSuccess) {
+    on_device = attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+    pinned = attr.type == cudaMemoryTypeHost;
+  } else {
+    cudaGetLastError();
+  }
+  // worst case: every record emits two keys into each stream
+  st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * (ull)n + 64, ctx->n_keys);
+  if (st) return st;
+  if (ctx->cfg.track_pc) {
+    st = grow_keys(ctx, &ctx->d_pckeys, &ctx->pckeys_cap, ctx->n_pckeys + 2 * (ull)n + 64, ctx->n_pckeys);
+    if (st) return st;
+  }
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  if (on_device) {
+    st = decode_device(ctx, reinterpret_cast<const uint4*>(recs), n);
+    if (st) return st;
+  } else {
+    // staged host ingest: chunks split at explicit instruction heads, copy of
+    // chunk k+1 overlapped with decoding of chunk k
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(recs);
+    for (int i = 0; i < 2; ++i) {
+      if (!ctx->d_stage[i]) CK(dalloc(&ctx->d_stage[i], kHostChunk + 4096));
+      if (!pinned && !ctx->h_pinned[i]) CK(cudaHostAlloc(&ctx->h_pinned[i], (kHostChunk + 4096) * 16, 0));
+    }
+    ull pos = 0;
+    int k = 0;
+    while (pos < n) {
+      ull end = n;
+      if (pos + kHostChunk < n) {  // cut at the next explicit head (bounded look-ahead)
+        const ull lim = std::min<ull>(n, pos + kHostChunk + 4096);
+        ull e = pos + kHostChunk;
+        while (e < lim) {
+          uint32_t hiw;
+          std::memcpy(&hiw, src + e * 16 + 4, 4);
+          if ((hiw >> 23) & 1u) break;
+          ++e;
+        }
+        end = e < lim ? e : n;  // no head within reach: take the rest in one piece
+      }
+      const ull cnt = end - pos;
+      const int b = k & 1;
+      if (cnt > kHostChunk + 4096) {
+        // oversize tail (no instruction head in reach): one-off device buffer
+        uint4* tmp = nullptr;
+        CK(dalloc(&tmp, cnt));
+        CK(cudaMemcpyAsync(tmp, src + pos * 16, cnt * 16, cudaMemcpyHostToDevice, ctx->stream));
+        st = decode_device(ctx, tmp, cnt);
+        CK(cudaStreamSynchronize(ctx->stream));
+        dfree(tmp);
+        if (st) return st;
+        pos = end;
+        ++k;
+        continue;
+      }
+      CK(cudaEventSynchronize(ctx->ev_used[b]));  // staging buffer b free again
+      const void* hsrc = src + pos * 16;
+      if (!pinned) {
+        std::memcpy(ctx->h_pinned[b], hsrc, cnt * 16);
+        hsrc = ctx->h_pinned[b];
+      }
+      CK(cudaMemcpyAsync(ctx->d_stage[b], hsrc, cnt * 16, cudaMemcpyHostToDevice, ctx->copy_stream));
+      CK(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+      st = decode_device(ctx, ctx->d_stage[b], cnt);
+      if (st) return st;
+      CK(cudaEventRecord(ctx->ev_used[b], ctx->stream));
+      pos = end;
+      ++k;
+    }
+  }
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  st = sync_counts(ctx);
+  if (st) return st;
+  cudaEventElapsedTime(&ctx->ms_ingest, ctx->ev0, ctx->ev1);
+  if (on_device) cudaEventElapsedTime(&ctx->ms_phase[0], ctx->evp[6], ctx->evp[7]);
+  else ctx->ms_phase[0] = ctx->ms_ingest;
+  ctx->records += n;
+  ctx->state = 2;
+  ctx->hist_valid = false;
+  return THERMO_OK;
+}
+
+thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32_t launch_filter) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state < 2) return fail(ctx, THERMO_ESTATE, "ingest a trace before build");
+  if (g < THERMO_WORD || g > THERMO_BOTH) return fail(ctx, THERMO_EINVAL, "bad granularity");
+  if (launch_filter != THERMO_ALL_LAUNCHES && launch_filter >= ctx->cfg.max_launches)
+    return fail(ctx, THERMO_EINVAL, "launch_filter beyond max_launches");
+  DevCounters hc;
+  CK(cudaMemcpyAsync(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hc.out_of_range) return fail(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths");
+  if (ctx->cfg.track_pc && hc.pc_overflow) return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs");
+  const size_t n = ctx->reg.size();
+  cudaStream_t s = ctx->stream;
+  CK(cudaEventRecord(ctx->ev0, s));
+  const ull l0 = ctx->launches;
+  CK(cudaMemsetAsync(ctx->d_wc, 0, 8 * ctx->S_tot * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->d_sc, 0, ctx->S_tot * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
+  CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
+  CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
+  uint32_t mode = ctx->cfg.dedup == THERMO_DEDUP_AUTO ? THERMO_DEDUP_SORT : ctx->cfg.dedup;
+  ctx->dedup_used = mode;
+  const KeyLayout kl = ctx->kl;
+  cudaError_t e = cudaSuccess;
+  // ---- main keys: a4 dedup + a5 count ----
+  if (mode == THERMO_DEDUP_SORT) {
+    CK(cudaEventRecord(ctx->evp[0], s));
+    ull* sorted = radix_sort_keys(ctx->d_keys, ctx->n_keys, 8, kl.S + kl.L + kl.W, ctx->sw, ctx->num_sms, s, &e);
+    CK(cudaEventRecord(ctx->evp[1], s));
+    if (e) return fail(ctx, THERMO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
+    if (sorted != ctx->d_keys) {  // keep the sorted copy as the retained keys
+      std::swap(ctx->d_keys, ctx->sw.alt);
+      std::swap(ctx->keys_cap, ctx->sw.alt_cap);
+    }
+    launch_count_sorted(ctx->d_keys, ctx->n_keys, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
+    ctx->launches += 1;
+  } else {
+    ull cap = next_pow2(std::max<ull>(1024, 2 * ctx->n_keys));
+    if (ctx->table_cap < cap) {
+      dfree(ctx->d_table);
+      ctx->table_cap = cap;
+      CK(dalloc(&ctx->d_table, cap));
+    }
+    CK(cudaEventRecord(ctx->evp[0], s));
+    CK(cudaMemsetAsync(ctx->d_table, 0xFF, cap * 8, s));
+    launch_hash_insert(ctx->d_keys, ctx->n_keys, ctx->d_table, cap - 1, ctx->d_ctr, ctx->num_sms, s);
+    CK(cudaEventRecord(ctx->evp[1], s));
+    ctx->launches += 2;
+    launch_count_hash(ctx->d_table, cap, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evp[2], s));
+  // ---- a6 histograms ----
+  launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->num_sms, s);
+  ctx->launches += 1;
+  CK(cudaEventRecord(ctx->evp[3], s));
+  if (ctx->cfg.track_pc) {
+    if (mode == THERMO_DEDUP_SORT) {
+      ull* sorted = radix_sort_keys(ctx->d_pckeys, ctx->n_pckeys, 8, kl.P + kl.S, ctx->swpc, ctx->num_sms, s, &e);
+      if (e) return fail(ctx, THERMO_ECUDA, std::string("radix sort (pc): ") + cudaGetErrorString(e));
+      if (sorted != ctx->d_pckeys) {
+        std::swap(ctx->d_pckeys, ctx->swpc.alt);
+        std::swap(ctx->pckeys_cap, ctx->swpc.alt_cap);
+      }
+      ctx->launches += 1;
+      launch_pc_hist_sorted(ctx->d_pckeys, ctx->n_pckeys, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
+                            ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
+    } else {
+      ull cap = next_pow2(std::max<ull>(1024, 2 * ctx->n_pckeys));
+      if (ctx->pctable_cap < cap) {
+        dfree(ctx->d_pctable);
+        ctx->pctable_cap = cap;
+        CK(dalloc(&ctx->d_pctable, cap));
+      }
+      CK(cudaMemsetAsync(ctx->d_pctable, 0xFF, cap * 8, s));
+      launch_hash_insert(ctx->d_pckeys, ctx->n_pckeys, ctx->d_pctable, cap - 1, ctx->d_ctr, ctx->num_sms, s);
+      ctx->launches += 2;
+      launch_pc_hist_hash(ctx->d_pctable, cap, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
+                          ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evp[4], s));
+  CK(cudaEventRecord(ctx->ev1, s));
+  CK(cudaEventSynchronize(ctx->ev1));
+  cudaEventElapsedTime(&ctx->ms_build, ctx->ev0, ctx->ev1);
+  for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ctx->ms_phase[1 + i], ctx->evp[i], ctx->evp[i + 1]);
+  ctx->launches += ctx->sw.launches + ctx->swpc.launches;
+  ctx->sw.launches = ctx->swpc.launches = 0;
+  (void)l0;
+  DevCounters hc2;
+  CK(cudaMemcpy(&hc2, ctx->d_ctr, sizeof hc2, cudaMemcpyDeviceToHost));
+  if (hc2.hash_fail) return fail(ctx, THERMO_ECUDA, "hash table overflow");
+  ctx->built_filter = launch_filter;
+  ctx->built_gran = g;
+  ctx->state = 3;
+  ctx->hist_valid = true;
+  return THERMO_OK;
+}
+
+thermo_status thermo_query_heatmap(thermo_ctx* ctx, uint32_t object_id, thermo_granularity g, uint32_t* out,
+                                   size_t cap, size_t* n_out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
+  auto it = ctx->id_to_reg.find(object_id);
+  if (it == ctx->id_to_reg.end()) return fail(ctx, THERMO_EINVAL, "unknown object id");
+  const uint32_t j = ctx->reg_to_sorted[it->second];
+  const ull nw = ctx->h_nwords[j], ns = ctx->h_soff[j + 1] - ctx->h_soff[j], so = ctx->h_soff[j];
+  size_t need = g == THERMO_WORD ? nw : g == THERMO_SECTOR ? ns : 9 * ns;
+  if (n_out) *n_out = need;
+  if (!out || cap < need) return fail(ctx, THERMO_ERANGE, "output capacity too small");
+  if (g == THERMO_WORD) {
+    CK(cudaMemcpy(out, ctx->d_wc + 8 * so, nw * 4, cudaMemcpyDeviceToHost));
+  } else if (g == THERMO_SECTOR) {
+    CK(cudaMemcpy(out, ctx->d_sc + so, ns * 4, cudaMemcpyDeviceToHost));
+  } else {
+    CK(cudaMemcpy2D(out, 9 * 4, ctx->d_wc + 8 * so, 8 * 4, 8 * 4, ns, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy2D(out + 8, 9 * 4, ctx->d_sc + so, 4, 4, ns, cudaMemcpyDeviceToHost));
+    for (ull s2 = 0; s2 < ns; ++s2)
+      for (int b = 0; b < 8; ++b)
+        if (8 * s2 + b >= nw) out[9 * s2 + b] = 0;
+  }
+  return THERMO_OK;
+}
+
+thermo_status thermo_query_histogram(thermo_ctx* ctx, uint32_t object_id, thermo_granularity g,
+                                     uint64_t hist[THERMO_LEVELS]) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
+  if (g != THERMO_WORD && g != THERMO_SECTOR) return fail(ctx, THERMO_EINVAL, "granularity must be WORD or SECTOR");
+  auto it = ctx->id_to_reg.find(object_id);
+  if (it == ctx->id_to_reg.end()) return fail(ctx, THERMO_EINVAL, "unknown object id");
+  const uint32_t j = ctx->reg_to_sorted[it->second];
+  const size_t off = ((size_t)j * 2 + (g == THERMO_SECTOR ? 1 : 0)) * kLevels;
+  CK(cudaMemcpy(hist, ctx->d_hist + off, kLevels * 8, cudaMemcpyDeviceToHost));
+  return THERMO_OK;
+}
+
+thermo_status thermo_query_per_pc(thermo_ctx* ctx, thermo_granularity g, thermo_pc_hist* out, size_t cap,
+                                  size_t* n_out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
+  if (!ctx->cfg.track_pc) return fail(ctx, THERMO_ESTATE, "context created with track_pc = 0");
+  if (g != THERMO_WORD && g != THERMO_SECTOR) return fail(ctx, THERMO_EINVAL, "granularity must be WORD or SECTOR");
+  DevCounters hc;
+  CK(cudaMemcpy(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost));
+  const ull npc = std::min<ull>(hc.pc_count, ctx->cfg.max_pcs);
+  std::vector<uint32_t> site(npc);
+  std::vector<ull> hist(npc * 2 * kLevels);
+  if (npc) {
+    CK(cudaMemcpy(site.data(), ctx->d_site_of, npc * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hist.data(), ctx->d_pchist, npc * 2 * kLevels * 8, cudaMemcpyDeviceToHost));
+  }
+  std::vector<uint32_t> ids;
+  for (uint32_t i = 0; i < npc; ++i)
+    if (ctx->built_filter == THERMO_ALL_LAUNCHES || (site[i] >> 20) == ctx->built_filter) ids.push_back(i);
+  std::sort(ids.begin(), ids.end(), [&](uint32_t a, uint32_t b) { return site[a] < site[b]; });
+  if (n_out) *n_out = ids.size();
+  if (!out || cap < ids.size()) return fail(ctx, THERMO_ERANGE, "output capacity too small");
+  for (size_t k = 0; k < ids.size(); ++k) {
+    const uint32_t i = ids[k];
+    out[k].launch = site[i] >> 20;
+    out[k].pc = (site[i] & 0xFFFFFu) << 4;
+    const size_t off = ((size_t)i * 2 + (g == THERMO_SECTOR ? 1 : 0)) * kLevels;
+    std::memcpy(out[k].hist, hist.data() + off, kLevels * 8);
+  }
+  return THERMO_OK;
+}
+
+thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, thermo_indicators* out, size_t cap,
+                              size_t* n_out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
+  const size_t n = ctx->reg.size();
+  if (n_out) *n_out = n;
+  if (!out || cap < n) return fail(ctx, THERMO_ERANGE, "output capacity too small");
+  thermo_params p;
+  if (params) p = *params; else thermo_default_params(&p);
+  if (!p.alpha_den || !p.beta_den || !p.smem_cov_den || !p.gamma_den || !p.dom_den || !p.hot_frac_den ||
+      !p.fs_frac_den || !p.mis_frac_den || !p.cv_den)
+    return fail(ctx, THERMO_EINVAL, "zero denominator in params");
+  cudaStream_t s = ctx->stream;
+  CK(cudaEventRecord(ctx->ev0, s));
+  CK(cudaMemsetAsync(ctx->d_ind, 0, n * kIndFields * 8, s));
+  IndicatorArgs a{};
+  a.word_cnt = ctx->d_wc;
+  a.sector_cnt = ctx->d_sc;
+  a.obj = obj_table(ctx);
+  a.obj_nwords = ctx->d_nwords;
+  a.obj_space = ctx->d_space;
+  a.tile_obj = ctx->d_tile_obj;
+  a.tile_first = ctx->d_tile_first;
+  a.tile_end = ctx->d_tile_end;
+  a.n_tiles = ctx->n_tiles;
+  a.instr_ctr = ctx->d_instr;
+  a.max_launches = ctx->cfg.max_launches;
+  a.launch_filter = ctx->built_filter;
+  a.prm = p;
+  a.ind = ctx->d_ind;
+  a.tile_info = ctx->d_tile_info;
+  a.tile_prev = ctx->d_tile_prev;
+  launch_indicators(a, ctx->num_sms, s);
+  ctx->launches += ctx->n_tiles ? 4 : 2;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev1, s));
+  std::vector<ull> ind(n * kIndFields);
+  CK(cudaMemcpyAsync(ind.data(), ctx->d_ind, n * kIndFields * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&ctx->ms_classify, ctx->ev0, ctx->ev1);
+  ctx->ms_phase[5] = ctx->ms_classify;
+  for (size_t r = 0; r < n; ++r) {
+    const ull* v = ind.data() + ctx->reg_to_sorted[r] * kIndFields;
+    thermo_indicators& o = out[r];
+    o.object_id = ctx->reg[r].id;
+    o.labels = (uint32_t)v[F_LABELS];
+    o.n_words = v[F_NWORDS]; o.n_sectors = v[F_NSECTORS];
+    o.touched_sectors = v[F_T]; o.touched_words = v[F_TW];
+    o.hot_sectors = v[F_HOT]; o.fs_sectors = v[F_FS];
+    o.sum_x = v[F_SUMX]; o.sum_x2_lo = v[F_SUMX2_LO]; o.sum_x2_hi = v[F_SUMX2_HI];
+    o.le1_words = v[F_LE1]; o.max_sector_count = v[F_MAXSEC];
+    o.instrs = v[F_INSTRS]; o.misaligned_instrs = v[F_MIS];
+    o.gaps = v[F_GAPS]; o.dom_gap = v[F_DOMGAP]; o.dom_count = v[F_DOMCNT];
+  }
+  return THERMO_OK;
+}
+
+thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (!out) return THERMO_EINVAL;
+  std::memset(out, 0, sizeof *out);
+  DevCounters hc;
+  CK(cudaMemcpyAsync(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<ull> lc;
+  if (ctx->state >= 1) {
+    lc.resize((size_t)ctx->cfg.max_launches * 2);
+    CK(cudaMemcpyAsync(lc.data(), ctx->d_launch_ctr, lc.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  out->records = ctx->records;
+  out->invalid = hc.invalid;
+  out->out_of_range = hc.out_of_range;
+  for (uint32_t la = 0; la < ctx->cfg.max_launches && !lc.empty(); ++la) {
+    if (ctx->state == 3 && ctx->built_filter != THERMO_ALL_LAUNCHES && la != ctx->built_filter) continue;
+    out->unmapped_words += lc[2 * la];
+    out->mapped_word_accesses += lc[2 * la + 1];
+  }
+  out->keys_emitted = hc.n_keys;
+  out->pc_keys_emitted = hc.n_pckeys;
+  out->distinct_pairs = hc.distinct_pairs;
+  out->distinct_pc_pairs = hc.distinct_pc;
+  out->n_pcs = hc.pc_count;
+  out->dedup_used = ctx->dedup_used;
+  out->ms_ingest = ctx->ms_ingest;
+  out->ms_build = ctx->ms_build;
+  out->ms_classify = ctx->ms_classify;
+  out->ms_decode = ctx->ms_phase[0];
+  out->ms_dedup = ctx->ms_phase[1];
+  out->ms_count = ctx->ms_phase[2];
+  out->ms_hist = ctx->ms_phase[3];
+  out->ms_pc = ctx->ms_phase[4];
+  out->ms_indicators = ctx->ms_phase[5];
+  out->kernel_launches = ctx->launches;
+  return THERMO_OK;
+}
+
+const char* thermo_last_error(const thermo_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

@@ -1,0 +1,147 @@
+// thermo_internal.cuh -- shared declarations of libthermo's CUDA implementation.
+//
+// Citation keys: P:n = PAPER.md line n; S:n = SPEC.md line n; G# = DESIGN.md
+// "Readings".  Nothing in this directory includes or links anything under
+// oracle/ (the test oracle); the two share no code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/thermo.h"
+
+namespace thermo {
+
+typedef unsigned long long ull;
+
+constexpr int kLevels = THERMO_LEVELS;
+constexpr ull kEmptyKey = ~0ull;  // sentinel key (prefix all-ones is reserved)
+constexpr uint32_t kPcNone = 0xFFFFFFFFu;
+
+// ---- device-resident counters (one struct per context) -------------------
+struct DevCounters {
+  ull n_keys;          // main keys emitted (after pre-dedup)
+  ull n_pckeys;        // pc keys emitted
+  ull invalid;         // invalid records
+  ull out_of_range;    // launch/warp beyond the declared widths
+  ull pc_count;        // distinct (launch, pc) pairs assigned an id
+  ull pc_overflow;     // (launch, pc) pairs beyond max_pcs
+  ull distinct_pairs;  // set by the count kernels
+  ull distinct_pc;     // set by the per-pc kernel
+  ull hash_fail;       // hash-table insert failures (probe limit)
+  ull pad[7];
+};
+
+// ---- object table in device memory, sorted by (space << 48 | base) -------
+struct ObjTable {
+  const ull* lo;    // space << 48 | base           [n]
+  const ull* hi;    // lo + len                     [n]
+  const ull* soff;  // first global sector index    [n + 1]
+  uint32_t n;
+};
+
+// ---- (launch, pc) -> dense pc id map (open addressing, global memory) ----
+struct PcMap {
+  ull* keys;         // site + 1 (0 = empty)      [cap]
+  uint32_t* vals;    // pc id, kPcNone = pending   [cap]
+  uint32_t* site_of; // pc id -> site              [max_pcs]
+  uint32_t cap_mask;
+  uint32_t max_pcs;
+};
+
+// ---- key layout -----------------------------------------------------------
+// main key:  [ g : S ][ launch : L ][ warp : W ][ mask : 8 ]   (S+L+W <= 56)
+// pc key:    [ pcid : P ][ g : S ][ mask : 8 ]                  (P+S <= 56)
+struct KeyLayout {
+  uint32_t S, L, W, P;
+};
+
+struct DecodeArgs {
+  const uint4* recs;
+  ull n;                  // records in this ingest call
+  const ull* heads;       // [n_ranges + 1] range boundaries (explicit heads)
+  uint32_t n_ranges;
+  ObjTable obj;
+  KeyLayout kl;
+  uint32_t max_launches, max_warps;
+  int track_pc;
+  PcMap pcmap;
+  ull* keys;              // main key buffer (append)
+  ull* pckeys;            // pc key buffer (append)
+  DevCounters* ctr;
+  ull* instr_ctr;         // [max_launches * n_obj * 2] (instrs, misaligned)
+  ull* launch_ctr;        // [max_launches * 2] (unmapped words, mapped word accesses)
+};
+
+// ---- kernels (launch wrappers live in the .cu files) ----------------------
+void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_ranges, ull* heads,
+                       cudaStream_t s);
+void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
+
+// onesweep LSD radix sort of u64 keys on bits [lo_bit, lo_bit + nbits)
+struct SortWorkspace {
+  ull* alt = nullptr;        size_t alt_cap = 0;
+  ull* status = nullptr;     size_t status_cap = 0;   // tiles * 256
+  uint32_t* hist = nullptr;  // [8 * 256] digit histograms
+  uint32_t* counters = nullptr;  // [8] tile counters
+  uint32_t epoch = 0;
+  ull launches = 0;  // kernels launched (for stats)
+};
+// returns pointer to the sorted keys (either keys or ws.alt)
+ull* radix_sort_keys(ull* keys, ull n, int lo_bit, int nbits, SortWorkspace& ws, int num_sms,
+                     cudaStream_t s, cudaError_t* err);
+
+// hash-set dedup: insert keys (prefix<<8 | mask) into table; EMPTY = ~0
+void launch_hash_insert(const ull* keys, ull n, ull* table, ull cap_mask, DevCounters* ctr, int num_sms,
+                        cudaStream_t s);
+
+// segmented count (a5) -> dense arrays
+void launch_count_sorted(const ull* keys, ull n, KeyLayout kl, uint32_t launch_filter, uint32_t* word_cnt,
+                         uint32_t* sector_cnt, DevCounters* ctr, int num_sms, cudaStream_t s);
+void launch_count_hash(const ull* table, ull cap, KeyLayout kl, uint32_t launch_filter, uint32_t* word_cnt,
+                       uint32_t* sector_cnt, DevCounters* ctr, int num_sms, cudaStream_t s);
+
+// a6 histograms over dense arrays, per object
+void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj,
+                        const ull* obj_nwords, ull* hist /*[n_obj][2][33]*/, ull total_sectors,
+                        int num_sms, cudaStream_t s);
+// a6 per-pc histograms from deduped pc keys
+void launch_pc_hist_sorted(const ull* pckeys, ull n, KeyLayout kl, const uint32_t* site_of,
+                           uint32_t launch_filter, const uint32_t* word_cnt, const uint32_t* sector_cnt,
+                           ull* pc_hist /*[max_pcs][2][33]*/, DevCounters* ctr, int num_sms, cudaStream_t s);
+void launch_pc_hist_hash(const ull* table, ull cap, KeyLayout kl, const uint32_t* site_of,
+                         uint32_t launch_filter, const uint32_t* word_cnt, const uint32_t* sector_cnt,
+                         ull* pc_hist, DevCounters* ctr, int num_sms, cudaStream_t s);
+
+// a7 indicators
+struct IndicatorArgs {
+  const uint32_t* word_cnt;
+  const uint32_t* sector_cnt;
+  ObjTable obj;
+  const ull* obj_nwords;     // [n]
+  const uint32_t* obj_space; // [n]
+  const ull* tile_obj;       // [n_tiles] object of tile
+  const ull* tile_first;     // [n_tiles] first sector (global) of tile
+  const ull* tile_end;       // [n_tiles] end sector (global, exclusive)
+  uint32_t n_tiles;
+  const ull* instr_ctr;      // [max_launches * n * 2]
+  uint32_t max_launches, launch_filter;
+  thermo_params prm;
+  ull* ind;                  // [n][kIndFields] accumulators
+  ull* tile_info;            // [n_tiles][4] first touched, last touched, cand, cnt
+  ull* tile_prev;            // [n_tiles] last touched word before the tile (or ~0)
+};
+constexpr int kIndFields = 24;
+enum IndField {
+  F_NWORDS, F_NSECTORS, F_T, F_TW, F_HOT, F_FS, F_SUMX, F_SUMX2_LO, F_SUMX2_HI, F_LE1, F_MAXSEC,
+  F_INSTRS, F_MIS, F_GAPS, F_DOMGAP, F_DOMCNT, F_LABELS, F_CAND, F_CANDCNT, F_VERIFY, F_PAD0,
+  F_PAD1, F_PAD2, F_PAD3
+};
+void launch_indicators(const IndicatorArgs& a, int num_sms, cudaStream_t s);
+
+}  // namespace thermo

@@ -82,7 +82,11 @@ def brute_instructions(objects, records, calls=None):
     bounds = calls or [(0, n)]
     out = {}
     for lo, hi in bounds:
-        heads = [i for i in range(lo, hi) if i == lo or f["istart"][i]]
+        heads, last = [], None
+        for i in range(lo, hi):   # explicit heads, plus a split every 32 records (G24)
+            if i == lo or f["istart"][i] or i - last == 32:
+                heads.append(i)
+                last = i
         heads.append(hi)
         for h0, h1 in zip(heads[:-1], heads[1:]):
             idx = [i for i in range(h0, h1) if f["valid"][i]]

@@ -1,0 +1,177 @@
+"""GPU parity: libthermo (through its C ABI) against the CPU oracle, element by
+element, bit-exact (all outputs are integers; BJ north_star "must match the
+oracle bit-exactly").  Sizes span several decode ranges / sort tiles with
+ragged tails; full-size configs are checked on sampled sectors and closed forms.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tracegen as tg
+
+pytestmark = pytest.mark.gpu
+
+WORD, SECTOR, BOTH = 1, 2, 3
+
+
+def gpu_ctx(t, dedup=0, max_launches=None, track_pc=True):
+    from paper_2507_18729_b200 import Thermo
+    ml = max_launches or max(1, int(t.meta.get("launches", 1)))
+    th = Thermo(max_launches=ml, max_warps_per_launch=1 << 22, max_pcs=4096, dedup=dedup, track_pc=track_pc)
+    th.register_objects(t.objects)
+    return th
+
+
+def run_both(t, calls=None, dedup=0, launch_filter=oracle.ALL_LAUNCHES, max_launches=None, host=False):
+    calls = calls if calls is not None else t.calls()
+    orc = oracle.run([o[:4] for o in t.objects], calls, launch_filter)
+    th = gpu_ctx(t, dedup, max_launches)
+    for c in calls:
+        th.ingest(c.contiguous() if host else c.cuda().contiguous())
+    th.build(BOTH, launch_filter)
+    return orc, th
+
+
+def compare(orc, th, t, check_pc=True, check_ind=True):
+    for k, obj in enumerate(t.objects):
+        oid = obj[3]
+        w, s = th.heatmap(oid, WORD), th.heatmap(oid, SECTOR)
+        ow, os_ = orc.word_counts(k), orc.sector_counts(k)
+        assert np.array_equal(w, ow), (t.name, obj[4], "word", np.nonzero(w != ow)[0][:10])
+        assert np.array_equal(s, os_), (t.name, obj[4], "sector", np.nonzero(s != os_)[0][:10])
+        assert np.array_equal(th.histogram(oid, WORD), orc.hist(k, False)), (t.name, obj[4])
+        assert np.array_equal(th.histogram(oid, SECTOR), orc.hist(k, True)), (t.name, obj[4])
+        both = th.heatmap(oid, BOTH).reshape(-1, 9)
+        assert np.array_equal(both[:, 8], os_)
+    if check_pc:
+        rows = orc.per_pc()
+        gw, gs = th.per_pc(WORD), th.per_pc(SECTOR)
+        assert [(r[0], r[1]) for r in rows] == [(r[0], r[1]) for r in gw] == [(r[0], r[1]) for r in gs]
+        for r, a, b in zip(rows, gw, gs):
+            assert np.array_equal(r[2], a[2]), (t.name, hex(r[1]))
+            assert np.array_equal(r[3], b[2]), (t.name, hex(r[1]))
+    if check_ind:
+        oi, gi = orc.classify(), th.classify()
+        for k, (a, b) in enumerate(zip(oi, gi)):
+            for f, v in a.items():
+                assert b[f] == v, (t.name, t.objects[k][4], f, v, b[f])
+    st, ost = th.stats(), orc.stats()
+    for f in ("records", "invalid", "unmapped_words", "mapped_word_accesses"):
+        assert st[f] == ost[f], (f, st[f], ost[f])
+
+
+SMALL = [
+    lambda: tg.tiny("A"), lambda: tg.tiny("B"), lambda: tg.fig3("a"), lambda: tg.fig3("b"),
+    lambda: tg.fig6(3, 16), lambda: tg.fig6(8, 0), lambda: tg.gemm(64, 64, 16, "v00"),
+    lambda: tg.gemm(128, 96, 40, "v01"), lambda: tg.stencil(96), lambda: tg.spmv(10, 8),
+    lambda: tg.strided_gather(64, 1024, 3), lambda: tg.smem_thread_local(), lambda: tg.smem_warp_broadcast(),
+]
+
+
+@pytest.mark.parametrize("dedup", [1, 2])
+@pytest.mark.parametrize("i", range(len(SMALL)))
+def test_small_workloads(i, dedup):
+    t = SMALL[i]()
+    orc, th = run_both(t, dedup=dedup)
+    compare(orc, th, t)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+@pytest.mark.parametrize("dedup", [1, 2])
+def test_random_traces(seed, dedup):
+    """Unaligned/straddling sizes, unmapped and invalid records, 3 launches,
+    shared-space objects, instructions of 1..40 records (split at 32)."""
+    t = tg.random_trace(n=30000 + 777 * seed, seed=seed, n_warps=300, n_launches=3)
+    t.meta["launches"] = 3
+    calls = [t.records[a:b] for a, b in tg.split_calls(t.n, t.records, 3)]
+    for lf in (oracle.ALL_LAUNCHES, 2):
+        orc, th = run_both(t, calls=calls, dedup=dedup, launch_filter=lf)
+        compare(orc, th, t)
+
+
+def test_launch_filter_rebuild_and_host_ingest():
+    t = tg.random_trace(n=20000, seed=21, n_launches=4)
+    t.meta["launches"] = 4
+    orc, th = run_both(t, host=True)       # host-pointer ingest (staged by the library)
+    compare(orc, th, t)
+    for lf in range(4):                     # build again from the retained keys
+        th.build(BOTH, lf)
+        o2 = oracle.run([o[:4] for o in t.objects], t.calls(), lf)
+        compare(o2, th, t)
+
+
+def test_permutation_and_duplication_invariance():
+    t = tg.gemm(64, 64, 24, "v00")
+    perm = tg.shuffle_instructions(t.records, 7)
+    dup = torch.cat([t.records, perm])
+    ref = None
+    for calls in ([t.records], [perm], [dup], [t.records[a:b] for a, b in tg.split_calls(t.n, t.records, 6)]):
+        th = gpu_ctx(t)
+        for c in calls:
+            th.ingest(c.cuda().contiguous())
+        th.build()
+        out = [th.heatmap(o[3], BOTH) for o in t.objects]
+        if ref is None:
+            ref = out
+        for a, b in zip(ref, out):
+            assert np.array_equal(a, b)
+
+
+def test_empty_and_degenerate():
+    from paper_2507_18729_b200 import Thermo, ThermoError
+    t = tg.tiny("B")
+    th = gpu_ctx(t)
+    th.ingest(t.records[:0].cuda())        # empty call is a no-op
+    with pytest.raises(ThermoError):        # nothing ingested yet
+        th.build()
+    th.ingest(t.records[:1].cuda())         # a single record
+    th.build()
+    w = th.heatmap(0, WORD)
+    assert w[0] == 1 and w.sum() == 1
+    with pytest.raises(ThermoError):
+        th.register_objects(t.objects)      # second registration
+    th2 = Thermo()
+    with pytest.raises(ThermoError):
+        th2.register_objects([(0x1010, 64, 0, 0)])  # misaligned base
+    th3 = Thermo()
+    with pytest.raises(ThermoError):
+        th3.register_objects([(0x1000, 64, 0, 0), (0x1020, 64, 0, 1)])  # overlap
+    # out-of-range warp id -> ERANGE at build
+    th4 = Thermo(max_warps_per_launch=4)
+    th4.register_objects(t.objects)
+    th4.ingest(t.records.cuda())
+    with pytest.raises(ThermoError):
+        th4.build()
+
+
+def test_gemm_full_size_closed_form_and_sample():
+    """BJ configs[1] at full size (270,532,608 records) in the bench's launch
+    configuration: closed forms on every cell, oracle on sampled sectors."""
+    t = tg.gemm(1024, 1024, 128, "v00", device="cuda")
+    th = gpu_ctx(t)
+    th.ingest(t.records)
+    th.build()
+    wa, sa = th.heatmap(0, WORD), th.heatmap(0, SECTOR)
+    assert (wa == 1024).all() and (sa == 1024).all()
+    assert (th.heatmap(1, WORD) == 32).all() and (th.heatmap(1, SECTOR) == 256).all()
+    assert (th.heatmap(2, WORD) == 1).all() and (th.heatmap(2, SECTOR) == 8).all()
+    labels = [oracle.label_names(r["labels"]) for r in th.classify()]
+    assert labels == [["Hot"], ["FalseSharing"], ["FalseSharing"]]
+    st = th.stats()
+    assert st["records"] == 270532608 and st["distinct_pairs"] == 22020096
+    # oracle on a sample of sectors (restricted mode over the full trace)
+    rng = np.random.default_rng(5)
+    oi = np.repeat(np.arange(3), 20)
+    se = np.concatenate([rng.choice((o[1] + 31) // 32, 20, replace=False) for o in t.objects])
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.restrict(oi, se)
+    recs = t.records.cpu()
+    del t
+    for a in range(0, recs.shape[0], 1 << 25):
+        orc.ingest(recs[a:a + (1 << 25)])
+    orc.build()
+    ref = orc.sample(oi, se)
+    for row, o, s in zip(ref, oi, se):
+        b = th.heatmap(int(o), BOTH).reshape(-1, 9)[s]
+        assert np.array_equal(b, row), (o, s)

@@ -112,7 +112,7 @@ def fig6(n_warps: int = 2, offset: int = 16, device="cpu") -> Trace:
 # --------------------------------------------------------------------------
 # gemm_v00 / gemm_v01 (Listing 1; block 32x32)
 # --------------------------------------------------------------------------
-def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 26) -> Trace:
+def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 26, warp_limit=None) -> Trace:
     """Naive SGEMM trace, one C element per thread, fp32 row-major.
 
     v00: C_row = bx*32 + tx, C_col = by*32 + ty (Listing 1).  v01 swaps them
@@ -128,6 +128,8 @@ def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 
                (baseC, 4 * M * N, SPACE_GLOBAL, 2, "C")]
     gdx = M // 32 if variant == "v00" else N // 32
     n_warps = (M // 32) * (N // 32) * 32
+    if warp_limit is not None:  # prefix of the trace (first warp_limit warps)
+        n_warps = min(n_warps, warp_limit)
     ipw = 2 * K + 2                       # instructions per warp
     n_rec = n_warps * ipw * 32
     out = torch.empty((n_rec, 4), dtype=torch.int32, device=dev)
