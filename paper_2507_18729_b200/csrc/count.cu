@@ -237,6 +237,7 @@ __device__ __forceinline__ void pc_contrib(ull pre, uint32_t m, bool head, KeyLa
   bool ok = head;
   if (ok && filter != THERMO_ALL_LAUNCHES) ok = (site_of[pcid] >> 20) == filter;
   distinct += ok ? 1 : 0;
+  if (!__any_sync(CFULL, ok)) return;  // warp-uniform: nothing to add
   // sector bin then word bins, each aggregated across the warp
   {
     const uint32_t bin = ok ? (pcid * 2 + 1) * kLevels + level_of(sc[g]) : 0xFFFFFFFFu;

@@ -74,7 +74,7 @@ __global__ void sort_scan_kernel(uint32_t* hist, int passes) {
 }
 
 // ---- one digit pass ----------------------------------------------------------
-__global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const ull* __restrict__ in, ull* __restrict__ out,
+__global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(const ull* __restrict__ in, ull* __restrict__ out,
                                                                 ull n, int shift,
                                                                 const uint32_t* __restrict__ gofs,
                                                                 ull* __restrict__ status,
@@ -106,12 +106,7 @@ __global__ void __launch_bounds__(kSortThreads) onesweep_kernel(const ull* __res
     ull idx = wbase + (ull)r * 32 + lane;
     const bool valid = idx < n;
     const uint32_t d = (uint32_t)(k[r] >> shift) & 255u;
-    unsigned peers = __ballot_sync(SFULL, valid);
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      unsigned bb = __ballot_sync(SFULL, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bb : ~bb;
-    }
+    const unsigned peers = __match_any_sync(SFULL, valid ? d : 0x100u + lane);
     uint32_t old = 0;
     const int leader = __ffs(peers) - 1;
     if (valid && lane == leader) old = whist[w][d];

@@ -568,7 +568,10 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   ctx->launches += 1;
   CK(cudaEventRecord(ctx->evp[3], s));
   if (ctx->cfg.track_pc) {
-    if (mode == THERMO_DEDUP_SORT) {
+    // the pc stream defaults to the hash path: its distinct set is bounded by
+    // n_pcs * S_tot, usually small enough for an L2-resident table
+    const uint32_t pc_mode = ctx->cfg.dedup == THERMO_DEDUP_SORT ? THERMO_DEDUP_SORT : THERMO_DEDUP_HASH;
+    if (pc_mode == THERMO_DEDUP_SORT) {
       ull* sorted = radix_sort_keys(ctx->d_pckeys, ctx->n_pckeys, 8, kl.P + kl.S, ctx->swpc, ctx->num_sms, s, &e);
       if (e) return fail(ctx, THERMO_ECUDA, std::string("radix sort (pc): ") + cudaGetErrorString(e));
       if (sorted != ctx->d_pckeys) {
@@ -579,7 +582,8 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       launch_pc_hist_sorted(ctx->d_pckeys, ctx->n_pckeys, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
                             ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
     } else {
-      ull cap = next_pow2(std::max<ull>(1024, 2 * ctx->n_pckeys));
+      const ull bound = std::min<ull>(ctx->n_pckeys, std::max<ull>(1, hc.pc_count) * ctx->S_tot);
+      ull cap = next_pow2(std::max<ull>(1024, 2 * bound));
       if (ctx->pctable_cap < cap) {
         dfree(ctx->d_pctable);
         ctx->pctable_cap = cap;
