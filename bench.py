@@ -160,7 +160,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="sgemm")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash"])
+    ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash", "segment"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -180,7 +180,7 @@ def main():
     t = make_trace(args.workload, str(dev), rank)
     n = t.n
     stream = torch.cuda.current_stream(dev)
-    dedup = {"auto": 0, "sort": 1, "hash": 2}[args.dedup]
+    dedup = {"auto": 0, "sort": 1, "hash": 2, "segment": 3}[args.dedup]
     th = Thermo(device=local, stream=stream.cuda_stream, max_launches=max(1, int(t.meta.get("launches", 1))),
                 max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), dedup=dedup)
     th.register_objects(t.objects)
@@ -267,7 +267,7 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": args.workload, "records": n, "objects": len(t.objects),
-                       "dedup": {1: "sort", 2: "hash"}.get(st["dedup_used"], "?"),
+                       "dedup": {1: "sort", 2: "hash", 3: "segment"}.get(st["dedup_used"], "?"),
                        "l2": "inputs larger than L2 (16 B x records >> 126 MB), no flush",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single"},
             "roofline": roof, "pipeline_roofline": pipe, "phase_ms": ph_mean, "dominant_phase": dominant,

@@ -94,7 +94,15 @@ typedef enum {
   THERMO_ENCCL = -6    /* NCCL error (sticky)                              */
 } thermo_status;
 
-typedef enum { THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2 } thermo_dedup;
+/* dedup paths for the main (sector, launch, warp) keys (a4):
+ *   SORT     onesweep LSD radix sort on all key bits
+ *   HASH     open-addressing hash set in HBM
+ *   SEGMENT  counting sort by sector + per-chunk shared-memory dedup (falls
+ *            back to SORT when one sector holds more keys than a chunk)
+ *   AUTO     SEGMENT (chosen by measurement) */
+typedef enum {
+  THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2, THERMO_DEDUP_SEGMENT = 3
+} thermo_dedup;
 
 /*
  * Context configuration.  max_launches / max_warps_per_launch fix the bit
@@ -172,7 +180,7 @@ typedef struct {
   uint64_t distinct_pairs;     /* distinct (sector, launch, warp) = sum of sector counts */
   uint64_t distinct_pc_pairs;  /* distinct (launch, pc, sector)                */
   uint64_t n_pcs;              /* distinct (launch, pc) pairs seen             */
-  uint32_t dedup_used;         /* THERMO_DEDUP_SORT or THERMO_DEDUP_HASH       */
+  uint32_t dedup_used;         /* THERMO_DEDUP_SORT, _HASH or _SEGMENT          */
   uint32_t reserved0;
   double ms_ingest, ms_build, ms_classify;  /* device time of the last calls   */
   /* device time (CUDA events on the context stream) of the phases of the last

@@ -22,12 +22,12 @@ __device__ __forceinline__ int level_of(uint32_t c) { return 32 - __clz(c); }
 
 // ---- a4 hash path: open addressing, linear probing, slot = prefix<<8 | mask ----
 __global__ void hash_insert_kernel(const ull* __restrict__ keys, ull n, ull* __restrict__ table, ull cap_mask,
-                                   DevCounters* ctr) {
+                                   uint32_t drop_low, DevCounters* ctr) {
   const ull stride = (ull)gridDim.x * blockDim.x;
   for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const ull key = keys[i];
-    const ull pre = key >> 8;
-    const ull m = key & 0xFFull;
+    const ull m = keys[i] & 0xFFull;
+    const ull pre = (keys[i] >> 8) >> drop_low;
+    const ull key = (pre << 8) | m;
     ull h = mix64(pre) & cap_mask;
     bool done = false;
     for (ull probe = 0; probe <= cap_mask && !done; ++probe) {
@@ -48,11 +48,26 @@ __global__ void hash_insert_kernel(const ull* __restrict__ keys, ull n, ull* __r
   }
 }
 
-void launch_hash_insert(const ull* keys, ull n, ull* table, ull cap_mask, DevCounters* ctr, int num_sms,
-                        cudaStream_t s) {
+void launch_hash_insert(const ull* keys, ull n, ull* table, ull cap_mask, uint32_t drop_low, DevCounters* ctr,
+                        int num_sms, cudaStream_t s) {
   if (!n) return;
   unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
-  hash_insert_kernel<<<grid, 256, 0, s>>>(keys, n, table, cap_mask, ctr);
+  hash_insert_kernel<<<grid, 256, 0, s>>>(keys, n, table, cap_mask, drop_low, ctr);
+}
+
+// pc keys [pcid : P][g : S][mask : 8] from keys [g][launch, warp][pcid][mask]
+__global__ void pc_extract_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl, ull* __restrict__ out) {
+  const ull stride = (ull)gridDim.x * blockDim.x;
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const ull k = keys[i];
+    out[i] = ((((ull)key_pcid(k, kl) << kl.S) | key_g(k, kl)) << 8) | (k & 0xFF);
+  }
+}
+
+void launch_pc_extract(const ull* keys, ull n, KeyLayout kl, ull* pckeys, int num_sms, cudaStream_t s) {
+  if (!n) return;
+  unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
+  pc_extract_kernel<<<grid, 256, 0, s>>>(keys, n, kl, pckeys);
 }
 
 // ---- a5 on sorted keys ------------------------------------------------------
@@ -81,29 +96,28 @@ __global__ void __launch_bounds__(256) count_sorted_kernel(const ull* __restrict
   const int lane = threadIdx.x & 31;
   const ull nw = (n + 31) / 32;
   const ull wstride = ((ull)gridDim.x * blockDim.x) >> 5;
-  const int LW = kl.L + kl.W;
+  const int RS = 8 + kl.P;  // a run is one (g, launch, warp): the pc id is ignored
   ull distinct = 0;
   for (ull wi = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < nw; wi += wstride) {
     const ull i = wi * 32 + lane;
     const ull key = i < n ? keys[i] : kEmptyKey;
-    const ull pre = key >> 8;
+    const ull pre = key >> RS;
     bool valid = key != kEmptyKey;
-    if (filter != THERMO_ALL_LAUNCHES && kl.L > 0) valid &= ((pre >> kl.W) & ((1ull << kl.L) - 1)) == filter;
-    if (filter != THERMO_ALL_LAUNCHES && kl.L == 0) valid &= filter == 0;
+    if (filter != THERMO_ALL_LAUNCHES) valid &= key_launch(key, kl) == filter;
     ull prev = __shfl_up_sync(CFULL, pre, 1);
-    if (lane == 0) prev = i > 0 && i - 1 < n ? (keys[i - 1] >> 8) : ~0ull;
+    if (lane == 0) prev = i > 0 && i - 1 < n ? (keys[i - 1] >> RS) : ~0ull;
     const bool head = valid && pre != prev;
     uint32_t m = (uint32_t)(key & 0xFF);
     if (head) {  // OR the run (duplicates are adjacent after the sort)
       for (ull j = i + 1; j < n; ++j) {
         ull kj = keys[j];
-        if ((kj >> 8) != pre) break;
+        if ((kj >> RS) != pre) break;
         m |= (uint32_t)(kj & 0xFF);
       }
     }
     ull v = head ? pack_contrib(m) : 0ull;
     distinct += head ? 1 : 0;
-    const ull g = pre >> LW;
+    const ull g = key == kEmptyKey ? ~0ull : key_g(key, kl);
     // reverse segmented sum over equal g (contiguous after the sort)
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {

@@ -1,0 +1,352 @@
+// decode_common.cuh -- pieces shared by the fast and the general decode
+// kernels (rows a2 + a3): constants, warp helpers, object lookup,
+// the (launch, pc) -> pc id map, per-warp staging / dedup tables and the
+// misalignment counter caches.  See decode.cu for the paper passages.
+#pragma once
+#include <cstdlib>
+
+#include "thermo_internal.cuh"
+
+namespace thermo {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr int kDecWarps = 8;            // warps per block
+constexpr int kStage = 256;             // staged keys per warp before a flush
+constexpr int kFlushAt = kStage - 32;   // flush when the next push may not fit
+constexpr int kInstrSlots = 64;         // per-block (launch, object) counter table
+constexpr int kPcSlots = 64;            // per-block (site -> pc id) cache
+constexpr uint32_t kNoG = 0xFFFFFFFFu;  // empty cache entry (sector ids are < 2^31)
+
+
+// ---------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ ull warp_min64(ull v) {
+  for (int d = 16; d; d >>= 1) { ull o = __shfl_xor_sync(FULL, v, d); v = o < v ? o : v; }
+  return v;
+}
+__device__ __forceinline__ ull warp_max64(ull v) {
+  for (int d = 16; d; d >>= 1) { ull o = __shfl_xor_sync(FULL, v, d); v = o > v ? o : v; }
+  return v;
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
+  return x;
+}
+
+// last object with lo <= x, or -1 if x lies in no object
+__device__ __forceinline__ int obj_lookup(const ull* s_lo, const ull* s_hi, uint32_t n, int steps, ull x) {
+  uint32_t lo = 0, hi = n;
+  for (int i = 0; i < steps; ++i) {
+    uint32_t mid = (lo + hi) >> 1;
+    bool le = s_lo[mid] <= x;
+    lo = le ? mid : lo;
+    hi = le ? hi : mid;
+  }
+  return (n > 0 && x >= s_lo[lo] && x < s_hi[lo]) ? (int)lo : -1;
+}
+
+__device__ __forceinline__ bool in_obj(const ull* s_lo, const ull* s_hi, int o, ull x) {
+  return o >= 0 && x >= s_lo[o] && x < s_hi[o];
+}
+
+// word mask of a sector restricted to the object's words (tail sector of an
+// object whose length is not a multiple of 32 bytes, G9)
+__device__ __forceinline__ uint32_t allow_mask(ull hi_obj, ull sector_start) {
+  const ull lim = hi_obj - sector_start;
+  return lim >= 32 ? 0xFFu : ((1u << ((lim + 3) >> 2)) - 1u);
+}
+
+// merge equal 64-bit prefixes held by adjacent lanes (general path): the first
+// lane of each run gets the OR of the run's masks, the others drop their key
+__device__ __forceinline__ void adjacent_merge(ull& prefix, uint32_t& mask, bool& has, int lane) {
+  ull pp = __shfl_up_sync(FULL, prefix, 1);
+  bool ph = __shfl_up_sync(FULL, has, 1);
+  bool same = lane > 0 && has && ph && pp == prefix;
+  unsigned sb = __ballot_sync(FULL, same);
+  if (sb == 0) return;
+  unsigned hb = __ballot_sync(FULL, has);
+  if (sb == (hb & (hb - 1))) {  // every key equals its predecessor: one run
+    uint32_t orm = __reduce_or_sync(FULL, has ? mask : 0u);
+    if (same) has = false; else if (has) mask = orm;
+    return;
+  }
+  for (int d = 1; d < 32; d <<= 1) {  // reverse segmented OR (Kogge-Stone)
+    ull np = __shfl_down_sync(FULL, prefix, d);
+    uint32_t nm = __shfl_down_sync(FULL, mask, d);
+    bool nh = __shfl_down_sync(FULL, has, d);
+    if (lane + d < 32 && nh && has && np == prefix) mask |= nm;
+  }
+  if (same) has = false;
+}
+
+// same on 32-bit sector ids (fast path: launch/warp are uniform)
+__device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, bool& has, int lane) {
+  const uint32_t pg = __shfl_up_sync(FULL, g, 1);
+  const bool ph = __shfl_up_sync(FULL, has, 1);
+  const bool same = lane > 0 && has && ph && pg == g;
+  const unsigned sb = __ballot_sync(FULL, same);
+  if (sb == 0) return;
+  const unsigned hb = __ballot_sync(FULL, has);
+  if (sb == (hb & (hb - 1))) {
+    const uint32_t orm = __reduce_or_sync(FULL, has ? mask : 0u);
+    if (has) mask = orm;
+  } else {
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t ng = __shfl_down_sync(FULL, g, d);
+      const uint32_t nm = __shfl_down_sync(FULL, mask, d);
+      const bool nh = __shfl_down_sync(FULL, has, d);
+      if (lane + d < 32 && nh && has && ng == g) mask |= nm;
+    }
+  }
+  has = has && !same;
+}
+
+
+
+// full 64-bit key from a packed (pcid << 32 | g) cache entry:
+// [ g : S ][ launch, warp : LW ][ pcid : P ][ mask : 8 ]
+__device__ __forceinline__ ull make_key(ull packed, ull lw, uint32_t mask, uint32_t LW, uint32_t P) {
+  const ull g = packed & 0xFFFFFFFFull, pcid = packed >> 32;
+  return ((((g << LW) | lw) << P | pcid) << 8) | mask;
+}
+
+// per-warp staging buffer in shared memory; flushed to global with one atomic
+struct Stage {
+  ull* s;        // smem [kStage]
+  uint32_t cnt;  // warp-uniform
+  __device__ __forceinline__ void flush(ull* g, ull* gcount, int lane) {
+    __syncwarp();
+    if (cnt == 0) return;
+    ull base = 0;
+    if (lane == 0) base = atomicAdd(gcount, (ull)cnt);
+    base = __shfl_sync(FULL, base, 0);
+    for (uint32_t i = lane; i < cnt; i += 32) g[base + i] = s[i];
+    __syncwarp();
+    cnt = 0;
+  }
+};
+// push the lanes' keys for which HAS holds; KEY is evaluated only on them
+#define STAGE_PUSH(st, HAS, KEY, gbuf, gcnt)                              \
+  do {                                                                    \
+    const bool has_ = (HAS);                                              \
+    const unsigned b_ = __ballot_sync(FULL, has_);                        \
+    if (b_) {                                                             \
+      if (has_) (st).s[(st).cnt + __popc(b_ & lanemask_lt())] = (KEY);    \
+      (st).cnt += __popc(b_);                                             \
+      if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane); \
+    }                                                                     \
+  } while (0)
+
+// (launch, pc) -> dense pc id; inserts on first sight (G11)
+static __device__ uint32_t pc_lookup_global(const PcMap& pm, uint32_t site, DevCounters* ctr) {
+  const ull key = (ull)site + 1ull;
+  uint32_t h = hash32(site) & pm.cap_mask;
+  for (uint32_t probe = 0; probe <= pm.cap_mask; ++probe) {
+    ull cur = *((volatile ull*)&pm.keys[h]);
+    if (cur == 0) {
+      const ull old = atomicCAS(&pm.keys[h], 0ull, key);
+      if (old == 0) {
+        const ull id = atomicAdd(&ctr->pc_count, 1ull);
+        uint32_t v;
+        if (id >= pm.max_pcs) { atomicAdd(&ctr->pc_overflow, 1ull); v = kPcNone - 1; }
+        else { pm.site_of[id] = site; v = (uint32_t)id; }
+        __threadfence();
+        atomicExch(&pm.vals[h], v);
+        return v;
+      }
+      cur = old;
+    }
+    if (cur == key) {
+      uint32_t v;
+      while ((v = *((volatile uint32_t*)&pm.vals[h])) == kPcNone) { }
+      return v;
+    }
+    h = (h + 1) & pm.cap_mask;
+  }
+  return kPcNone - 1;
+}
+
+static __device__ __noinline__ uint32_t pc_lookup(ull* s_pc, const PcMap& pm, uint32_t site, DevCounters* ctr) {
+  const uint32_t h = hash32(site) & (kPcSlots - 1);
+  const ull e = *((volatile ull*)&s_pc[h]);
+  if ((uint32_t)(e >> 32) == site && (uint32_t)e != kPcNone) return (uint32_t)e;
+  const uint32_t id = pc_lookup_global(pm, site, ctr);
+  s_pc[h] = ((ull)site << 32) | id;
+  return id;
+}
+
+static __device__ __noinline__ void instr_flush(uint32_t* s_ikey, ull* s_ival, ull* g_ctr, uint32_t key, uint32_t ni,
+                                         uint32_t nm) {
+  uint32_t h = hash32(key) & (kInstrSlots - 1);
+  for (int probe = 0; probe < kInstrSlots; ++probe) {
+    uint32_t cur = s_ikey[h];
+    if (cur == 0) {
+      cur = atomicCAS(&s_ikey[h], 0u, key);
+      if (cur == 0) cur = key;
+    }
+    if (cur == key) {
+      atomicAdd(&s_ival[2 * h], (ull)ni);
+      if (nm) atomicAdd(&s_ival[2 * h + 1], (ull)nm);
+      return;
+    }
+    h = (h + 1) & (kInstrSlots - 1);
+  }
+  atomicAdd(&g_ctr[2 * (key - 1)], (ull)ni);
+  if (nm) atomicAdd(&g_ctr[2 * (key - 1) + 1], (ull)nm);
+}
+
+// per-warp register cache of the (launch, object) misalignment counters;
+// warp-uniform values, lane 0 flushes evictions into the block's table
+struct InstrCache {
+  uint32_t k0, k1, i0, m0, i1, m1;
+  __device__ __forceinline__ void init() { k0 = k1 = 0; i0 = m0 = i1 = m1 = 0; }
+  __device__ __forceinline__ void add(uint32_t key, bool mis, uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
+    if (key == k0) { ++i0; m0 += mis; return; }
+    if (key == k1) { ++i1; m1 += mis; return; }
+    if (k1 && lane == 0) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
+    k1 = k0; i1 = i0; m1 = m0;
+    k0 = key; i0 = 1; m0 = mis;
+  }
+  __device__ __forceinline__ void drain(uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
+    if (lane == 0) {
+      if (k0) instr_flush(s_ikey, s_ival, g, k0, i0, m0);
+      if (k1) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
+    }
+    init();
+  }
+};
+
+
+// shared-memory layout common to both decode kernels: object table, one
+// per-warp region (fast kernel: dedup table; general kernel: staging buffer),
+// the block's (launch, object) counter table and (site -> pc id) cache
+constexpr int kTab = 512;                            // per-warp dedup table entries
+constexpr int kTabFlush = 384;                       // flush when this full
+constexpr size_t kWarpRegion = kTab * sizeof(ull) + kTab * sizeof(uint32_t);  // >= kStage * 8
+static_assert(kWarpRegion >= kStage * sizeof(ull), "warp region too small for the staging buffer");
+struct Smem {
+  ull *lo, *hi, *soff, *ival, *pc;
+  unsigned char* warp;  // [kDecWarps][kWarpRegion]
+  uint32_t* ikey;
+};
+__device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs& a) {
+  const uint32_t nobj = a.obj.n;
+  Smem m;
+  m.lo = reinterpret_cast<ull*>(smem);
+  m.hi = m.lo + nobj;
+  m.soff = m.hi + nobj;
+  m.ival = m.soff + nobj;                   // [kInstrSlots][2]
+  m.pc = m.ival + 2 * kInstrSlots;          // [kPcSlots]
+  m.ikey = reinterpret_cast<uint32_t*>(m.pc + kPcSlots);
+  m.warp = reinterpret_cast<unsigned char*>(m.ikey + kInstrSlots);
+  for (uint32_t i = threadIdx.x; i < nobj; i += blockDim.x) {
+    m.lo[i] = a.obj.lo[i];
+    m.hi[i] = a.obj.hi[i];
+    m.soff[i] = a.obj.soff[i];
+  }
+  for (int i = threadIdx.x; i < kInstrSlots; i += blockDim.x) {
+    m.ikey[i] = 0;
+    m.ival[2 * i] = 0;
+    m.ival[2 * i + 1] = 0;
+  }
+  for (int i = threadIdx.x; i < kPcSlots; i += blockDim.x) m.pc[i] = ((ull)0xFFFFFFFFu << 32) | kPcNone;
+  __syncthreads();
+  return m;
+}
+
+__device__ __forceinline__ void smem_flush_instr(const Smem& m, ull* g) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kInstrSlots; i += blockDim.x) {
+    const uint32_t k = m.ikey[i];
+    if (k) {
+      atomicAdd(&g[2 * (k - 1)], m.ival[2 * i]);
+      if (m.ival[2 * i + 1]) atomicAdd(&g[2 * (k - 1) + 1], m.ival[2 * i + 1]);
+    }
+  }
+}
+
+__device__ __forceinline__ void flush_launch_ctr(ull* lc, uint32_t launch, ull& unmapped, ull& mapped) {
+  if (launch != 0xFFFFFFFFu && (mapped | unmapped)) {
+    atomicAdd(&lc[2 * launch], unmapped);
+    atomicAdd(&lc[2 * launch + 1], mapped);
+  }
+  unmapped = mapped = 0;
+}
+
+// per-warp dedup table in shared memory: (pc id << 32 | sector) -> word mask,
+// for the records of one source (launch, warp); emitted to the key buffer when
+// the source warp changes, when the table fills, and at the end
+struct WarpTable {
+  ull* key;        // [kTab], ~0 = empty
+  uint32_t* msk;   // [kTab]
+  uint32_t count;  // warp-uniform number of entries
+  ull tag;         // warp-uniform (launch << W | warp) of the entries
+  __device__ __forceinline__ void init(unsigned char* region, int lane) {
+    key = reinterpret_cast<ull*>(region);
+    msk = reinterpret_cast<uint32_t*>(key + kTab);
+    for (int i = lane; i < kTab; i += 32) { key[i] = ~0ull; msk[i] = 0; }
+    count = 0;
+    tag = ~0ull;
+    __syncwarp();
+  }
+  // insert (lane-divergent); returns true if a new entry was created
+  __device__ __forceinline__ bool insert(ull k, uint32_t m) {
+    uint32_t h = ((uint32_t)k * 0x9E3779B1u ^ (uint32_t)(k >> 32) * 0x85EBCA6Bu) >> (32 - 9);
+    for (int probe = 0; probe < kTab; ++probe) {
+      ull cur = key[h];
+      if (cur == ~0ull) {
+        cur = atomicCAS(&key[h], ~0ull, k);
+        if (cur == ~0ull) { atomicOr(&msk[h], m); return true; }
+      }
+      if (cur == k) {
+        if ((msk[h] & m) != m) atomicOr(&msk[h], m);
+        return false;
+      }
+      h = (h + 1) & (kTab - 1);
+    }
+    return false;  // unreachable: the table is flushed before it can fill
+  }
+  // emit every entry as a full key and clear the table (warp-collective)
+  __device__ __forceinline__ void flush(ull* gkeys, ull* gcount, uint32_t LW, uint32_t P, int lane) {
+    __syncwarp();
+    if (count == 0) return;
+    ull base = 0;
+    if (lane == 0) base = atomicAdd(gcount, (ull)count);
+    base = __shfl_sync(FULL, base, 0);
+    const unsigned lt = lanemask_lt();
+    uint32_t pos = 0;
+    for (int i = lane; i < kTab; i += 32) {
+      const ull k = key[i];
+      const bool v = k != ~0ull;
+      const unsigned b = __ballot_sync(FULL, v);
+      if (v) {
+        gkeys[base + pos + __popc(b & lt)] = make_key(k, tag, msk[i], LW, P);
+        key[i] = ~0ull;
+        msk[i] = 0;
+      }
+      pos += __popc(b);
+    }
+    count = 0;
+    __syncwarp();
+  }
+};
+
+
+size_t decode_smem(const DecodeArgs& a);
+
+}  // namespace thermo

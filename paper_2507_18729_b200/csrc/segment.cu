@@ -1,0 +1,423 @@
+// segment.cu -- rows a4 + a5 (+ the per-pc part of a6), "sector-segmented"
+// dedup path: a counting sort of the keys by sector id, then one CTA per chunk
+// of consecutive sectors deduplicates its keys in shared memory, writes the
+// chunk's dense word/sector counts (the paper's popcount flush) and,
+// from the same keys, the per-pc level histograms (G11).
+//
+// Why: a5 only needs the keys grouped per sector, and the sector range is
+// small (SGEMM: 163,840 sectors), so an exact counting sort by sector
+// (histogram, scan, scatter) groups them in ~3 streaming passes instead of one
+// LSD pass per 8 key bits; the (launch, warp) and (pc) dedup then runs in
+// shared memory.  Sectors with more keys than a chunk holds make the caller
+// fall back to the onesweep path (thermo_api.cu).
+#include "thermo_internal.cuh"
+
+namespace thermo {
+
+constexpr unsigned GFULL = 0xFFFFFFFFu;
+constexpr int kSegThreads = 256;
+constexpr int kSegWarps = kSegThreads / 32;
+constexpr int kSegCap = 2048;            // chunk window (keys); a chunk holds < 2 * kSegCap keys
+constexpr int kSegBuf = 2 * kSegCap;     // shared-memory key buffer
+constexpr int kSegRounds = kSegBuf / kSegThreads;  // 32 keys per thread
+constexpr int kScanBlock = 2048;         // scan elements per block (256 threads x 8)
+
+__device__ __forceinline__ unsigned lanemask_lt_g() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int level_of_g(uint32_t c) { return 32 - __clz(c); }
+
+// ---- 1. per-sector key histogram ----------------------------------------------
+__global__ void seg_hist_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl, uint32_t* __restrict__ cnt) {
+  const ull stride = (ull)gridDim.x * blockDim.x;
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&cnt[key_g(keys[i], kl)], 1u);
+}
+
+// ---- 2. exclusive scan of the S_tot counts (3 phases) ----------------------------
+__global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __restrict__ bsum,
+                                uint32_t* __restrict__ maxc) {
+  __shared__ ull s[kSegWarps];
+  __shared__ uint32_t smax[kSegWarps];
+  const ull base = (ull)blockIdx.x * kScanBlock;
+  ull t = 0;
+  uint32_t mx = 0;
+  for (int i = threadIdx.x; i < kScanBlock; i += kSegThreads) {
+    const ull j = base + i;
+    const uint32_t v = j < n ? in[j] : 0u;
+    t += v;
+    mx = v > mx ? v : mx;
+  }
+  for (int d = 16; d; d >>= 1) {
+    t += __shfl_xor_sync(GFULL, t, d);
+    const uint32_t o = __shfl_xor_sync(GFULL, mx, d);
+    mx = o > mx ? o : mx;
+  }
+  if ((threadIdx.x & 31) == 0) { s[threadIdx.x >> 5] = t; smax[threadIdx.x >> 5] = mx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ull a = 0;
+    uint32_t m = 0;
+    for (int i = 0; i < kSegWarps; ++i) { a += s[i]; m = smax[i] > m ? smax[i] : m; }
+    bsum[blockIdx.x] = a;
+    atomicMax(maxc, m);
+  }
+}
+
+// one block: exclusive scan of the block sums; writes the grand total to *total
+__global__ void seg_scan_blocks(ull* bsum, ull nb, ull* total) {
+  __shared__ ull carry;
+  __shared__ ull ws[kSegWarps];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (ull b0 = 0; b0 < nb; b0 += kSegThreads) {
+    const ull i = b0 + threadIdx.x;
+    const ull v = i < nb ? bsum[i] : 0;
+    ull incl = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const ull o = __shfl_up_sync(GFULL, incl, d);
+      if (lane >= d) incl += o;
+    }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    ull wpre = 0;
+    for (int k = 0; k < w; ++k) wpre += ws[k];
+    const ull c = carry;
+    if (i < nb) bsum[i] = c + wpre + incl - v;
+    __syncthreads();
+    if (threadIdx.x == kSegThreads - 1) carry = c + wpre + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// off[j] = exclusive prefix of cnt; cur[j] = off[j] (scatter cursors)
+__global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum,
+                               ull* __restrict__ off, ull* __restrict__ cur) {
+  __shared__ ull ws[kSegWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
+  uint32_t v[8];
+  ull t = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const ull j = base + k;
+    v[k] = j < n ? in[j] : 0u;
+    t += v[k];
+  }
+  ull incl = t;
+  for (int d = 1; d < 32; d <<= 1) {
+    const ull o = __shfl_up_sync(GFULL, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) ws[w] = incl;
+  __syncthreads();
+  ull pre = bsum[blockIdx.x];
+  for (int k = 0; k < w; ++k) pre += ws[k];
+  pre += incl - t;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const ull j = base + k;
+    if (j < n) { off[j] = pre; cur[j] = pre; }
+    pre += v[k];
+  }
+}
+
+// ---- 3. scatter keys into their sector's segment ------------------------------------
+__global__ void seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl, ull* __restrict__ cur,
+                                   ull* __restrict__ out) {
+  const ull stride = (ull)gridDim.x * blockDim.x;
+  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const ull k = keys[i];
+    const ull pos = atomicAdd(&cur[key_g(k, kl)], 1ull);
+    out[pos] = k;
+  }
+}
+
+// ---- 4. per-chunk shared-memory dedup + count --------------------------------------
+// chunk c owns the sectors whose segment starts in [c*kSegCap, (c+1)*kSegCap);
+// their keys lie in [off[s0], off[s1]) and number < 2*kSegCap when every
+// sector has < kSegCap keys (checked by the caller).
+__device__ __forceinline__ ull first_sector_at(const ull* off, ull nsec, ull pos) {
+  ull lo = 0, hi = nsec;  // smallest s with off[s] >= pos (off[nsec] = total)
+  while (lo < hi) {
+    const ull mid = (lo + hi) >> 1;
+    if (off[mid] >= pos) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// stable LSD radix sort of kSegBuf u64 keys in shared memory on bits
+// [lo, lo + bits); returns the buffer holding the result
+__device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* whist, uint32_t* blk_ofs) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt_g();
+  __shared__ uint32_t wsum[kSegWarps];
+  for (int shift = lo; shift < lo + bits; shift += 8) {
+    for (int i = threadIdx.x; i < kSegWarps * 256; i += kSegThreads) whist[i] = 0;
+    __syncthreads();
+    uint32_t rank[kSegRounds];
+#pragma unroll
+    for (int r = 0; r < kSegRounds; ++r) {  // warp w ranks its own contiguous keys
+      const uint32_t idx = (uint32_t)w * kSegRounds * 32 + r * 32 + lane;
+      const uint32_t d = (uint32_t)(src[idx] >> shift) & 255u;
+      const unsigned peers = __match_any_sync(GFULL, d);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (lane == leader) old = whist[w * 256 + d];
+      old = __shfl_sync(GFULL, old, leader);
+      rank[r] = old + __popc(peers & lt);
+      __syncwarp();
+      if (lane == leader) whist[w * 256 + d] = old + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    uint32_t tot = 0;
+    for (int ww = 0; ww < kSegWarps; ++ww) {
+      const uint32_t v = whist[ww * 256 + t];
+      whist[ww * 256 + t] = tot;
+      tot += v;
+    }
+    // exclusive scan of the 256 digit totals: warp scans + warp sums
+    uint32_t incl = tot;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(GFULL, incl, d);
+      if (lane >= d) incl += o;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int k = 0; k < w; ++k) wpre += wsum[k];
+    blk_ofs[t] = wpre + incl - tot;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kSegRounds; ++r) {
+      const uint32_t idx = (uint32_t)w * kSegRounds * 32 + r * 32 + lane;
+      const ull k = src[idx];
+      const uint32_t d = (uint32_t)(k >> shift) & 255u;
+      dst[blk_ofs[d] + whist[w * 256 + d] + rank[r]] = k;
+    }
+    __syncthreads();
+    ull* tmp = src; src = dst; dst = tmp;
+  }
+  return src;
+}
+
+// per-block (pc, level) bin table in shared memory: open addressing on the
+// bin id; a full table falls back to the global atomic
+constexpr int kPcBins = 512;
+__device__ __forceinline__ void bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, uint32_t bin, uint32_t v) {
+  uint32_t h = (bin * 0x9E3779B1u) >> (32 - 9);
+  for (int probe = 0; probe < 16; ++probe) {
+    uint32_t cur = tbin[h];
+    if (cur == 0xFFFFFFFFu) {
+      cur = atomicCAS(&tbin[h], 0xFFFFFFFFu, bin);
+      if (cur == 0xFFFFFFFFu) cur = bin;
+    }
+    if (cur == bin) { atomicAdd(&tcnt[h], v); return; }
+    h = (h + 1) & (kPcBins - 1);
+  }
+  atomicAdd(&g[bin], (ull)v);
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ off,
+                                                               ull nsec, KeyLayout kl, uint32_t filter,
+                                                               uint32_t* __restrict__ wc, uint32_t* __restrict__ sc,
+                                                               const uint32_t* __restrict__ site_of,
+                                                               ull* __restrict__ pc_hist, DevCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ull* buf0 = reinterpret_cast<ull*>(smem_raw);                      // [kSegBuf]
+  ull* buf1 = buf0 + kSegBuf;                                        // [kSegBuf]
+  uint32_t* whist = reinterpret_cast<uint32_t*>(buf1 + kSegBuf);     // [kSegWarps][256]
+  __shared__ uint32_t blk_ofs[256];
+  __shared__ ull s_range[2];
+  const int lane = threadIdx.x & 31;
+  const ull c = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_range[0] = first_sector_at(off, nsec, c * kSegCap);
+    s_range[1] = first_sector_at(off, nsec, (c + 1) * kSegCap);
+  }
+  __syncthreads();
+  const ull s0 = s_range[0], s1 = s_range[1];
+  if (s0 >= s1) return;
+  const ull k0 = off[s0];
+  const uint32_t nk = (uint32_t)(off[s1] - k0);  // < kSegBuf
+  int ls = 0;
+  while ((1ull << ls) < (s1 - s0)) ++ls;
+  const uint32_t LWP = kl.L + kl.W + kl.P;
+  // local key: [g - s0 : ls][launch, warp, pcid : LWP][mask : 8]; filtered-out
+  // launches and padding become the all-ones sentinel (sorted last)
+  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) {
+    ull v = ~0ull;
+    if (i < nk) {
+      const ull k = seg[k0 + i];
+      if (filter == THERMO_ALL_LAUNCHES || key_launch(k, kl) == filter)
+        v = ((key_g(k, kl) - s0) << (LWP + 8)) | (k & ((1ull << (LWP + 8)) - 1));
+    }
+    buf0[i] = v;
+  }
+  __syncthreads();
+  // runs of (g, launch, warp) only need those bits sorted; the pc id bits below stay unsorted
+  ull* src = smem_radix_sort(buf0, buf1, 8 + (int)kl.P, ls + (int)(kl.L + kl.W), whist, blk_ofs);
+  // ---- (a) runs of equal (g, launch, warp): distinct warps per sector / word ----
+  const int RS = 8 + (int)kl.P;
+  ull distinct = 0;
+  for (uint32_t base = 0; base < kSegBuf; base += kSegThreads) {
+    const uint32_t i = base + threadIdx.x;
+    const ull key = src[i];
+    const bool valid = key != ~0ull;
+    const ull pre = key >> RS;
+    const ull prev = i > 0 ? (src[i - 1] >> RS) : ~0ull;
+    const bool head = valid && pre != prev;
+    uint32_t m = (uint32_t)(key & 0xFF);
+    if (head)
+      for (uint32_t j = i + 1; j < kSegBuf && (src[j] >> RS) == pre; ++j) m |= (uint32_t)(src[j] & 0xFF);
+    const ull g = valid ? s0 + (key >> (LWP + 8)) : ~0ull;
+    ull v = 0;
+    if (head) {
+      v = 1ull;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) v |= (ull)((m >> b) & 1u) << (6 * (b + 1));
+    }
+    distinct += head ? 1 : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const ull ov = __shfl_down_sync(GFULL, v, d);
+      const ull og = __shfl_down_sync(GFULL, g, d);
+      if (lane + d < 32 && og == g) v += ov;
+    }
+    const ull pg = __shfl_up_sync(GFULL, g, 1);
+    if ((lane == 0 || pg != g) && v && valid) {
+      const uint32_t c0 = (uint32_t)(v & 63);
+      if (c0) atomicAdd(&sc[g], c0);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const uint32_t cb = (uint32_t)((v >> (6 * (b + 1))) & 63);
+        if (cb) atomicAdd(&wc[8 * g + b], cb);
+      }
+    }
+  }
+  for (int d = 16; d; d >>= 1) distinct += __shfl_xor_sync(GFULL, distinct, d);
+  if (lane == 0 && distinct) atomicAdd(&ctr->distinct_pairs, distinct);
+  if (!pc_hist) return;
+  __syncthreads();  // this chunk's dense counts are final (it owns its sectors)
+  // ---- (b) distinct (g, pcid) with OR-ed masks: per-pc level histograms (G11) ----
+  // a shared-memory hash set on the 32-bit (g - s0, pcid) key in the free buffer
+  // (runs of one (g, pcid) hold every warp touching the sector: too long to scan)
+  uint32_t* hk = reinterpret_cast<uint32_t*>(src == buf0 ? buf1 : buf0);  // [kSegBuf] keys
+  uint32_t* hm = hk + kSegBuf;                                            // [kSegBuf] masks
+  uint32_t* tbin = reinterpret_cast<uint32_t*>(whist);                    // [kPcBins] bin ids
+  uint32_t* tcnt = tbin + kPcBins;                                        // [kPcBins] counts
+  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) { hk[i] = 0xFFFFFFFFu; hm[i] = 0; }
+  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
+  __syncthreads();
+  const ull pmask = (1ull << kl.P) - 1;
+  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) {
+    const ull k = src[i];
+    if (k == ~0ull) continue;
+    const uint32_t hkey = (uint32_t)(((k >> (LWP + 8)) << kl.P) | ((k >> 8) & pmask));
+    const uint32_t m = (uint32_t)(k & 0xFF);
+    uint32_t h = (hkey * 0x9E3779B1u) & (kSegBuf - 1);
+    for (int probe = 0; probe < kSegBuf; ++probe) {
+      uint32_t cur = hk[h];
+      if (cur == 0xFFFFFFFFu) {
+        cur = atomicCAS(&hk[h], 0xFFFFFFFFu, hkey);
+        if (cur == 0xFFFFFFFFu) cur = hkey;
+      }
+      if (cur == hkey) {
+        if ((hm[h] & m) != m) atomicOr(&hm[h], m);
+        break;
+      }
+      h = (h + 1) & (kSegBuf - 1);
+    }
+  }
+  __syncthreads();
+  ull dpc = 0;
+  for (uint32_t base = 0; base < kSegBuf; base += kSegThreads) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t hkey = hk[i];
+    const bool head = hkey != 0xFFFFFFFFu;
+    const uint32_t m = hm[i];
+    dpc += head ? 1 : 0;
+    if (!__any_sync(GFULL, head)) continue;
+    const ull g = s0 + (hkey >> kl.P);
+    const uint32_t pcid = (uint32_t)(hkey & pmask);
+    {
+      const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(sc[g]) : 0xFFFFFFFFu;
+      const unsigned mm = __match_any_sync(GFULL, bin);
+      if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const bool hb = head && ((m >> b) & 1u);
+      const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wc[8 * g + b]) : 0xFFFFFFFFu;
+      const unsigned mm = __match_any_sync(GFULL, bin);
+      if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+    }
+  }
+  for (int d = 16; d; d >>= 1) dpc += __shfl_xor_sync(GFULL, dpc, d);
+  if (lane == 0 && dpc) atomicAdd(&ctr->distinct_pc, dpc);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
+    if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
+  (void)site_of;
+}
+
+static size_t segment_chunk_smem() { return (size_t)2 * kSegBuf * sizeof(ull) + kSegWarps * 256 * sizeof(uint32_t); }
+ull segment_chunk_cap() { return kSegCap; }
+
+// phases 1-2; syncs once so the caller can read the largest per-sector count
+cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
+                            cudaStream_t s, uint32_t* max_per_sector) {
+  cudaError_t e;
+  if (ws.cap_sec < nsec + 1) {
+    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum);
+    ws.cap_sec = nsec + 1;
+    if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
+    if ((e = cudaMalloc(&ws.off, (nsec + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
+    if (!ws.maxc && (e = cudaMalloc(&ws.maxc, sizeof(uint32_t)))) return e;
+  }
+  cudaMemsetAsync(ws.cnt, 0, (nsec + 1) * sizeof(uint32_t), s);
+  cudaMemsetAsync(ws.maxc, 0, sizeof(uint32_t), s);
+  if (n) {
+    const unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
+    seg_hist_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cnt);
+  }
+  const ull nb = (nsec + kScanBlock - 1) / kScanBlock;
+  seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
+  seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
+  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.cur);
+  ws.launches += 4;
+  if ((e = cudaMemcpyAsync(max_per_sector, ws.maxc, sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) return e;
+  return cudaStreamSynchronize(s);
+}
+
+// phases 3-4: keys -> out (grouped by sector) -> dense counts (+ per-pc histograms)
+cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull nsec, uint32_t filter,
+                          SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
+                          DevCounters* ctr, int num_sms, cudaStream_t s) {
+  if (n) {
+    const unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
+    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cur, out);
+  }
+  const size_t smem = segment_chunk_smem();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(seg_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const ull chunks = (n + kSegCap - 1) / kSegCap;
+  if (chunks)
+    seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
+                                                                  pc_hist, ctr);
+  ws.launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace thermo

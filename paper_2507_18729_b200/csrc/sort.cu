@@ -136,15 +136,26 @@ __global__ void __launch_bounds__(kSortThreads, 3) onesweep_kernel(const ull* __
   }
   ull prefix = 0;
   if (tile > 0) {
+    // look back 4 predecessors per step (independent loads in flight)
+    const uint32_t ep8 = epoch & 0xFF;
     long long tp = (long long)tile - 1;
     while (tp >= 0) {
-      ull s = vs[(ull)tp * 256 + t];
-      uint32_t ep = (uint32_t)(s >> 56);
-      ull flag = (s >> 54) & 3ull;
-      if (ep != (epoch & 0xFF) || flag == 0) continue;  // not ready yet: spin
-      prefix += s & ((1ull << 54) - 1);
-      if (flag == kFlagInc) break;
-      --tp;
+      ull s[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[j] = tp - j >= 0 ? vs[(ull)(tp - j) * 256 + t] : pack_status(ep8, kFlagInc, 0);
+      bool stop = false;
+      int used = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (stop) continue;
+        const ull flag = (s[j] >> 54) & 3ull;
+        if ((uint32_t)(s[j] >> 56) != ep8 || flag == 0) { stop = true; continue; }  // not ready: retry from here
+        prefix += s[j] & ((1ull << 54) - 1);
+        ++used;
+        if (flag == kFlagInc) { stop = true; used = 1 << 20; }
+      }
+      if (used >= (1 << 20)) break;
+      tp -= used;
     }
     __threadfence();
     vs[(ull)tile * 256 + t] = pack_status(epoch, kFlagInc, prefix + tot);

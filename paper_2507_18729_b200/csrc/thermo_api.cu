@@ -79,11 +79,14 @@ struct thermo_ctx {
   ull* d_tile_prev = nullptr;  // followed by obj_tile0 (u32[n+1])
   ull* d_heads = nullptr;
   size_t heads_cap = 0;
+  ull* d_deferred = nullptr;
+  size_t deferred_cap = 0;
   ull* d_table = nullptr;
   size_t table_cap = 0;
   ull* d_pctable = nullptr;
   size_t pctable_cap = 0;
   SortWorkspace sw, swpc;
+  SegWorkspace seg;
   // host staging
   void* h_pinned[2] = {nullptr, nullptr};
   uint4* d_stage[2] = {nullptr, nullptr};
@@ -171,6 +174,12 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
     CK(dalloc(&ctx->d_heads, ctx->heads_cap));
   }
   CK(cudaEventRecord(ctx->evp[6], ctx->stream));
+  if (ctx->deferred_cap < n) {
+    dfree(ctx->d_deferred);
+    ctx->deferred_cap = n + n / 4 + 1024;
+    CK(dalloc(&ctx->d_deferred, ctx->deferred_cap));
+  }
+  CK(cudaMemsetAsync(&ctx->d_ctr->n_deferred, 0, sizeof(ull), ctx->stream));
   launch_find_heads(recs, n, kRangeLen, (uint32_t)n_ranges, ctx->d_heads, ctx->stream);
   DecodeArgs a{};
   a.recs = recs;
@@ -184,14 +193,15 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.track_pc = ctx->cfg.track_pc ? 1 : 0;
   a.pcmap = PcMap{ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of, ctx->pc_cap - 1, ctx->cfg.max_pcs};
   a.keys = ctx->d_keys;
-  a.pckeys = ctx->d_pckeys;
   a.ctr = ctx->d_ctr;
   a.instr_ctr = ctx->d_instr;
   a.launch_ctr = ctx->d_launch_ctr;
+  a.deferred = ctx->d_deferred;
   launch_decode(a, ctx->num_sms, ctx->stream);
+  launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->evp[7], ctx->stream));
-  ctx->launches += 2;
+  ctx->launches += 3;
   return THERMO_OK;
 }
 
@@ -234,7 +244,7 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
   thermo_config c;
   if (cfg) c = *cfg; else thermo_default_config(&c);
   if (c.max_launches < 1 || c.max_launches > 4096 || c.max_warps_per_launch < 1 || c.max_pcs < 1 ||
-      c.max_pcs > 65536 || c.dedup > THERMO_DEDUP_HASH)
+      c.max_pcs > 65536 || c.dedup > THERMO_DEDUP_SEGMENT)
     return THERMO_EINVAL;
   thermo_ctx* ctx = new thermo_ctx();
   ctx->device = device;
@@ -290,8 +300,9 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_keys, ctx->d_pckeys, ctx->d_ctr, ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of,
                   ctx->d_instr, ctx->d_launch_ctr, ctx->d_hist, ctx->d_pchist, ctx->d_ind, ctx->d_tile_obj,
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
-                  ctx->d_table, ctx->d_pctable, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
-                  ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->d_stage[0],
+                  ctx->d_table, ctx->d_pctable, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
+                  ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
+                  ctx->seg.bsum, ctx->seg.maxc, ctx->d_stage[0],
                   ctx->d_stage[1]};
   for (void* b : bufs) dfree(b);
   for (int i = 0; i < 2; ++i) {
@@ -364,9 +375,13 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   kl.S = std::max(1, bit_width(soff - 1));
   kl.L = bit_width(c.max_launches - 1);
   kl.W = bit_width(c.max_warps_per_launch - 1);
-  kl.P = bit_width(c.max_pcs - 1);
-  if (kl.S + kl.L + kl.W > 56 || kl.P + kl.S > 56)
-    return fail(ctx, THERMO_ERANGE, "sector/launch/warp key widths exceed 56 bits");
+  kl.P = c.track_pc ? bit_width(c.max_pcs - 1) : 0;
+  if (kl.S + kl.L + kl.W + kl.P > 56)
+    return fail(ctx, THERMO_ERANGE,
+                "key widths exceed 56 bits: sectors " + std::to_string(kl.S) + " + launch " + std::to_string(kl.L) +
+                    " + warp " + std::to_string(kl.W) + " + pc " + std::to_string(kl.P) +
+                    " (lower max_warps_per_launch / max_pcs)");
+  if (soff >= (1ull << 31)) return fail(ctx, THERMO_ERANGE, "more than 2^31 sectors (64 GiB) of registered objects");
   ctx->kl = kl;
   // ---- device tables ----
   CK(dalloc(&ctx->d_lo, n)); CK(dalloc(&ctx->d_hi, n)); CK(dalloc(&ctx->d_soff, n + 1));
@@ -433,13 +448,9 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
   } else {
     cudaGetLastError();
   }
-  // worst case: every record emits two keys into each stream
+  // worst case: every record emits two keys (one per sector it touches)
   st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * (ull)n + 64, ctx->n_keys);
   if (st) return st;
-  if (ctx->cfg.track_pc) {
-    st = grow_keys(ctx, &ctx->d_pckeys, &ctx->pckeys_cap, ctx->n_pckeys + 2 * (ull)n + 64, ctx->n_pckeys);
-    if (st) return st;
-  }
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
   if (on_device) {
     st = decode_device(ctx, reinterpret_cast<const uint4*>(recs), n);
@@ -531,14 +542,43 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
-  uint32_t mode = ctx->cfg.dedup == THERMO_DEDUP_AUTO ? THERMO_DEDUP_SORT : ctx->cfg.dedup;
-  ctx->dedup_used = mode;
+  uint32_t mode = ctx->cfg.dedup == THERMO_DEDUP_AUTO ? THERMO_DEDUP_SEGMENT : ctx->cfg.dedup;
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
-  // ---- main keys: a4 dedup + a5 count ----
+  bool pc_done = false;
+  // ---- a4 dedup + a5 count (+ a6 per-pc on the segment path) ----
+  if (mode == THERMO_DEDUP_SEGMENT) {
+    // counting sort by sector; falls back to the onesweep path when one
+    // sector holds more keys than a shared-memory chunk
+    CK(cudaEventRecord(ctx->evp[0], s));
+    uint32_t maxc = 0;
+    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc);
+    if (e) return fail(ctx, THERMO_ECUDA, std::string("segment prepare: ") + cudaGetErrorString(e));
+    if (maxc < segment_chunk_cap()) {
+      if (ctx->sw.alt_cap < ctx->n_keys) {
+        dfree(ctx->sw.alt);
+        ctx->sw.alt_cap = ctx->n_keys + ctx->n_keys / 8 + 1024;
+        CK(dalloc(&ctx->sw.alt, ctx->sw.alt_cap));
+      }
+      CK(cudaEventRecord(ctx->evp[1], s));
+      e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, kl, ctx->S_tot, launch_filter, ctx->seg, ctx->d_wc,
+                        ctx->d_sc, ctx->d_site_of, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
+                        ctx->num_sms, s);
+      if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
+      ctx->launches += ctx->seg.launches;
+      ctx->seg.launches = 0;
+      pc_done = true;
+    } else {
+      mode = THERMO_DEDUP_SORT;
+      ctx->launches += ctx->seg.launches;
+      ctx->seg.launches = 0;
+    }
+  }
+  ctx->dedup_used = mode;
   if (mode == THERMO_DEDUP_SORT) {
     CK(cudaEventRecord(ctx->evp[0], s));
-    ull* sorted = radix_sort_keys(ctx->d_keys, ctx->n_keys, 8, kl.S + kl.L + kl.W, ctx->sw, ctx->num_sms, s, &e);
+    ull* sorted =
+        radix_sort_keys(ctx->d_keys, ctx->n_keys, 8, kl.S + kl.L + kl.W + kl.P, ctx->sw, ctx->num_sms, s, &e);
     CK(cudaEventRecord(ctx->evp[1], s));
     if (e) return fail(ctx, THERMO_ECUDA, std::string("radix sort: ") + cudaGetErrorString(e));
     if (sorted != ctx->d_keys) {  // keep the sorted copy as the retained keys
@@ -547,7 +587,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     }
     launch_count_sorted(ctx->d_keys, ctx->n_keys, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
     ctx->launches += 1;
-  } else {
+  } else if (mode == THERMO_DEDUP_HASH) {
     ull cap = next_pow2(std::max<ull>(1024, 2 * ctx->n_keys));
     if (ctx->table_cap < cap) {
       dfree(ctx->d_table);
@@ -556,7 +596,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     }
     CK(cudaEventRecord(ctx->evp[0], s));
     CK(cudaMemsetAsync(ctx->d_table, 0xFF, cap * 8, s));
-    launch_hash_insert(ctx->d_keys, ctx->n_keys, ctx->d_table, cap - 1, ctx->d_ctr, ctx->num_sms, s);
+    launch_hash_insert(ctx->d_keys, ctx->n_keys, ctx->d_table, cap - 1, kl.P, ctx->d_ctr, ctx->num_sms, s);
     CK(cudaEventRecord(ctx->evp[1], s));
     ctx->launches += 2;
     launch_count_hash(ctx->d_table, cap, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
@@ -567,11 +607,18 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->num_sms, s);
   ctx->launches += 1;
   CK(cudaEventRecord(ctx->evp[3], s));
-  if (ctx->cfg.track_pc) {
-    // the pc stream defaults to the hash path: its distinct set is bounded by
-    // n_pcs * S_tot, usually small enough for an L2-resident table
-    const uint32_t pc_mode = ctx->cfg.dedup == THERMO_DEDUP_SORT ? THERMO_DEDUP_SORT : THERMO_DEDUP_HASH;
-    if (pc_mode == THERMO_DEDUP_SORT) {
+  if (ctx->cfg.track_pc && !pc_done) {
+    // pc keys [pcid][g][mask] derived from the keys; deduplicated by sort
+    // (SORT mode) or by a hash table bounded by n_pcs * S_tot (usually L2-sized)
+    if (ctx->pckeys_cap < ctx->n_keys) {
+      dfree(ctx->d_pckeys);
+      ctx->pckeys_cap = ctx->n_keys + ctx->n_keys / 8 + 1024;
+      CK(dalloc(&ctx->d_pckeys, ctx->pckeys_cap));
+    }
+    ctx->n_pckeys = ctx->n_keys;
+    launch_pc_extract(ctx->d_keys, ctx->n_keys, kl, ctx->d_pckeys, ctx->num_sms, s);
+    ctx->launches += 1;
+    if (mode == THERMO_DEDUP_SORT) {
       ull* sorted = radix_sort_keys(ctx->d_pckeys, ctx->n_pckeys, 8, kl.P + kl.S, ctx->swpc, ctx->num_sms, s, &e);
       if (e) return fail(ctx, THERMO_ECUDA, std::string("radix sort (pc): ") + cudaGetErrorString(e));
       if (sorted != ctx->d_pckeys) {
@@ -590,7 +637,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
         CK(dalloc(&ctx->d_pctable, cap));
       }
       CK(cudaMemsetAsync(ctx->d_pctable, 0xFF, cap * 8, s));
-      launch_hash_insert(ctx->d_pckeys, ctx->n_pckeys, ctx->d_pctable, cap - 1, ctx->d_ctr, ctx->num_sms, s);
+      launch_hash_insert(ctx->d_pckeys, ctx->n_pckeys, ctx->d_pctable, cap - 1, 0, ctx->d_ctr, ctx->num_sms, s);
       ctx->launches += 2;
       launch_pc_hist_hash(ctx->d_pctable, cap, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
                           ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);

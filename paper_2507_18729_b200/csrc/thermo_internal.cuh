@@ -34,7 +34,8 @@ struct DevCounters {
   ull distinct_pairs;  // set by the count kernels
   ull distinct_pc;     // set by the per-pc kernel
   ull hash_fail;       // hash-table insert failures (probe limit)
-  ull pad[7];
+  ull n_deferred;      // views deferred to the general decode kernel (per call)
+  ull pad[6];
 };
 
 // ---- object table in device memory, sorted by (space << 48 | base) -------
@@ -55,11 +56,19 @@ struct PcMap {
 };
 
 // ---- key layout -----------------------------------------------------------
-// main key:  [ g : S ][ launch : L ][ warp : W ][ mask : 8 ]   (S+L+W <= 56)
-// pc key:    [ pcid : P ][ g : S ][ mask : 8 ]                  (P+S <= 56)
+// key:     [ g : S ][ launch : L ][ warp : W ][ pcid : P ][ mask : 8 ]  (S+L+W+P <= 56)
+//          one stream carries the (sector, warp) and the (pc, sector) facts
+// pc key:  [ pcid : P ][ g : S ][ mask : 8 ]   (derived at build for the sort/hash paths)
 struct KeyLayout {
   uint32_t S, L, W, P;
 };
+__host__ __device__ __forceinline__ ull key_g(ull key, const KeyLayout& k) { return key >> (8 + k.P + k.L + k.W); }
+__host__ __device__ __forceinline__ uint32_t key_launch(ull key, const KeyLayout& k) {
+  return k.L ? (uint32_t)((key >> (8 + k.P + k.W)) & ((1ull << k.L) - 1)) : 0u;
+}
+__host__ __device__ __forceinline__ uint32_t key_pcid(ull key, const KeyLayout& k) {
+  return k.P ? (uint32_t)((key >> 8) & ((1ull << k.P) - 1)) : 0u;
+}
 
 struct DecodeArgs {
   const uint4* recs;
@@ -71,17 +80,19 @@ struct DecodeArgs {
   uint32_t max_launches, max_warps;
   int track_pc;
   PcMap pcmap;
-  ull* keys;              // main key buffer (append)
-  ull* pckeys;            // pc key buffer (append)
+  ull* keys;              // key buffer (append)
   DevCounters* ctr;
   ull* instr_ctr;         // [max_launches * n_obj * 2] (instrs, misaligned)
   ull* launch_ctr;        // [max_launches * 2] (unmapped words, mapped word accesses)
+  ull* deferred;          // [n] (p << 6 | len) of non-uniform views
 };
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------
 void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_ranges, ull* heads,
                        cudaStream_t s);
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
+void launch_decode_batch(const DecodeArgs& a, int num_sms, cudaStream_t s);
+void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s);
 
 // onesweep LSD radix sort of u64 keys on bits [lo_bit, lo_bit + nbits)
 struct SortWorkspace {
@@ -96,9 +107,32 @@ struct SortWorkspace {
 ull* radix_sort_keys(ull* keys, ull n, int lo_bit, int nbits, SortWorkspace& ws, int num_sms,
                      cudaStream_t s, cudaError_t* err);
 
-// hash-set dedup: insert keys (prefix<<8 | mask) into table; EMPTY = ~0
-void launch_hash_insert(const ull* keys, ull n, ull* table, ull cap_mask, DevCounters* ctr, int num_sms,
-                        cudaStream_t s);
+// sector-segmented dedup (segment.cu): counting sort by sector + per-chunk
+// shared-memory dedup and count
+struct SegWorkspace {
+  uint32_t* cnt = nullptr;   // [S_tot + 1] keys per sector
+  ull* off = nullptr;        // [S_tot + 1] exclusive prefix (off[S_tot] = total)
+  ull* cur = nullptr;        // [S_tot + 1] scatter cursors
+  ull* bsum = nullptr;       // scan block sums
+  uint32_t* maxc = nullptr;  // max keys in one sector
+  ull cap_sec = 0;
+  ull launches = 0;
+};
+cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
+                            cudaStream_t s, uint32_t* max_per_sector);
+// scatter + per-chunk dedup: dense counts (a5) and, if pc_hist != null, the
+// per-pc histograms (a6) of the chunk's sectors
+cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull nsec, uint32_t filter,
+                          SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
+                          DevCounters* ctr, int num_sms, cudaStream_t s);
+ull segment_chunk_cap();
+
+// hash-set dedup: insert keys (prefix<<8 | mask) into table; EMPTY = ~0.
+// drop_low: prefix bits dropped before inserting (the pc id of main keys)
+void launch_hash_insert(const ull* keys, ull n, ull* table, ull cap_mask, uint32_t drop_low, DevCounters* ctr,
+                        int num_sms, cudaStream_t s);
+// derive pc keys [pcid : P][g : S][mask : 8] from keys (sort / hash paths)
+void launch_pc_extract(const ull* keys, ull n, KeyLayout kl, ull* pckeys, int num_sms, cudaStream_t s);
 
 // segmented count (a5) -> dense arrays
 void launch_count_sorted(const ull* keys, ull n, KeyLayout kl, uint32_t launch_filter, uint32_t* word_cnt,

@@ -69,7 +69,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("dedup", [1, 2])
+@pytest.mark.parametrize("dedup", [1, 2, 3])
 @pytest.mark.parametrize("i", range(len(SMALL)))
 def test_small_workloads(i, dedup):
     t = SMALL[i]()
@@ -78,7 +78,7 @@ def test_small_workloads(i, dedup):
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3, 4])
-@pytest.mark.parametrize("dedup", [1, 2])
+@pytest.mark.parametrize("dedup", [1, 2, 3])
 def test_random_traces(seed, dedup):
     """Unaligned/straddling sizes, unmapped and invalid records, 3 launches,
     shared-space objects, instructions of 1..40 records (split at 32)."""
