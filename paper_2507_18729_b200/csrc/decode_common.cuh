@@ -118,13 +118,6 @@ __device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, boo
 
 
 
-// full 64-bit key from a packed (pcid << 32 | g) cache entry:
-// [ g : S ][ launch, warp : LW ][ pcid : P ][ mask : 8 ]
-__device__ __forceinline__ ull make_key(ull packed, ull lw, uint32_t mask, uint32_t LW, uint32_t P) {
-  const ull g = packed & 0xFFFFFFFFull, pcid = packed >> 32;
-  return ((((g << LW) | lw) << P | pcid) << 8) | mask;
-}
-
 // per-warp staging buffer in shared memory; flushed to global with one atomic
 struct Stage {
   ull* s;        // smem [kStage]
@@ -233,12 +226,9 @@ struct InstrCache {
 
 
 // shared-memory layout common to both decode kernels: object table, one
-// per-warp region (fast kernel: dedup table; general kernel: staging buffer),
-// the block's (launch, object) counter table and (site -> pc id) cache
-constexpr int kTab = 512;                            // per-warp dedup table entries
-constexpr int kTabFlush = 384;                       // flush when this full
-constexpr size_t kWarpRegion = kTab * sizeof(ull) + kTab * sizeof(uint32_t);  // >= kStage * 8
-static_assert(kWarpRegion >= kStage * sizeof(ull), "warp region too small for the staging buffer");
+// per-warp key staging buffer, the block's (launch, object) counter table and
+// (site -> pc id) cache
+constexpr size_t kWarpRegion = kStage * sizeof(ull);
 struct Smem {
   ull *lo, *hi, *soff, *ival, *pc;
   unsigned char* warp;  // [kDecWarps][kWarpRegion]
@@ -287,65 +277,6 @@ __device__ __forceinline__ void flush_launch_ctr(ull* lc, uint32_t launch, ull& 
   }
   unmapped = mapped = 0;
 }
-
-// per-warp dedup table in shared memory: (pc id << 32 | sector) -> word mask,
-// for the records of one source (launch, warp); emitted to the key buffer when
-// the source warp changes, when the table fills, and at the end
-struct WarpTable {
-  ull* key;        // [kTab], ~0 = empty
-  uint32_t* msk;   // [kTab]
-  uint32_t count;  // warp-uniform number of entries
-  ull tag;         // warp-uniform (launch << W | warp) of the entries
-  __device__ __forceinline__ void init(unsigned char* region, int lane) {
-    key = reinterpret_cast<ull*>(region);
-    msk = reinterpret_cast<uint32_t*>(key + kTab);
-    for (int i = lane; i < kTab; i += 32) { key[i] = ~0ull; msk[i] = 0; }
-    count = 0;
-    tag = ~0ull;
-    __syncwarp();
-  }
-  // insert (lane-divergent); returns true if a new entry was created
-  __device__ __forceinline__ bool insert(ull k, uint32_t m) {
-    uint32_t h = ((uint32_t)k * 0x9E3779B1u ^ (uint32_t)(k >> 32) * 0x85EBCA6Bu) >> (32 - 9);
-    for (int probe = 0; probe < kTab; ++probe) {
-      ull cur = key[h];
-      if (cur == ~0ull) {
-        cur = atomicCAS(&key[h], ~0ull, k);
-        if (cur == ~0ull) { atomicOr(&msk[h], m); return true; }
-      }
-      if (cur == k) {
-        if ((msk[h] & m) != m) atomicOr(&msk[h], m);
-        return false;
-      }
-      h = (h + 1) & (kTab - 1);
-    }
-    return false;  // unreachable: the table is flushed before it can fill
-  }
-  // emit every entry as a full key and clear the table (warp-collective)
-  __device__ __forceinline__ void flush(ull* gkeys, ull* gcount, uint32_t LW, uint32_t P, int lane) {
-    __syncwarp();
-    if (count == 0) return;
-    ull base = 0;
-    if (lane == 0) base = atomicAdd(gcount, (ull)count);
-    base = __shfl_sync(FULL, base, 0);
-    const unsigned lt = lanemask_lt();
-    uint32_t pos = 0;
-    for (int i = lane; i < kTab; i += 32) {
-      const ull k = key[i];
-      const bool v = k != ~0ull;
-      const unsigned b = __ballot_sync(FULL, v);
-      if (v) {
-        gkeys[base + pos + __popc(b & lt)] = make_key(k, tag, msk[i], LW, P);
-        key[i] = ~0ull;
-        msk[i] = 0;
-      }
-      pos += __popc(b);
-    }
-    count = 0;
-    __syncwarp();
-  }
-};
-
 
 size_t decode_smem(const DecodeArgs& a);
 

@@ -1,19 +1,96 @@
 // decode_fast.cu -- the fast decode kernel (rows a2 + a3): one
-// warp instruction ("view") per iteration when every active record of it
-// shares warp, pc, launch, space and size (what a collector emits for one
-// instruction); any other view is deferred to decode_general_kernel
-// (decode.cu), which produces the same keys and counters.
+// warp instruction ("view", lane l = record p + l) per iteration when all its
+// records share warp, pc, launch, size, kind, space and the upper 16 address
+// bits, and none straddles a sector -- what a collector emits for one
+// instruction.  Any other view is deferred to
+// decode_general_kernel (decode.cu), which produces the same keys and counters.
 //
-// Per view: decode, object resolution through a two-entry
-// warp-uniform object cache, word mask (G3/G4), adjacent-lane
-// merge, insert of (pc id, sector) -> word mask into the warp's shared-memory
-// table (emitted as keys when the source warp changes, P:325's OR being
-// idempotent), and the instruction's distinct-sector / span test for the
-// misalignment indicator (G24).  Boolean conditions use bitwise
-// operators so they compile to predicates rather than branches.
+// The kernel is issue-bound, so it is written for instruction economy:
+//  * addresses are handled as 32-bit offsets inside the view's uniform 4 GiB
+//    window H = (space, addr[32,48));
+//  * object resolution goes through a two-entry warp-uniform cache
+//    of window intervals: either the part of an object inside the window, with
+//    the sector id of its first sector and the allowed words of its partial
+//    last sector (G9), or the gap between two objects.  A lane's test is one
+//    subtraction and one compare; its sector id g one shift and one add;
+//  * word mask (G3/G4): ((1 << words) - 1) << first word;
+//  * pre-dedup (P:325's OR is idempotent): lanes holding the same sector merge
+//    into the run's first lane; each lane then keeps, in registers, the last
+//    (pc id, sector) -> mask of each of two pc slots and emits a key only when
+//    an entry is replaced (A[row][k..k+7] of Listing 1 hit the same lane's
+//    entry for 8 consecutive k) or the source warp changes.  Keys go through a
+//    256-entry per-warp shared-memory stage flushed with one global atomic;
+//  * the misalignment test of the instruction (G24) counts sector
+//    changes with one ballot when the offsets are non-decreasing.
 #include "decode_common.cuh"
 
 namespace thermo {
+
+// one interval of a 4 GiB window: [blo, blo + bn) in 32-bit offsets
+struct WinEnt {
+  uint32_t H;       // window id (space << 16 | addr[32,48)); 0xFFFFFFFF = empty
+  uint32_t blo, bn;
+  uint32_t sbase;   // sector id of the sector at blo (objects)
+  uint32_t tail_s;  // offset of the object's partial last sector, 1 if none
+  uint32_t tail_m;  // its allowed words
+  int oid;          // object index, -1 for a gap
+};
+
+// the interval of window H holding the sector at offset xs (xs % 32 == 0)
+__device__ __forceinline__ WinEnt win_lookup(const ull* s_lo, const ull* s_hi, const ull* s_soff, uint32_t n,
+                                             int steps, uint32_t H, uint32_t xs) {
+  const ull wlo = (ull)H << 32, wend = wlo + (1ull << 32);
+  const ull X = wlo | xs;
+  int i = -1;  // last object with lo <= X
+  {
+    uint32_t lo = 0, hi = n;
+    for (int k = 0; k < steps; ++k) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const bool le = s_lo[mid] <= X;
+      lo = le ? mid : lo;
+      hi = le ? hi : mid;
+    }
+    if (n > 0 && s_lo[lo] <= X) i = (int)lo;
+  }
+  WinEnt e;
+  e.H = H;
+  e.tail_s = 1;
+  e.tail_m = 0xFFu;
+  ull a, b;
+  if (i >= 0 && X < s_hi[i]) {  // a sector of object i
+    const ull olo = s_lo[i], ohi = s_hi[i];
+    const ull ohi32 = (ohi + 31) & ~31ull;
+    a = olo > wlo ? olo : wlo;
+    b = ohi32 < wend ? ohi32 : wend;
+    e.oid = i;
+    e.sbase = (uint32_t)(s_soff[i] + ((a - olo) >> 5));
+    const ull ts = ohi & ~31ull;
+    if ((ohi & 31) && ts >= wlo && ts < wend) {
+      e.tail_s = (uint32_t)(ts - wlo);
+      e.tail_m = (1u << (((uint32_t)(ohi & 31) + 3) >> 2)) - 1u;
+    }
+  } else {  // the gap between objects i and i + 1
+    const ull glo = i >= 0 ? ((s_hi[i] + 31) & ~31ull) : 0ull;
+    const ull ghi = (uint32_t)(i + 1) < n ? s_lo[i + 1] : ~0ull;
+    a = glo > wlo ? glo : wlo;
+    b = ghi < wend ? ghi : wend;
+    e.oid = -1;
+    e.sbase = 0;
+  }
+  e.blo = (uint32_t)(a - wlo);
+  const ull len = b > a ? b - a : 0;
+  e.bn = len > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)len;  // xs - blo <= 0xFFFFFFE0 then always passes
+  return e;
+}
+
+__device__ __forceinline__ bool win_has(const WinEnt& e, uint32_t H, uint32_t xs) {
+  return (e.H == H) & (xs - e.blo < e.bn);
+}
+
+// full key of a lane entry (pc id << 32 | g) -> mask: [g][launch, warp][pc id][mask]
+__device__ __forceinline__ ull entry_key(ull c, uint32_t m, ull tag, uint32_t SH, uint32_t P) {
+  return ((((c & 0xFFFFFFFFull) << SH) | (tag << P) | (c >> 32)) << 8) | m;
+}
 
 template <int MINB>
 __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs a) {
@@ -24,23 +101,31 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   const int wib = threadIdx.x >> 5;
   int steps = 0;
   while ((1u << steps) < nobj) ++steps;
-  const uint32_t LW = a.kl.L + a.kl.W, P = a.kl.P, W = a.kl.W;
+  const uint32_t P = a.kl.P, W = a.kl.W;
+  const uint32_t SH = a.kl.L + a.kl.W + P;
   const uint32_t max_launches = a.max_launches, max_warps = a.max_warps;
   ull* const gkeys = a.keys;
   ull* const gnk = &a.ctr->n_keys;
+  Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0};
 
-  WarpTable tab;
-  tab.init(sm.warp + wib * kWarpRegion, lane);
   InstrCache icache;
   icache.init();
-
-  ull n_mapped = 0, n_unmapped = 0;
+  uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
-  // warp-uniform object cache: [lo, hi) and sector base (soff - lo/32) of two objects
-  ull olo0 = 1, ohi0 = 0, ob0 = 0, olo1 = 1, ohi1 = 0, ob1 = 0;
-  int oi0 = -1, oi1 = -1;
-  bool last1 = false;                                                // entry 1 used last
+  WinEnt e0, e1;
+  e0.H = e1.H = 0xFFFFFFFFu;
+  e0.blo = e1.blo = 0;
+  e0.bn = e1.bn = 0;
+  e0.sbase = e1.sbase = 0;
+  e0.tail_s = e1.tail_s = 1;
+  e0.tail_m = e1.tail_m = 0xFFu;
+  e0.oid = e1.oid = -1;
+  bool last1 = false;
   uint32_t ps0 = 0xFFFFFFFFu, pi0 = 0, ps1 = 0xFFFFFFFFu, pi1 = 0;  // site -> pc id cache
+  // this lane's dedup entries, slot = pc id & 1: (pc id << 32 | g) -> mask
+  ull c0 = 0, c1 = 0;
+  uint32_t m0 = 0, m1 = 0;
+  ull tag = 0;  // (launch << W | warp) of the entries (uniform)
 
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -68,9 +153,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       const bool ok0 = (l2s <= 4) & (((y0 >> 19) & 3u) != 3u) & (((y0 >> 21) & 3u) != 3u) & ((y0 >> 24) == 0) &
                        (launch0 < max_launches) & (z0 < max_warps);
       const uint32_t size = 1u << l2s;
-      // uniform instruction, no sector straddle, no 2^48 overflow risk
-      const bool odd = act & ((cur.z != z0) | (cur.w != w0) | (((cur.y ^ y0) & 0xFF7F0000u) != 0) |
-                              ((cur.x & 31u) + size > 32u) | ((cur.y & 0xFFFFu) == 0xFFFFu));
+      const uint32_t x = cur.x;
+      // uniform instruction (upper address bits included), no sector straddle
+      const bool odd = act & ((cur.z != z0) | (cur.w != w0) | (((cur.y ^ y0) & 0xFF7FFFFFu) != 0) |
+                              ((x & 31u) + size > 32u));
       if (!ok0 || __ballot_sync(FULL, odd) != 0) {
         if (lane == 0) {  // defer the view to the general kernel
           const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);
@@ -80,54 +166,59 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         p = pn;
         continue;
       }
-      // ---- object of lane 0's sector: two-entry uniform cache; lanes verify ----
-      const ull spc = (ull)((y0 >> 21) & 3u) << 48;
-      const ull lo = spc | ((ull)(cur.y & 0xFFFFu) << 32) | cur.x;  // space | byte address
-      const ull xs = lo & ~31ull;                                   // sector start
-      const ull x0 = __shfl_sync(FULL, xs, 0);
-      const bool in0 = (x0 >= olo0) & (x0 < ohi0), in1 = (x0 >= olo1) & (x0 < ohi1);
-      if (!(in0 | in1)) {  // uniform miss: replace the entry not used last
-        const int o = obj_lookup(sm.lo, sm.hi, nobj, steps, x0);
-        const ull nlo = o >= 0 ? sm.lo[o] : 1, nhi = o >= 0 ? sm.hi[o] : 0;
-        const ull nb = o >= 0 ? sm.soff[o] - (sm.lo[o] >> 5) : 0;
-        if (last1) { olo0 = nlo; ohi0 = nhi; ob0 = nb; oi0 = o; last1 = false; }
-        else { olo1 = nlo; ohi1 = nhi; ob1 = nb; oi1 = o; last1 = true; }
+      // ---- interval of lane 0's sector (uniform cache), lanes test theirs ----
+      const uint32_t H = ((y0 >> 5) & 0x30000u) | (y0 & 0xFFFFu);  // space << 16 | addr[32,48)
+      const uint32_t xs = x & ~31u;
+      const uint32_t xs0 = __shfl_sync(FULL, xs, 0);
+      const bool h0 = win_has(e0, H, xs0), h1 = win_has(e1, H, xs0);
+      if (!(h0 | h1)) {  // uniform miss: replace the entry not used last
+        const WinEnt ne = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs0);
+        if (last1) { e0 = ne; last1 = false; } else { e1 = ne; last1 = true; }
       } else {
-        last1 = !in0;
+        last1 = !h0;
       }
-      const ull wlo = last1 ? olo1 : olo0;
-      ull ohi = last1 ? ohi1 : ohi0, ob = last1 ? ob1 : ob0;
-      const int oiw = last1 ? oi1 : oi0;
-      bool mapped = (xs >= wlo) & (xs < ohi);
-      if (__ballot_sync(FULL, act & !mapped)) {  // lanes outside lane 0's object (rare)
-        if (act & !mapped) {
-          const int o = obj_lookup(sm.lo, sm.hi, nobj, steps, xs);
-          mapped = o >= 0;
-          if (mapped) { ohi = sm.hi[o]; ob = sm.soff[o] - (sm.lo[o] >> 5); }
+      uint32_t blo = last1 ? e1.blo : e0.blo;
+      uint32_t sbase = last1 ? e1.sbase : e0.sbase;
+      uint32_t tail_s = last1 ? e1.tail_s : e0.tail_s, tail_m = last1 ? e1.tail_m : e0.tail_m;
+      const int oid0 = last1 ? e1.oid : e0.oid;
+      int oid = oid0;
+      const bool inw = xs - blo < (last1 ? e1.bn : e0.bn);
+      if (__ballot_sync(FULL, act & !inw)) {  // lanes outside lane 0's interval (rare)
+        if (act & !inw) {
+          const WinEnt le = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs);
+          blo = le.blo; sbase = le.sbase; tail_s = le.tail_s; tail_m = le.tail_m; oid = le.oid;
         }
       }
-      // ---- word mask, restricted to the object's words (G9) ----
-      const uint32_t wa = (cur.x >> 2) & 7u, wb = ((cur.x + size - 1u) >> 2) & 7u;
-      const uint32_t ma = act ? ((0xFFu << wa) & (0xFFu >> (7u - wb))) : 0u;
-      const ull lim = ohi - xs;
-      const uint32_t allow = lim >= 32 ? 0xFFu : ((1u << ((uint32_t)(lim + 3) >> 2)) - 1u);
-      const uint32_t fa = (act & mapped) ? (ma & allow) : 0u;
-      const uint32_t g = (uint32_t)((xs >> 5) + ob);
+      // ---- word mask (P:324), restricted to the object's words (G9) ----
+      const uint32_t words = ((x & 3u) + size + 3u) >> 2;
+      const uint32_t ma = act ? (((1u << words) - 1u) << ((x >> 2) & 7u)) : 0u;
+      const uint32_t fa = (oid >= 0) ? (ma & (xs == tail_s ? tail_m : 0xFFu)) : 0u;
       if (launch0 != cur_launch) {
-        flush_launch_ctr(a.launch_ctr, cur_launch, n_unmapped, n_mapped);
+        if (cur_launch != 0xFFFFFFFFu) {
+          const uint32_t um = __reduce_add_sync(FULL, lane_unmapped), mm = __reduce_add_sync(FULL, lane_mapped);
+          if (lane == 0 && (um | mm)) {
+            atomicAdd(&a.launch_ctr[2 * cur_launch], (ull)um);
+            atomicAdd(&a.launch_ctr[2 * cur_launch + 1], (ull)mm);
+          }
+        }
+        lane_mapped = lane_unmapped = 0;
         cur_launch = launch0;
       }
-      n_mapped += __popc(fa);
-      n_unmapped += __popc(ma) - __popc(fa);
-      // ---- keys: adjacent-lane merge, then the warp's dedup table ----
+      const uint32_t pf = __popc(fa);
+      lane_mapped += pf;
+      lane_unmapped += __popc(ma) - pf;
+      // ---- keys: adjacent-lane merge, then this lane's (pc id, sector) entries ----
       bool has = fa != 0;
       uint32_t mk = fa;
+      const uint32_t g = sbase + ((xs - blo) >> 5);
       adjacent_merge32(g, mk, has, lane);
       if (__any_sync(FULL, has)) {
         const ull lw = ((ull)launch0 << W) | z0;
-        if ((lw != tab.tag) | (tab.count > (uint32_t)kTabFlush)) {
-          tab.flush(gkeys, gnk, LW, P, lane);
-          tab.tag = lw;
+        if (lw != tag) {  // new source warp: every entry leaves as a key
+          STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
+          STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
+          m0 = m1 = 0;
+          tag = lw;
         }
         uint32_t pcid = 0;
         if (a.track_pc) {
@@ -143,45 +234,55 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
           }
           pcid = pcid < a.pcmap.max_pcs ? pcid : 0u;  // overflow is reported at build (ERANGE)
         }
-        bool fresh = false;
-        if (has) fresh = tab.insert(((ull)pcid << 32) | g, mk);
-        tab.count += __popc(__ballot_sync(FULL, fresh));
+        const ull ck = ((ull)pcid << 32) | g;
+        const bool s1 = pcid & 1u;
+        const ull co = s1 ? c1 : c0;
+        const uint32_t mo = s1 ? m1 : m0;
+        const bool hit = co == ck;
+        // a replaced entry leaves as a key
+        STAGE_PUSH(st, has & !hit & (mo != 0), entry_key(co, mo, tag, SH, P), gkeys, gnk);
+        if (has) {
+          const uint32_t mn = hit ? (mo | mk) : mk;
+          if (s1) { c1 = ck; m1 = mn; } else { c0 = ck; m0 = mn; }
+        }
       }
       // ---- instruction statistics (G24) ----
       const uint32_t fa0 = __shfl_sync(FULL, fa, 0);
-      const uint32_t xl0 = __shfl_sync(FULL, cur.x, 0);
-      const uint32_t wa0 = (xl0 >> 2) & 7u;
-      if ((oiw >= 0) & ((fa0 >> wa0) & 1u)) {  // lane 0's first word is mapped (warp-uniform)
-        // offsets from lane 0 (32-bit when the instruction spans < 2 GiB, else the 64-bit path)
-        const ull rel64 = lo - __shfl_sync(FULL, lo, 0);
-        const uint32_t rel = (uint32_t)rel64;
-        const uint32_t prel = __shfl_up_sync(FULL, rel, 1);
-        const bool down = act & (lane > 0) & (((rel64 >> 31) != 0) | (rel < prel));
+      const uint32_t x0 = __shfl_sync(FULL, x, 0);
+      if ((oid0 >= 0) & ((fa0 >> ((x0 >> 2) & 7u)) & 1u)) {  // lane 0's first word is mapped (uniform)
+        const uint32_t px = __shfl_up_sync(FULL, x, 1);
+        const bool down = act & (lane > 0) & (x < px);
         uint32_t distinct;
-        bool mis;
+        ull span;
         if (__ballot_sync(FULL, down) == 0) {
-          // monotone starts, uniform size: count sector changes; span = rel(last) + size
-          const uint32_t s0 = xl0 & 31u;  // lane 0's byte offset in its sector
-          const uint32_t sec = (rel + s0) >> 5, psec = (prel + s0) >> 5;
-          distinct = __popc(__ballot_sync(FULL, act & ((lane == 0) | (sec != psec))));
-          const uint32_t span = __shfl_sync(FULL, rel, len - 1) + size;
-          mis = distinct > (span + 31) / 32;
+          // non-decreasing offsets in one window: count sector changes; span = last - first + size
+          distinct = __popc(__ballot_sync(FULL, act & ((lane == 0) | ((x >> 5) != (px >> 5)))));
+          span = (ull)(__shfl_sync(FULL, x, len - 1) - x0) + size;
         } else {
-          const unsigned m = __match_any_sync(FULL, act ? (lo >> 5) : (0xFFFF000000000000ull | (ull)lane));
+          const unsigned m = __match_any_sync(FULL, act ? (x >> 5) : (0xF8000000u | (uint32_t)lane));
           distinct = __popc(__ballot_sync(FULL, act & (__ffs(m) - 1 == lane)));
-          const ull mn = warp_min64(act ? lo : ~0ull);
-          const ull mx = warp_max64(act ? lo : 0ull) + size - 1;
-          mis = distinct > (mx - mn + 1 + 31) / 32;
+          const uint32_t mn = __reduce_min_sync(FULL, act ? x : 0xFFFFFFFFu);
+          const uint32_t mx = __reduce_max_sync(FULL, act ? x : 0u);
+          span = (ull)(mx - mn) + size;
         }
-        icache.add(launch0 * nobj + (uint32_t)oiw + 1u, mis, sm.ikey, sm.ival, a.instr_ctr, lane);
+        icache.add(launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, sm.ikey, sm.ival,
+                   a.instr_ctr, lane);
       }
       cur = nxt;
       p = pn;
     }
   }
-  tab.flush(gkeys, gnk, LW, P, lane);
+  STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
+  STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
+  st.flush(gkeys, gnk, lane);
   icache.drain(sm.ikey, sm.ival, a.instr_ctr, lane);
-  flush_launch_ctr(a.launch_ctr, cur_launch, n_unmapped, n_mapped);
+  if (cur_launch != 0xFFFFFFFFu) {
+    const uint32_t um = __reduce_add_sync(FULL, lane_unmapped), mm = __reduce_add_sync(FULL, lane_mapped);
+    if (lane == 0 && (um | mm)) {
+      atomicAdd(&a.launch_ctr[2 * cur_launch], (ull)um);
+      atomicAdd(&a.launch_ctr[2 * cur_launch + 1], (ull)mm);
+    }
+  }
   smem_flush_instr(sm, a.instr_ctr);
 }
 
@@ -203,15 +304,6 @@ static void launch_decode_t(const DecodeArgs& a, int num_sms, cudaStream_t s, si
 }
 
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
-  static int batch = -1;
-  if (batch < 0) {
-    const char* e = getenv("THERMO_DECODE");
-    batch = (e && e[0] == 'b') ? 1 : 0;
-  }
-  if (batch) {
-    launch_decode_batch(a, num_sms, s);
-    return;
-  }
   const size_t smem = decode_smem(a);
   static int minb = -1;
   if (minb < 0) {

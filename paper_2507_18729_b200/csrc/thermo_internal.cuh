@@ -84,14 +84,13 @@ struct DecodeArgs {
   DevCounters* ctr;
   ull* instr_ctr;         // [max_launches * n_obj * 2] (instrs, misaligned)
   ull* launch_ctr;        // [max_launches * 2] (unmapped words, mapped word accesses)
-  ull* deferred;          // [n] (p << 6 | len) of non-uniform views
+  ull* deferred;          // [n] p << 7 | stats_only << 6 | len of deferred views
 };
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------
 void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_ranges, ull* heads,
                        cudaStream_t s);
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
-void launch_decode_batch(const DecodeArgs& a, int num_sms, cudaStream_t s);
 void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s);
 
 // onesweep LSD radix sort of u64 keys on bits [lo_bit, lo_bit + nbits)

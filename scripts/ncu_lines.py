@@ -19,7 +19,11 @@ hdr = None
 agg = {}
 src = {}
 cur = None
+fname = "?"
 for r in rows:
+    if r and r[0] == "File Path":
+        fname = r[1].rsplit("/", 1)[-1]
+        continue
     if r and r[0] == "Line No":
         hdr = r
         ie = hdr.index("Instructions Executed")
@@ -28,7 +32,7 @@ for r in rows:
     if hdr is None or len(r) < len(hdr) - 2:
         continue
     if r[0]:
-        cur = int(r[0]) if r[0].isdigit() else None
+        cur = (fname, int(r[0])) if r[0].isdigit() else None
         src[cur] = r[1]
         continue
     if cur is None or r[2] in ("...", ""):
@@ -43,4 +47,4 @@ ti = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print(f"total instructions {ti}, stall samples {ts}")
 for ln, (i, s) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
-    print(f"L{ln:5d} inst {100*i/ti:5.1f}%  stall {100*s/ts:5.1f}%  {src.get(ln, '')[:90]}")
+    print(f"{ln[0][:14]:>14}:{ln[1]:<4d} inst {100*i/ti:5.1f}%  stall {100*s/ts:5.1f}%  {src.get(ln, '')[:90]}")
