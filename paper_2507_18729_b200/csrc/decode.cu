@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
   const Smem sm = smem_setup(smem, a);
   const uint32_t nobj = a.obj.n;
   const int lane = threadIdx.x & 31;
+  const unsigned lane_lt = lanemask_lt();
   const int wib = threadIdx.x >> 5;
   int steps = 0;
   while ((1u << steps) < nobj) ++steps;

@@ -134,12 +134,13 @@ struct Stage {
   }
 };
 // push the lanes' keys for which HAS holds; KEY is evaluated only on them
+// (needs `lane_lt` = lanemask_lt() and `lane` in scope)
 #define STAGE_PUSH(st, HAS, KEY, gbuf, gcnt)                              \
   do {                                                                    \
     const bool has_ = (HAS);                                              \
     const unsigned b_ = __ballot_sync(FULL, has_);                        \
     if (b_) {                                                             \
-      if (has_) (st).s[(st).cnt + __popc(b_ & lanemask_lt())] = (KEY);    \
+      if (has_) (st).s[(st).cnt + __popc(b_ & lane_lt)] = (KEY);          \
       (st).cnt += __popc(b_);                                             \
       if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane); \
     }                                                                     \
@@ -209,11 +210,18 @@ struct InstrCache {
   uint32_t k0, k1, i0, m0, i1, m1;
   __device__ __forceinline__ void init() { k0 = k1 = 0; i0 = m0 = i1 = m1 = 0; }
   __device__ __forceinline__ void add(uint32_t key, bool mis, uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
-    if (key == k0) { ++i0; m0 += mis; return; }
-    if (key == k1) { ++i1; m1 += mis; return; }
-    if (k1 && lane == 0) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
-    k1 = k0; i1 = i0; m1 = m0;
-    k0 = key; i0 = 1; m0 = mis;
+    bool h0 = key == k0;
+    const bool h1 = key == k1;
+    if (!(h0 | h1)) {  // (warp-uniform) evict entry 1
+      if (k1 && lane == 0) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
+      k1 = k0; i1 = i0; m1 = m0;
+      k0 = key; i0 = 0; m0 = 0;
+      h0 = true;
+    }
+    i0 += h0;
+    m0 += h0 & mis;
+    i1 += h1;
+    m1 += h1 & mis;
   }
   __device__ __forceinline__ void drain(uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
     if (lane == 0) {

@@ -15,9 +15,9 @@
 //    subtraction and one compare; its sector id g one shift and one add;
 //  * word mask (G3/G4): ((1 << words) - 1) << first word;
 //  * pre-dedup (P:325's OR is idempotent): lanes holding the same sector merge
-//    into the run's first lane; each lane then keeps, in registers, the last
-//    (pc id, sector) -> mask of each of two pc slots and emits a key only when
-//    an entry is replaced (A[row][k..k+7] of Listing 1 hit the same lane's
+//    into the run's first lane; each lane then keeps, in registers, its two
+//    most recent (pc id, sector) -> mask entries and emits a key only when an
+//    entry is replaced (A[row][k..k+7] of Listing 1 hit the same lane's
 //    entry for 8 consecutive k) or the source warp changes.  Keys go through a
 //    256-entry per-warp shared-memory stage flushed with one global atomic;
 //  * the misalignment test of the instruction (G24) counts sector
@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   const Smem sm = smem_setup(smem, a);
   const uint32_t nobj = a.obj.n;
   const int lane = threadIdx.x & 31;
+  const unsigned lane_lt = lanemask_lt();
   const int wib = threadIdx.x >> 5;
   int steps = 0;
   while ((1u << steps) < nobj) ++steps;
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   e0.oid = e1.oid = -1;
   bool last1 = false;
   uint32_t ps0 = 0xFFFFFFFFu, pi0 = 0, ps1 = 0xFFFFFFFFu, pi1 = 0;  // site -> pc id cache
-  // this lane's dedup entries, slot = pc id & 1: (pc id << 32 | g) -> mask
+  // this lane's two most recent dedup entries: (pc id << 32 | g) -> mask
   ull c0 = 0, c1 = 0;
   uint32_t m0 = 0, m1 = 0;
   ull tag = 0;  // (launch << W | warp) of the entries (uniform)
@@ -234,16 +235,16 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
           }
           pcid = pcid < a.pcmap.max_pcs ? pcid : 0u;  // overflow is reported at build (ERANGE)
         }
+        // two-entry LRU of (pc id, sector) -> mask; entry 0 is the most recent
         const ull ck = ((ull)pcid << 32) | g;
-        const bool s1 = pcid & 1u;
-        const ull co = s1 ? c1 : c0;
-        const uint32_t mo = s1 ? m1 : m0;
-        const bool hit = co == ck;
+        const bool hit0 = c0 == ck, hit1 = c1 == ck;
         // a replaced entry leaves as a key
-        STAGE_PUSH(st, has & !hit & (mo != 0), entry_key(co, mo, tag, SH, P), gkeys, gnk);
+        STAGE_PUSH(st, has & !hit0 & !hit1 & (m1 != 0), entry_key(c1, m1, tag, SH, P), gkeys, gnk);
         if (has) {
-          const uint32_t mn = hit ? (mo | mk) : mk;
-          if (s1) { c1 = ck; m1 = mn; } else { c0 = ck; m0 = mn; }
+          const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : 0u);
+          if (!hit0) { c1 = c0; m1 = m0; }
+          c0 = ck;
+          m0 = mprev | mk;
         }
       }
       // ---- instruction statistics (G24) ----
