@@ -243,7 +243,8 @@ thermo_status thermo_register_objects(thermo_ctx *ctx, const thermo_object *objs
  * staged through pinned chunks with copies overlapped with decoding; the call
  * returns when the host buffer may be reused).  The first record starts an
  * instruction.  n == 0 is a no-op.  Errors: EINVAL (recs NULL with n > 0,
- * misaligned), ESTATE, ENOMEM, ECUDA.
+ * misaligned, a device pointer with n >= 2^32: split such traces at
+ * instr_start records), ESTATE, ENOMEM, ECUDA.
  */
 thermo_status thermo_ingest_trace(thermo_ctx *ctx, const thermo_record *recs, size_t n);
 

@@ -236,7 +236,9 @@ struct InstrCache {
 // shared-memory layout common to both decode kernels: object table, one
 // per-warp key staging buffer, the block's (launch, object) counter table and
 // (site -> pc id) cache
-constexpr size_t kWarpRegion = kStage * sizeof(ull);
+constexpr int kRingChunks = 8;          // fast kernel: per-warp record ring of 8 x 32 records (4 KB)
+constexpr int kAhead = 6;               // chunks in flight ahead of the current one (cp.async)
+constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16;
 struct Smem {
   ull *lo, *hi, *soff, *ival, *pc;
   unsigned char* warp;  // [kDecWarps][kWarpRegion]
@@ -251,7 +253,8 @@ __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs
   m.ival = m.soff + nobj;                   // [kInstrSlots][2]
   m.pc = m.ival + 2 * kInstrSlots;          // [kPcSlots]
   m.ikey = reinterpret_cast<uint32_t*>(m.pc + kPcSlots);
-  m.warp = reinterpret_cast<unsigned char*>(m.ikey + kInstrSlots);
+  // 16-byte aligned: the fast kernel's record ring is read with 128-bit loads
+  m.warp = reinterpret_cast<unsigned char*>(((uintptr_t)(m.ikey + kInstrSlots) + 15) & ~(uintptr_t)15);
   for (uint32_t i = threadIdx.x; i < nobj; i += blockDim.x) {
     m.lo[i] = a.obj.lo[i];
     m.hi[i] = a.obj.hi[i];

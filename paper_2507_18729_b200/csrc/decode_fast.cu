@@ -87,6 +87,18 @@ __device__ __forceinline__ bool win_has(const WinEnt& e, uint32_t H, uint32_t xs
   return (e.H == H) & (xs - e.blo < e.bn);
 }
 
+// record ring: chunk c = records [32c, 32c + 32) of the range (offsets from its
+// first record) lives in ring slot c % kRingChunks; lane l copies record
+// 32c + l with cp.async, zero-filled at or past the range end
+__device__ __forceinline__ void ring_issue(uint4* ring, const uint4* rbase, uint32_t c, uint32_t rlen, int lane) {
+  const uint32_t pos = c * 32 + lane;
+  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (pos & (kRingChunks * 32 - 1)));
+  const bool in = pos < rlen;
+  const uint4* src = rbase + (in ? pos : 0u);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 // full key of a lane entry (pc id << 32 | g) -> mask: [g][launch, warp][pc id][mask]
 __device__ __forceinline__ ull entry_key(ull c, uint32_t m, ull tag, uint32_t SH, uint32_t P) {
   return ((((c & 0xFFFFFFFFull) << SH) | (tag << P) | (c >> 32)) << 8) | m;
@@ -108,6 +120,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   ull* const gkeys = a.keys;
   ull* const gnk = &a.ctr->n_keys;
   Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0};
+  uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
 
   InstrCache icache;
   icache.init();
@@ -132,19 +145,25 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
 
   for (uint32_t r = gwarp; r < a.n_ranges; r += nwarps) {
-    const ull end = a.heads[r + 1];
-    ull p = a.heads[r];
-    uint4 cur = make_uint4(0, 0, 0, 0);
-    if (p + lane < end) cur = ld_stream(&a.recs[p + lane]);
-    while (p < end) {
-      // ---- view = one warp instruction: records [p, p + len) ----
+    const ull p0 = a.heads[r];
+    const uint32_t rlen = (uint32_t)(a.heads[r + 1] - p0);  // ingest calls hold < 2^32 records
+    const uint4* const rbase = a.recs + p0;
+    // keep kAhead chunks in flight ahead of the one holding the view (~3 KB per warp)
+    uint32_t issued = 0;
+    for (int k = 0; k <= kAhead; ++k) ring_issue(ring, rbase, issued++, rlen, lane);
+    uint32_t off = 0;  // the view's first record, from p0
+    while (off < rlen) {
+      if (issued <= (off >> 5) + kAhead) ring_issue(ring, rbase, issued++, rlen, lane);
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead - 1) : "memory");  // the view's 2 chunks landed
+      __syncwarp();
+      const uint32_t rem = rlen - off;
+      uint4 cur = make_uint4(0, 0, 0, 0);
+      if ((uint32_t)lane < rem) cur = ring[(off + lane) & (kRingChunks * 32 - 1)];
+      // ---- view = one warp instruction: records [off, off + len) ----
       const unsigned sb = __ballot_sync(FULL, (cur.y >> 23) & 1u) & ~1u;
-      const ull rem = end - p;
       uint32_t len = sb ? (uint32_t)(__ffs(sb) - 1) : 32u;
-      len = rem < len ? (uint32_t)rem : len;
-      const ull pn = p + len;
-      uint4 nxt = make_uint4(0, 0, 0, 0);
-      if (pn + lane < end) nxt = ld_stream(&a.recs[pn + lane]);  // next view, in flight during this one
+      len = rem < len ? rem : len;
+      const uint32_t offn = off + len;
 
       const bool act = lane < (int)len;
       const uint32_t y0 = __shfl_sync(FULL, cur.y, 0);
@@ -161,10 +180,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       if (!ok0 || __ballot_sync(FULL, odd) != 0) {
         if (lane == 0) {  // defer the view to the general kernel
           const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);
-          a.deferred[slot] = (p << 7) | len;
+          a.deferred[slot] = ((p0 + off) << 7) | len;
         }
-        cur = nxt;
-        p = pn;
+        off = offn;
         continue;
       }
       // ---- interval of lane 0's sector (uniform cache), lanes test theirs ----
@@ -269,9 +287,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         icache.add(launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, sm.ikey, sm.ival,
                    a.instr_ctr, lane);
       }
-      cur = nxt;
-      p = pn;
+      off = offn;
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // no copy may land in the next range's slots
+    __syncwarp();
   }
   STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
   STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);

@@ -15,7 +15,7 @@ using namespace thermo;
 
 namespace {
 
-constexpr ull kRangeLen = 2048;          // records per decode work range
+constexpr ull kRangeLen = 8192;          // records per decode work range
 constexpr ull kHostChunk = 1ull << 24;   // records per staged host chunk
 constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors)
 
@@ -448,6 +448,8 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
   } else {
     cudaGetLastError();
   }
+  if (on_device && n >= (1ull << 32))
+    return fail(ctx, THERMO_EINVAL, "a device-resident ingest call holds < 2^32 records (split at instr_start records)");
   // worst case: every record emits two keys (one per sector it touches)
   st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * (ull)n + 64, ctx->n_keys);
   if (st) return st;
