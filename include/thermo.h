@@ -207,16 +207,42 @@ uint32_t thermo_abi_version(void);
 thermo_status thermo_create(thermo_ctx **out, int device, void *stream, const thermo_config *cfg);
 
 /*
- * Multi-GPU (address-sharded) context: rank `rank` of `nranks`.  nccl_id is a
- * 128-byte ncclUniqueId produced by rank 0 and broadcast by the caller (e.g.
- * over a torch process group).  Every rank must issue the same sequence of
- * calls (collective semantics).  Each rank owns the sectors g with
- * (g >> 12) % nranks == rank.  Errors additionally: ENCCL.
+ * Multi-GPU (address-sharded) context: rank `rank` of `nranks`
+ * (1..64), one process per GPU.  nccl_id is a 128-byte ncclUniqueId made by
+ * rank 0 with thermo_nccl_unique_id and broadcast by the caller (e.g. over a
+ * torch.distributed group).  A sector's counts depend only on the records
+ * touching it (S:292-300 merge = OR, S:332 shard by sector), so:
+ *   - every rank ingests its own slice of the trace (split the trace at
+ *     instr_start records);
+ *   - thermo_build_heatmap and thermo_classify are COLLECTIVE: every rank
+ *     calls them, in the same order with the same arguments.  Build unifies
+ *     the (launch, pc) ids, moves each key to the owner of its sector --
+ *     rank (g >> 11) % nranks for global sector index g (2048-sector chunks)
+ *     -- in one all-to-all, counts the owned sectors, and sums the
+ *     histograms / counters over ranks;
+ *   - thermo_query_histogram, thermo_query_per_pc, thermo_classify and
+ *     thermo_get_stats (after a build) return job-wide results, identical on
+ *     every rank and bit-identical to one rank reducing the whole trace;
+ *   - thermo_query_heatmap returns this rank's partition: cells of sectors
+ *     owned by other ranks are 0, so the full rows are the element-wise sum
+ *     over ranks (thermo_sharding gives the chunk size).
+ * Errors additionally: ENCCL (sticky).  nranks == 1 is thermo_create.
  */
 thermo_status thermo_create_dist(thermo_ctx **out, int device, void *stream, const thermo_config *cfg,
                                  const void *nccl_id, int rank, int nranks);
-/* Writes a fresh 128-byte ncclUniqueId into out (rank 0 only). */
+/* Writes a fresh 128-byte ncclUniqueId into out128 (call on rank 0).  Errors: EINVAL, ENCCL. */
 thermo_status thermo_nccl_unique_id(void *out128);
+/*
+ * The same sharded mode inside one process on one device: creates nranks
+ * contexts (outs[0..nranks), each on its own new stream) whose collectives
+ * exchange through device-to-device copies.  Each context must be driven by
+ * its own host thread, because a collective call returns only when every
+ * rank has made it.  Used to run and test the P-rank algorithm on one GPU.
+ * Errors: EINVAL (nranks outside 1..64), ECUDA, ENOMEM.
+ */
+thermo_status thermo_create_local_shards(thermo_ctx **outs, int device, const thermo_config *cfg, int nranks);
+/* rank, nranks and the ownership chunk (sectors) of a context (1 rank: 0, 1). */
+thermo_status thermo_sharding(const thermo_ctx *ctx, int *rank, int *nranks, uint32_t *chunk_sectors);
 
 thermo_status thermo_destroy(thermo_ctx *ctx);
 

@@ -17,8 +17,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJDIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libthermo.so")
-SOURCES = ["decode.cu", "decode_fast.cu", "sort.cu", "segment.cu", "count.cu", "indicators.cu", "thermo_api.cu"]
-HEADERS = ["thermo_internal.cuh", "decode_common.cuh", os.path.join("..", "..", "include", "thermo.h")]
+SOURCES = ["decode.cu", "decode_fast.cu", "sort.cu", "segment.cu", "count.cu", "indicators.cu", "shard.cu", "thermo_api.cu"]
+HEADERS = ["thermo_internal.cuh", "decode_common.cuh", "shard.cuh", os.path.join("..", "..", "include", "thermo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(r.stderr)
             rebuilt = True
     if force or rebuilt or not os.path.exists(LIB):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

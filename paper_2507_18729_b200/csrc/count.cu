@@ -197,7 +197,8 @@ __device__ __forceinline__ void agg_add(uint32_t* s_hist, ull* g_hist, bool use_
 __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __restrict__ wc,
                                                           const uint32_t* __restrict__ sc, const ull* __restrict__ soff,
                                                           const ull* __restrict__ nwords, uint32_t nobj,
-                                                          ull* __restrict__ hist, ull total, int use_smem) {
+                                                          ull* __restrict__ hist, ull total, int use_smem,
+                                                          uint32_t rank, uint32_t nranks) {
   extern __shared__ uint32_t s_hist[];  // [nobj][2][33] when use_smem
   const uint32_t nb = nobj * 2 * kLevels;
   if (use_smem) {
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
   const ull stride = (ull)gridDim.x * blockDim.x;
   const ull nthreads = (total + 255) / 256 * 256;
   for (ull g = (ull)blockIdx.x * blockDim.x + threadIdx.x; g < nthreads; g += stride) {
-    const bool in = g < total;
+    const bool in = g < total && shard_owner(g, nranks) == rank;
     uint32_t o = in ? obj_of_sector(soff, nobj, g) : 0;
     const ull wl0 = in ? (g - soff[o]) * 8 : 0;
     const ull nwo = in ? nwords[o] : 0;
@@ -227,7 +228,8 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
 }
 
 void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj, const ull* obj_nwords,
-                        ull* hist, ull total_sectors, int num_sms, cudaStream_t s) {
+                        ull* hist, ull total_sectors, uint32_t rank, uint32_t nranks, int num_sms,
+                        cudaStream_t s) {
   const uint32_t nb = obj.n * 2 * kLevels;
   const int use_smem = nb * sizeof(uint32_t) <= 96 * 1024;
   size_t smem = use_smem ? nb * sizeof(uint32_t) : 0;
@@ -239,7 +241,7 @@ void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, Ob
   unsigned grid = (unsigned)std::min<ull>((total_sectors + 255) / 256, (ull)num_sms * 8);
   if (grid < 1) grid = 1;
   object_hist_kernel<<<grid, 256, smem, s>>>(word_cnt, sector_cnt, obj.soff, obj_nwords, obj.n, hist,
-                                              total_sectors, use_smem);
+                                              total_sectors, use_smem, rank, nranks);
 }
 
 // ---- a6: per-PC histograms ---------------------------------------------------------

@@ -91,6 +91,10 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   const uint32_t tile = blockIdx.x;
   const uint32_t o = (uint32_t)a.tile_obj[tile];
   const ull g0 = a.tile_first[tile], g1 = a.tile_end[tile];
+  if (shard_owner(g0, a.nranks) != a.rank) {  // another rank's tile (sharded mode)
+    if (mode == 0 && threadIdx.x < 4) a.tile_info[(ull)tile * 4 + threadIdx.x] = 0;  // identity of the sum
+    return;
+  }
   const ull soff = a.obj.soff[o];
   const ull nw = a.obj_nwords[o];
   const thermo_params& P = a.prm;
@@ -301,15 +305,59 @@ __global__ void indicator_finalize_kernel(IndicatorArgs a) {
   r[F_LABELS] = L;
 }
 
-void launch_indicators(const IndicatorArgs& a, int num_sms, cudaStream_t s) {
-  (void)num_sms;
+// sharded mode: per-object partial sums <-> reducible arrays
+__global__ void indicator_pack_kernel(ull* ind, uint32_t n, ull* sums, ull* maxs, ull* verify, int dir) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  ull* r = ind + (ull)o * kIndFields;
+  static constexpr int kSumF[6] = {F_T, F_TW, F_HOT, F_FS, F_SUMX, F_LE1};
+  if (dir == 0) {
+    if (sums) {
+      ull* d = sums + (ull)o * kIndSumFields;
+      for (int f = 0; f < 6; ++f) d[f] = r[kSumF[f]];
+      d[6] = r[F_SUMX2_LO] & 0xFFFFFFFFull; d[7] = r[F_SUMX2_LO] >> 32;
+      d[8] = r[F_SUMX2_HI] & 0xFFFFFFFFull; d[9] = r[F_SUMX2_HI] >> 32;
+      maxs[o] = r[F_MAXSEC];
+    }
+    if (verify) verify[o] = r[F_VERIFY];
+  } else {
+    if (sums) {
+      const ull* d = sums + (ull)o * kIndSumFields;
+      for (int f = 0; f < 6; ++f) r[kSumF[f]] = d[f];
+      const u128 v = (u128)d[6] + ((u128)d[7] << 32) + ((u128)d[8] << 64) + ((u128)d[9] << 96);
+      r[F_SUMX2_LO] = (ull)v;
+      r[F_SUMX2_HI] = (ull)(v >> 64);
+      r[F_MAXSEC] = maxs[o];
+    }
+    if (verify) r[F_VERIFY] = verify[o];
+  }
+}
+
+void launch_indicator_pack(ull* ind, uint32_t n, ull* sums, ull* maxs, ull* verify, int dir, cudaStream_t s) {
+  indicator_pack_kernel<<<(n + 127) / 128, 128, 0, s>>>(ind, n, sums, maxs, verify, dir);
+}
+
+void launch_indicator_tiles(const IndicatorArgs& a, int mode, cudaStream_t s) {
+  if (a.n_tiles) indicator_tile_kernel<<<a.n_tiles, kIndThreads, 0, s>>>(a, mode);
+}
+
+void launch_indicator_stitch(const IndicatorArgs& a, cudaStream_t s) {
   // obj_tile0: first tile of each object, derived from tile_obj on the host side
   // and stored right after tile_prev (see thermo_api.cu)
   const uint32_t* obj_tile0 = reinterpret_cast<const uint32_t*>(a.tile_prev + a.n_tiles);
-  if (a.n_tiles) indicator_tile_kernel<<<a.n_tiles, kIndThreads, 0, s>>>(a, 0);
   indicator_stitch_kernel<<<a.obj.n, 256, 0, s>>>(a, obj_tile0);
-  if (a.n_tiles) indicator_tile_kernel<<<a.n_tiles, kIndThreads, 0, s>>>(a, 1);
+}
+
+void launch_indicator_finalize(const IndicatorArgs& a, cudaStream_t s) {
   indicator_finalize_kernel<<<(a.obj.n + 127) / 128, 128, 0, s>>>(a);
+}
+
+void launch_indicators(const IndicatorArgs& a, int num_sms, cudaStream_t s) {
+  (void)num_sms;
+  launch_indicator_tiles(a, 0, s);
+  launch_indicator_stitch(a, s);
+  launch_indicator_tiles(a, 1, s);
+  launch_indicator_finalize(a, s);
 }
 
 }  // namespace thermo

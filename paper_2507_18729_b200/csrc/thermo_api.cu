@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "shard.cuh"
 #include "thermo_internal.cuh"
 
 using namespace thermo;
@@ -17,7 +18,8 @@ namespace {
 
 constexpr ull kRangeLen = 8192;          // records per decode work range
 constexpr ull kHostChunk = 1ull << 24;   // records per staged host chunk
-constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors)
+constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors) = 1 << kShardShift
+static_assert(kTileSectors == (1ull << kShardShift), "a tile is one ownership chunk");
 
 int bit_width(ull x) { return x ? 64 - __builtin_clzll(x) : 0; }
 ull next_pow2(ull x) {
@@ -102,6 +104,21 @@ struct thermo_ctx {
   ull records = 0;
   float ms_ingest = 0, ms_build = 0, ms_classify = 0;
   bool hist_valid = false;
+
+  // sharded mode (row e, shard.cu); comm == nullptr: one rank
+  Comm* comm = nullptr;
+  ull n_exch = 0;                            // keys [0, n_exch) are this rank's own (exchanged)
+  uint32_t pc_mapped = 0;                    // local pc ids [0, pc_mapped) have job-wide ids
+  std::vector<uint32_t> glob_sites;          // job-wide pc id -> site
+  std::unordered_map<uint32_t, uint32_t> glob_index;
+  uint32_t* d_pcmap = nullptr;               // local pc id -> job-wide id [max_pcs]
+  uint32_t* d_site_glob = nullptr;           // job-wide pc id -> site [max_pcs]
+  ull* d_tmp = nullptr;                      // [256] small scratch
+  ull* d_red = nullptr;                      // reduction scratch
+  size_t red_cap = 0;
+  ull *d_instr_g = nullptr, *d_launch_g = nullptr;  // job-wide copies (after build)
+  ull h_ctr_g[17] = {};                      // job-wide DevCounters + records (after build)
+  bool have_glob = false;
 };
 
 namespace {
@@ -131,6 +148,15 @@ cudaError_t dalloc(T** p, size_t n) {
 void dfree(void* p) {
   if (p) cudaFree(p);
 }
+
+thermo_status comm_fail(thermo_ctx* ctx, int rc) {
+  return fail(ctx, rc == 2 ? THERMO_ENCCL : THERMO_ECUDA, "exchange: " + ctx->comm->err);
+}
+#define DCK(call)                      \
+  do {                                 \
+    const int rc_ = (call);            \
+    if (rc_) return comm_fail(ctx, rc_); \
+  } while (0)
 
 ObjTable obj_table(thermo_ctx* c) { return ObjTable{c->d_lo, c->d_hi, c->d_soff, (uint32_t)c->reg.size()}; }
 
@@ -214,6 +240,107 @@ thermo_status sync_counts(thermo_ctx* ctx) {
   return THERMO_OK;
 }
 
+// =============================================================================
+// sharded mode, start of a build: consistent error flags, job-wide pc ids,
+// and the exchange of the keys decoded since the last build to their owners
+thermo_status dist_exchange(thermo_ctx* ctx, const DevCounters& hc) {
+  Comm* c = ctx->comm;
+  cudaStream_t s = ctx->stream;
+  const uint32_t P = (uint32_t)c->nranks;
+  ull flags[2] = {hc.out_of_range, ctx->cfg.track_pc ? hc.pc_overflow : 0ull};
+  CK(cudaMemcpyAsync(ctx->d_tmp, flags, sizeof flags, cudaMemcpyHostToDevice, s));
+  DCK(c->allreduce(ctx->d_tmp, 2, false, s));
+  CK(cudaMemcpyAsync(flags, ctx->d_tmp, sizeof flags, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (flags[0]) return fail(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths (job-wide)");
+  if (flags[1]) return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
+  // ---- job-wide pc ids: union of the new sites of every rank, appended in sorted order ----
+  if (ctx->cfg.track_pc) {
+    const uint32_t npc = (uint32_t)std::min<ull>(hc.pc_count, ctx->cfg.max_pcs);
+    std::vector<uint32_t> mine(npc - ctx->pc_mapped);
+    if (!mine.empty())
+      CK(cudaMemcpy(mine.data(), ctx->d_site_of + ctx->pc_mapped, mine.size() * 4, cudaMemcpyDeviceToHost));
+    ull cnt = mine.size();
+    std::vector<ull> cnts(P);
+    DCK(c->allgather_host(&cnt, sizeof cnt, cnts.data(), s));
+    const ull mx = *std::max_element(cnts.begin(), cnts.end());
+    if (mx) {
+      std::vector<uint32_t> pad(mx, 0xFFFFFFFFu), all(mx * P);
+      std::copy(mine.begin(), mine.end(), pad.begin());
+      DCK(c->allgather_host(pad.data(), mx * 4, all.data(), s));
+      std::vector<uint32_t> fresh;
+      for (uint32_t v : all)
+        if (v != 0xFFFFFFFFu && !ctx->glob_index.count(v)) fresh.push_back(v);
+      std::sort(fresh.begin(), fresh.end());
+      fresh.erase(std::unique(fresh.begin(), fresh.end()), fresh.end());
+      for (uint32_t v : fresh) {
+        ctx->glob_index[v] = (uint32_t)ctx->glob_sites.size();
+        ctx->glob_sites.push_back(v);
+      }
+      if (ctx->glob_sites.size() > ctx->cfg.max_pcs)
+        return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
+      std::vector<uint32_t> map(mine.size());
+      for (size_t i = 0; i < mine.size(); ++i) map[i] = ctx->glob_index[mine[i]];
+      if (!map.empty())
+        CK(cudaMemcpy(ctx->d_pcmap + ctx->pc_mapped, map.data(), map.size() * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(ctx->d_site_glob, ctx->glob_sites.data(), ctx->glob_sites.size() * 4, cudaMemcpyHostToDevice));
+      ctx->pc_mapped = npc;
+    }
+  }
+  // ---- keys [n_exch, n_keys) -> owners (one all-to-all) ----
+  const ull n_new = ctx->n_keys - ctx->n_exch;
+  if (ctx->sw.alt_cap < n_new) {
+    dfree(ctx->sw.alt);
+    ctx->sw.alt_cap = n_new + n_new / 8 + 1024;
+    CK(dalloc(&ctx->sw.alt, ctx->sw.alt_cap));
+  }
+  std::vector<ull> scnt(P), sdispl(P, 0), mat((size_t)P * P), rcnt(P), rdispl(P, 0);
+  cudaError_t e = shard_partition(ctx->d_keys + ctx->n_exch, n_new, ctx->kl, P,
+                                  ctx->cfg.track_pc ? ctx->d_pcmap : nullptr, ctx->sw.alt, ctx->d_tmp, scnt.data(),
+                                  ctx->num_sms, s);
+  if (e) return fail(ctx, THERMO_ECUDA, std::string("shard partition: ") + cudaGetErrorString(e));
+  ctx->launches += 2;
+  DCK(c->allgather_host(scnt.data(), P * sizeof(ull), mat.data(), s));
+  ull total = 0;
+  for (uint32_t q = 0; q < P; ++q) {
+    rcnt[q] = mat[(size_t)q * P + ctx->rank];
+    rdispl[q] = total;
+    total += rcnt[q];
+    if (q) sdispl[q] = sdispl[q - 1] + scnt[q - 1];
+  }
+  thermo_status st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_exch + total + 64, ctx->n_exch);
+  if (st) return st;
+  DCK(c->alltoallv(ctx->sw.alt, scnt.data(), sdispl.data(), ctx->d_keys + ctx->n_exch, rcnt.data(), rdispl.data(), s));
+  CK(cudaStreamSynchronize(s));
+  ctx->n_keys = ctx->n_exch + total;
+  ctx->n_exch = ctx->n_keys;
+  CK(cudaMemcpy(&ctx->d_ctr->n_keys, &ctx->n_keys, sizeof(ull), cudaMemcpyHostToDevice));  // later ingests append
+  return THERMO_OK;
+}
+
+// sharded mode, end of a build: job-wide histograms and counters
+thermo_status dist_combine(thermo_ctx* ctx) {
+  Comm* c = ctx->comm;
+  cudaStream_t s = ctx->stream;
+  const size_t n = ctx->reg.size();
+  DCK(c->allreduce(ctx->d_hist, n * 2 * kLevels, false, s));
+  if (ctx->cfg.track_pc && !ctx->glob_sites.empty())
+    DCK(c->allreduce(ctx->d_pchist, ctx->glob_sites.size() * 2 * kLevels, false, s));
+  const size_t ni = (size_t)ctx->cfg.max_launches * n * 2, nl = (size_t)ctx->cfg.max_launches * 2;
+  CK(cudaMemcpyAsync(ctx->d_instr_g, ctx->d_instr, ni * 8, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_launch_g, ctx->d_launch_ctr, nl * 8, cudaMemcpyDeviceToDevice, s));
+  DCK(c->allreduce(ctx->d_instr_g, ni, false, s));
+  DCK(c->allreduce(ctx->d_launch_g, nl, false, s));
+  static_assert(sizeof(DevCounters) == 16 * sizeof(ull), "DevCounters layout");
+  CK(cudaMemcpyAsync(ctx->d_tmp, ctx->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_tmp + 16, &ctx->records, sizeof(ull), cudaMemcpyHostToDevice, s));
+  DCK(c->allreduce(ctx->d_tmp, 17, false, s));
+  CK(cudaMemcpyAsync(ctx->h_ctr_g, ctx->d_tmp, 17 * sizeof(ull), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->have_glob = true;
+  return THERMO_OK;
+}
+
 }  // namespace
 
 // =============================================================================
@@ -272,7 +399,10 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
     cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->ev_used[i], cudaEventDisableTiming);
   }
-  if (dalloc(&ctx->d_ctr, 1) != cudaSuccess) { delete ctx; return THERMO_ENOMEM; }
+  if (dalloc(&ctx->d_ctr, 1) != cudaSuccess || dalloc(&ctx->d_tmp, 256) != cudaSuccess) {
+    thermo_destroy(ctx);
+    return THERMO_ENOMEM;
+  }
   cudaMemsetAsync(ctx->d_ctr, 0, sizeof(DevCounters), ctx->stream);
   *out = ctx;
   return THERMO_OK;
@@ -280,16 +410,56 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
 
 thermo_status thermo_create_dist(thermo_ctx** out, int device, void* stream, const thermo_config* cfg,
                                  const void* nccl_id, int rank, int nranks) {
-  if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks) return THERMO_EINVAL;
-  if (nranks == 1) return thermo_create(out, device, stream, cfg);
+  if (!out || !nccl_id || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) return THERMO_EINVAL;
   *out = nullptr;
-  return THERMO_ESTATE;  // address-sharded mode: see DESIGN.md "Multi-GPU" (next row)
+  thermo_status st = thermo_create(out, device, stream, cfg);
+  if (st || nranks == 1) return st;
+  thermo_ctx* ctx = *out;
+  std::string msg;
+  ctx->comm = make_nccl_comm(nccl_id, rank, nranks, &msg);
+  if (!ctx->comm) {
+    thermo_destroy(ctx);
+    *out = nullptr;
+    return THERMO_ENCCL;
+  }
+  ctx->rank = rank;
+  ctx->nranks = nranks;
+  return THERMO_OK;
+}
+
+thermo_status thermo_create_local_shards(thermo_ctx** outs, int device, const thermo_config* cfg, int nranks) {
+  if (!outs || nranks < 1 || nranks > kMaxRanks) return THERMO_EINVAL;
+  for (int r = 0; r < nranks; ++r) outs[r] = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    const thermo_status st = thermo_create(&outs[r], device, nullptr, cfg);
+    if (st) {
+      for (int q = 0; q < r; ++q) { thermo_destroy(outs[q]); outs[q] = nullptr; }
+      return st;
+    }
+  }
+  if (nranks > 1) {
+    std::vector<Comm*> comms = make_local_comms(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      outs[r]->comm = comms[r];
+      outs[r]->rank = r;
+      outs[r]->nranks = nranks;
+    }
+  }
+  return THERMO_OK;
 }
 
 thermo_status thermo_nccl_unique_id(void* out128) {
   if (!out128) return THERMO_EINVAL;
-  std::memset(out128, 0, 128);
-  return THERMO_ESTATE;
+  std::string msg;
+  return nccl_unique_id(out128, &msg) ? THERMO_ENCCL : THERMO_OK;
+}
+
+thermo_status thermo_sharding(const thermo_ctx* ctx, int* rank, int* nranks, uint32_t* chunk_sectors) {
+  if (!ctx) return THERMO_EINVAL;
+  if (rank) *rank = ctx->rank;
+  if (nranks) *nranks = ctx->nranks;
+  if (chunk_sectors) *chunk_sectors = 1u << kShardShift;
+  return THERMO_OK;
 }
 
 thermo_status thermo_destroy(thermo_ctx* ctx) {
@@ -303,7 +473,8 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_table, ctx->d_pctable, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->d_stage[0],
-                  ctx->d_stage[1]};
+                  ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
+                  ctx->d_launch_g};
   for (void* b : bufs) dfree(b);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_pinned[i]) cudaFreeHost(ctx->h_pinned[i]);
@@ -316,6 +487,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx->comm;
   delete ctx;
   return THERMO_OK;
 }
@@ -359,10 +531,14 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
     ctx->h_space[j] = o.space;
     const ull ns = (o.len + 31) / 32;
     obj_tile0[j] = (uint32_t)tile_obj.size();
-    for (ull t = 0; t < ns; t += kTileSectors) {
+    // tiles end at the object's end and at global multiples of kTileSectors,
+    // so that a tile lies in one ownership chunk of the sharded mode
+    for (ull t = soff; t < soff + ns;) {
+      const ull te = std::min(soff + ns, (t / kTileSectors + 1) * kTileSectors);
       tile_obj.push_back(j);
-      tile_first.push_back(soff + t);
-      tile_end.push_back(soff + std::min(ns, t + kTileSectors));
+      tile_first.push_back(t);
+      tile_end.push_back(te);
+      t = te;
     }
     soff += ns;
   }
@@ -412,6 +588,12 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   CK(dalloc(&ctx->d_pc_keys_tab, ctx->pc_cap));
   CK(dalloc(&ctx->d_pc_vals, ctx->pc_cap));
   CK(dalloc(&ctx->d_site_of, c.max_pcs));
+  if (ctx->comm) {
+    CK(dalloc(&ctx->d_pcmap, c.max_pcs));
+    CK(dalloc(&ctx->d_site_glob, c.max_pcs));
+    CK(dalloc(&ctx->d_instr_g, (size_t)c.max_launches * n * 2));
+    CK(dalloc(&ctx->d_launch_g, (size_t)c.max_launches * 2));
+  }
   ctx->state = 1;
   return thermo_reset(ctx);
 }
@@ -430,6 +612,11 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
   ctx->records = 0;
   ctx->state = 1;
   ctx->hist_valid = false;
+  ctx->n_exch = 0;
+  ctx->pc_mapped = 0;
+  ctx->glob_sites.clear();
+  ctx->glob_index.clear();
+  ctx->have_glob = false;
   return THERMO_OK;
 }
 
@@ -520,21 +707,31 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
   ctx->records += n;
   ctx->state = 2;
   ctx->hist_valid = false;
+  ctx->have_glob = false;
   return THERMO_OK;
 }
 
 thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32_t launch_filter) {
   thermo_status st = pre(ctx);
   if (st) return st;
-  if (ctx->state < 2) return fail(ctx, THERMO_ESTATE, "ingest a trace before build");
+  // (sharded: a rank may hold an empty slice; build is collective)
+  if (ctx->state < (ctx->comm ? 1 : 2)) return fail(ctx, THERMO_ESTATE, "ingest a trace before build");
   if (g < THERMO_WORD || g > THERMO_BOTH) return fail(ctx, THERMO_EINVAL, "bad granularity");
   if (launch_filter != THERMO_ALL_LAUNCHES && launch_filter >= ctx->cfg.max_launches)
     return fail(ctx, THERMO_EINVAL, "launch_filter beyond max_launches");
   DevCounters hc;
   CK(cudaMemcpyAsync(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
-  if (hc.out_of_range) return fail(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths");
-  if (ctx->cfg.track_pc && hc.pc_overflow) return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs");
+  if (ctx->comm) {  // sharded: job-wide checks, pc ids and the key exchange (collective)
+    st = dist_exchange(ctx, hc);
+    if (st) return st;
+  } else {
+    if (hc.out_of_range) return fail(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths");
+    if (ctx->cfg.track_pc && hc.pc_overflow)
+      return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs");
+  }
+  const uint32_t* site_tab = ctx->comm ? ctx->d_site_glob : ctx->d_site_of;
+  const ull n_pc = ctx->comm ? ctx->glob_sites.size() : hc.pc_count;
   const size_t n = ctx->reg.size();
   cudaStream_t s = ctx->stream;
   CK(cudaEventRecord(ctx->ev0, s));
@@ -564,7 +761,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       }
       CK(cudaEventRecord(ctx->evp[1], s));
       e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, kl, ctx->S_tot, launch_filter, ctx->seg, ctx->d_wc,
-                        ctx->d_sc, ctx->d_site_of, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
+                        ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
                         ctx->num_sms, s);
       if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
       ctx->launches += ctx->seg.launches;
@@ -606,7 +803,8 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->evp[2], s));
   // ---- a6 histograms ----
-  launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->num_sms, s);
+  launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->rank,
+                     ctx->nranks, ctx->num_sms, s);
   ctx->launches += 1;
   CK(cudaEventRecord(ctx->evp[3], s));
   if (ctx->cfg.track_pc && !pc_done) {
@@ -628,10 +826,10 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
         std::swap(ctx->pckeys_cap, ctx->swpc.alt_cap);
       }
       ctx->launches += 1;
-      launch_pc_hist_sorted(ctx->d_pckeys, ctx->n_pckeys, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
+      launch_pc_hist_sorted(ctx->d_pckeys, ctx->n_pckeys, kl, site_tab, launch_filter, ctx->d_wc, ctx->d_sc,
                             ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
     } else {
-      const ull bound = std::min<ull>(ctx->n_pckeys, std::max<ull>(1, hc.pc_count) * ctx->S_tot);
+      const ull bound = std::min<ull>(ctx->n_pckeys, std::max<ull>(1, n_pc) * ctx->S_tot);
       ull cap = next_pow2(std::max<ull>(1024, 2 * bound));
       if (ctx->pctable_cap < cap) {
         dfree(ctx->d_pctable);
@@ -641,7 +839,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       CK(cudaMemsetAsync(ctx->d_pctable, 0xFF, cap * 8, s));
       launch_hash_insert(ctx->d_pckeys, ctx->n_pckeys, ctx->d_pctable, cap - 1, 0, ctx->d_ctr, ctx->num_sms, s);
       ctx->launches += 2;
-      launch_pc_hist_hash(ctx->d_pctable, cap, kl, ctx->d_site_of, launch_filter, ctx->d_wc, ctx->d_sc,
+      launch_pc_hist_hash(ctx->d_pctable, cap, kl, site_tab, launch_filter, ctx->d_wc, ctx->d_sc,
                           ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
     }
   }
@@ -654,6 +852,10 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   ctx->launches += ctx->sw.launches + ctx->swpc.launches;
   ctx->sw.launches = ctx->swpc.launches = 0;
   (void)l0;
+  if (ctx->comm) {
+    st = dist_combine(ctx);
+    if (st) return st;
+  }
   DevCounters hc2;
   CK(cudaMemcpy(&hc2, ctx->d_ctr, sizeof hc2, cudaMemcpyDeviceToHost));
   if (hc2.hash_fail) return fail(ctx, THERMO_ECUDA, "hash table overflow");
@@ -713,11 +915,12 @@ thermo_status thermo_query_per_pc(thermo_ctx* ctx, thermo_granularity g, thermo_
   if (g != THERMO_WORD && g != THERMO_SECTOR) return fail(ctx, THERMO_EINVAL, "granularity must be WORD or SECTOR");
   DevCounters hc;
   CK(cudaMemcpy(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost));
-  const ull npc = std::min<ull>(hc.pc_count, ctx->cfg.max_pcs);
+  const ull npc = ctx->comm ? ctx->glob_sites.size() : std::min<ull>(hc.pc_count, ctx->cfg.max_pcs);
   std::vector<uint32_t> site(npc);
   std::vector<ull> hist(npc * 2 * kLevels);
   if (npc) {
-    CK(cudaMemcpy(site.data(), ctx->d_site_of, npc * 4, cudaMemcpyDeviceToHost));
+    if (ctx->comm) site = ctx->glob_sites;
+    else CK(cudaMemcpy(site.data(), ctx->d_site_of, npc * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(hist.data(), ctx->d_pchist, npc * 2 * kLevels * 8, cudaMemcpyDeviceToHost));
   }
   std::vector<uint32_t> ids;
@@ -762,15 +965,46 @@ thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, ther
   a.tile_first = ctx->d_tile_first;
   a.tile_end = ctx->d_tile_end;
   a.n_tiles = ctx->n_tiles;
-  a.instr_ctr = ctx->d_instr;
+  a.instr_ctr = ctx->comm ? ctx->d_instr_g : ctx->d_instr;
   a.max_launches = ctx->cfg.max_launches;
   a.launch_filter = ctx->built_filter;
   a.prm = p;
   a.ind = ctx->d_ind;
   a.tile_info = ctx->d_tile_info;
   a.tile_prev = ctx->d_tile_prev;
-  launch_indicators(a, ctx->num_sms, s);
-  ctx->launches += ctx->n_tiles ? 4 : 2;
+  a.rank = (uint32_t)ctx->rank;
+  a.nranks = (uint32_t)ctx->nranks;
+  if (!ctx->comm) {
+    launch_indicators(a, ctx->num_sms, s);
+    ctx->launches += ctx->n_tiles ? 4 : 2;
+  } else {
+    // sharded: each rank scans its own tiles; sums, maxima, tile summaries and
+    // verify counts are combined between the steps (collective)
+    Comm* c = ctx->comm;
+    const size_t need = n * kIndSumFields + n + 1;
+    if (ctx->red_cap < need) {
+      dfree(ctx->d_red);
+      ctx->d_red = nullptr;
+      ctx->red_cap = 0;
+      CK(dalloc(&ctx->d_red, need));
+      ctx->red_cap = need;
+    }
+    ull* sums = ctx->d_red;
+    ull* maxs = sums + n * kIndSumFields;
+    launch_indicator_tiles(a, 0, s);
+    launch_indicator_pack(ctx->d_ind, (uint32_t)n, sums, maxs, nullptr, 0, s);
+    DCK(c->allreduce(sums, n * kIndSumFields, false, s));
+    DCK(c->allreduce(maxs, n, true, s));
+    if (ctx->n_tiles) DCK(c->allreduce(ctx->d_tile_info, (size_t)ctx->n_tiles * 4, false, s));
+    launch_indicator_pack(ctx->d_ind, (uint32_t)n, sums, maxs, nullptr, 1, s);
+    launch_indicator_stitch(a, s);
+    launch_indicator_tiles(a, 1, s);
+    launch_indicator_pack(ctx->d_ind, (uint32_t)n, nullptr, nullptr, sums, 0, s);
+    DCK(c->allreduce(sums, n, false, s));
+    launch_indicator_pack(ctx->d_ind, (uint32_t)n, nullptr, nullptr, sums, 1, s);
+    launch_indicator_finalize(a, s);
+    ctx->launches += ctx->n_tiles ? 8 : 6;
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev1, s));
   std::vector<ull> ind(n * kIndFields);
@@ -807,7 +1041,12 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
     CK(cudaMemcpyAsync(lc.data(), ctx->d_launch_ctr, lc.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
   }
   CK(cudaStreamSynchronize(ctx->stream));
-  out->records = ctx->records;
+  if (ctx->comm && ctx->have_glob) {  // sharded, after a build: job-wide totals
+    CK(cudaMemcpy(lc.data(), ctx->d_launch_g, lc.size() * 8, cudaMemcpyDeviceToHost));
+    std::memcpy(&hc, ctx->h_ctr_g, sizeof hc);
+    hc.pc_count = ctx->glob_sites.size();
+  }
+  out->records = ctx->comm && ctx->have_glob ? ctx->h_ctr_g[16] : ctx->records;
   out->invalid = hc.invalid;
   out->out_of_range = hc.out_of_range;
   for (uint32_t la = 0; la < ctx->cfg.max_launches && !lc.empty(); ++la) {

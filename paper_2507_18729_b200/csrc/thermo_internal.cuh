@@ -55,6 +55,14 @@ struct PcMap {
   uint32_t max_pcs;
 };
 
+// ---- sector ownership in the sharded mode (shard.cu, row e) ---------------
+constexpr int kShardShift = 11;  // ownership chunk: 2048 sectors = one indicator tile
+constexpr int kMaxRanks = 64;
+// owner rank of global sector g (block-cyclic over 2048-sector chunks)
+__host__ __device__ __forceinline__ uint32_t shard_owner(unsigned long long g, uint32_t nranks) {
+  return nranks <= 1 ? 0u : (uint32_t)((g >> kShardShift) % nranks);
+}
+
 // ---- key layout -----------------------------------------------------------
 // key:     [ g : S ][ launch : L ][ warp : W ][ pcid : P ][ mask : 8 ]  (S+L+W+P <= 56)
 //          one stream carries the (sector, warp) and the (pc, sector) facts
@@ -140,9 +148,10 @@ void launch_count_hash(const ull* table, ull cap, KeyLayout kl, uint32_t launch_
                        uint32_t* sector_cnt, DevCounters* ctr, int num_sms, cudaStream_t s);
 
 // a6 histograms over dense arrays, per object
+// (sharded mode: only the sectors rank owns; nranks = 1: all)
 void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj,
                         const ull* obj_nwords, ull* hist /*[n_obj][2][33]*/, ull total_sectors,
-                        int num_sms, cudaStream_t s);
+                        uint32_t rank, uint32_t nranks, int num_sms, cudaStream_t s);
 // a6 per-pc histograms from deduped pc keys
 void launch_pc_hist_sorted(const ull* pckeys, ull n, KeyLayout kl, const uint32_t* site_of,
                            uint32_t launch_filter, const uint32_t* word_cnt, const uint32_t* sector_cnt,
@@ -168,6 +177,7 @@ struct IndicatorArgs {
   ull* ind;                  // [n][kIndFields] accumulators
   ull* tile_info;            // [n_tiles][4] first touched, last touched, cand, cnt
   ull* tile_prev;            // [n_tiles] last touched word before the tile (or ~0)
+  uint32_t rank, nranks;     // sharded mode: tiles of other ranks are skipped
 };
 constexpr int kIndFields = 24;
 enum IndField {
@@ -176,5 +186,15 @@ enum IndField {
   F_PAD1, F_PAD2, F_PAD3
 };
 void launch_indicators(const IndicatorArgs& a, int num_sms, cudaStream_t s);
+// the same in steps, for the sharded mode (partial sums combined in between):
+// tiles (mode 0: sums + votes, 1: verify), stitch, finalize
+void launch_indicator_tiles(const IndicatorArgs& a, int mode, cudaStream_t s);
+void launch_indicator_stitch(const IndicatorArgs& a, cudaStream_t s);
+void launch_indicator_finalize(const IndicatorArgs& a, cudaStream_t s);
+// per-object partial sums <-> a reducible array: sums [n][10] (T, TW, hot, fs,
+// sum x, le1, sum x^2 as four 32-bit limbs), maxima [n] (largest sector
+// count); dir 0 packs, 1 unpacks.  verify: F_VERIFY <-> [n]
+constexpr int kIndSumFields = 10;
+void launch_indicator_pack(ull* ind, uint32_t n, ull* sums, ull* maxs, ull* verify, int dir, cudaStream_t s);
 
 }  // namespace thermo

@@ -77,7 +77,7 @@ EXPORTS = ("thermo_default_config", "thermo_default_params", "thermo_abi_version
            "thermo_create_dist", "thermo_nccl_unique_id", "thermo_destroy", "thermo_reset",
            "thermo_register_objects", "thermo_ingest_trace", "thermo_build_heatmap", "thermo_query_heatmap",
            "thermo_query_histogram", "thermo_query_per_pc", "thermo_classify", "thermo_get_stats",
-           "thermo_last_error")
+           "thermo_last_error", "thermo_create_local_shards", "thermo_sharding")
 
 _lib = None
 
@@ -99,6 +99,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.thermo_create.argtypes = [P(vp), ctypes.c_int, vp, P(thermo_config)]
     L.thermo_create_dist.argtypes = [P(vp), ctypes.c_int, vp, P(thermo_config), vp, ctypes.c_int, ctypes.c_int]
     L.thermo_nccl_unique_id.argtypes = [vp]
+    L.thermo_create_local_shards.argtypes = [P(vp), ctypes.c_int, P(thermo_config), ctypes.c_int]
+    L.thermo_sharding.argtypes = [vp, P(ctypes.c_int), P(ctypes.c_int), P(u32)]
     L.thermo_destroy.argtypes = [vp]
     L.thermo_reset.argtypes = [vp]
     L.thermo_register_objects.argtypes = [vp, P(thermo_object), sz]
@@ -135,6 +137,24 @@ def label_names(bits: int) -> list[str]:
     return [k for k, v in LABELS.items() if bits & v]
 
 
+def _config(max_launches: int = 1, max_warps_per_launch: int = 1 << 20, max_pcs: int = 4096,
+            dedup: int = DEDUP_AUTO, track_pc: bool = True) -> thermo_config:
+    cfg = thermo_config()
+    load().thermo_default_config(ctypes.byref(cfg))
+    cfg.max_launches, cfg.max_warps_per_launch, cfg.max_pcs = max_launches, max_warps_per_launch, max_pcs
+    cfg.dedup, cfg.track_pc = dedup, int(bool(track_pc))
+    return cfg
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (thermo_nccl_unique_id), made on rank 0."""
+    buf = ctypes.create_string_buffer(128)
+    st = load().thermo_nccl_unique_id(buf)
+    if st:
+        raise ThermoError(st, "thermo_nccl_unique_id")
+    return buf.raw
+
+
 class Thermo:
     """One libthermo context (bound to a CUDA device and stream).
 
@@ -142,19 +162,51 @@ class Thermo:
     (fast path) or in host memory (staged by the library).
     """
 
-    def __init__(self, device: int = 0, stream=None, max_launches: int = 1, max_warps_per_launch: int = 1 << 20,
-                 max_pcs: int = 4096, dedup: int = DEDUP_AUTO, track_pc: bool = True):
+    def __init__(self, device: int = 0, stream=None, _handle=None, **cfg_kw):
         self.L = load()
-        cfg = thermo_config()
-        self.L.thermo_default_config(ctypes.byref(cfg))
-        cfg.max_launches, cfg.max_warps_per_launch, cfg.max_pcs = max_launches, max_warps_per_launch, max_pcs
-        cfg.dedup, cfg.track_pc = dedup, int(bool(track_pc))
+        self.objects = []
+        if _handle is not None:
+            self.h = _handle
+            return
+        cfg = _config(**cfg_kw)
         h = vp()
         st = self.L.thermo_create(ctypes.byref(h), device, vp(stream) if stream else None, ctypes.byref(cfg))
         if st:
             raise ThermoError(st, "thermo_create")
         self.h = h
-        self.objects = []
+
+    @classmethod
+    def dist(cls, nccl_id: bytes, rank: int, nranks: int, device: int = 0, stream=None, **cfg_kw) -> "Thermo":
+        """Rank `rank` of the address-sharded mode (thermo_create_dist): build and
+        classify are collective; queries are job-wide except heatmap (this rank's
+        partition, other ranks' sectors 0)."""
+        L = load()
+        cfg = _config(**cfg_kw)
+        h = vp()
+        idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        st = L.thermo_create_dist(ctypes.byref(h), device, vp(stream) if stream else None, ctypes.byref(cfg), idb,
+                                  rank, nranks)
+        if st:
+            raise ThermoError(st, "thermo_create_dist")
+        return cls(_handle=h)
+
+    @classmethod
+    def local_shards(cls, nranks: int, device: int = 0, **cfg_kw) -> list:
+        """nranks contexts of the sharded mode inside this process
+        (thermo_create_local_shards); drive each from its own thread."""
+        L = load()
+        cfg = _config(**cfg_kw)
+        hs = (vp * nranks)()
+        st = L.thermo_create_local_shards(hs, device, ctypes.byref(cfg), nranks)
+        if st:
+            raise ThermoError(st, "thermo_create_local_shards")
+        return [cls(_handle=vp(hs[r])) for r in range(nranks)]
+
+    def sharding(self) -> tuple:
+        """(rank, nranks, ownership chunk in sectors)."""
+        r, n, c = ctypes.c_int(), ctypes.c_int(), u32()
+        self._ck(self.L.thermo_sharding(self.h, ctypes.byref(r), ctypes.byref(n), ctypes.byref(c)))
+        return r.value, n.value, c.value
 
     # ---- plumbing ----
     def _ck(self, st):

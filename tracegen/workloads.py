@@ -399,7 +399,7 @@ def smem_warp_broadcast(blocks=4, device="cpu") -> Trace:
 # --------------------------------------------------------------------------
 def random_trace(n=20000, seed=1, n_objects=5, n_warps=50, n_launches=3, n_pcs=7,
                  invalid_frac=0.01, unmapped_frac=0.05, shared_frac=0.2, device="cpu",
-                 instr_len=(1, 40)) -> Trace:
+                 instr_len=(1, 40), max_len=3000) -> Trace:
     """Random unaligned/straddling records of sizes 1/2/4/8/16 over random
     objects (global and shared), some unmapped and some invalid records, random
     instruction lengths (including > 32 records)."""
@@ -412,7 +412,7 @@ def random_trace(n=20000, seed=1, n_objects=5, n_warps=50, n_launches=3, n_pcs=7
     bases = {0: 0x100000, 1: 0x2000}
     for o in range(n_objects):
         space = 1 if (o % 5 == 4 or torch.rand(1, generator=g).item() < shared_frac) else 0
-        ln = int(ri(1, 3000, (1,)))
+        ln = int(ri(1, max_len, (1,)))
         base = bases[space] + 32 * int(ri(0, 4, (1,)))
         objects.append((base, ln, space, 100 + o, f"o{o}"))
         bases[space] = _align(base + ln + 1, 32) + 32 * int(ri(0, 3, (1,)))
