@@ -11,9 +11,14 @@ configs[1], the naive SGEMM 1024x1024 trace (K = 128: 270,532,608 records, G19).
 Inputs (4.3 GB) are larger than L2 (126 MB), so no explicit flush is needed.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the
-reference arm of this tier) on a bounded sample of the same workload.
-Multi-GPU (torchrun): each rank reduces its own independent trace of the
-workload (replicas; weak scaling) and the time is the max over ranks.
+reference arm of this tier) on bounded samples of the same workload.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): the sharded mode (row e) --
+the workload grows with N (SGEMM with M = 1024 N: N x 270.5 M records, weak
+scaling), each rank decodes its slice of warps, keys move to their sector's
+owner in one all-to-all inside thermo_build_heatmap, and histograms/indicators
+are combined by all-reduce; the step time is the max over ranks.
+`--mode replicas` instead runs N independent copies (no exchange).
 """
 from __future__ import annotations
 
@@ -89,9 +94,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_trace(workload: str, device: str, rank: int = 0):
+def make_trace(workload: str, device: str, rank: int = 0, ws: int = 1):
+    """The workload; with ws > 1 (sharded) rank's slice of the ws-times larger job."""
     import tracegen as tg
     if workload == "sgemm":
+        if ws > 1:  # SGEMM with M = 1024 ws; rank r holds warps [r W / ws, (r + 1) W / ws)
+            W = 32 * ws * 32 * 32
+            return tg.gemm(1024 * ws, 1024, 128, "v00", device=device,
+                           warp_range=(rank * W // ws, (rank + 1) * W // ws))
         return tg.gemm(1024, 1024, 128, "v00", device=device)
     if workload == "stencil":
         return tg.stencil(8192, device=device)
@@ -107,9 +117,9 @@ def cpu_baseline(workload: str, budget_s: float = 12.0):
     prefix sample of the same trace (records/s)."""
     import oracle
     import tracegen as tg
-    if workload == "sgemm":   # a prefix of whole warps: ~10 s of oracle work
+    if workload == "sgemm":   # a prefix of whole warps (the oracle runs ~2048 warps per 4 s)
         n_total = 270532608
-        warps = max(64, int(2048 * budget_s / 10.0))
+        warps = max(64, int(2048 * budget_s / 4.0))
         t = tg.gemm(1024, 1024, 128, "v00", device="cpu", warp_limit=warps)
     else:
         t = make_trace(workload, "cpu")
@@ -141,15 +151,40 @@ def dist_setup(args):
 
 
 def run_reference(args, ws, rank):
+    """The reference arm of this tier: the CPU oracle as it stands, single-threaded,
+    each step a bounded sample (a prefix of whole warps) of the same workload."""
     if rank != 0:
         return
-    base = cpu_baseline(args.workload, budget_s=min(20.0, 4.0 + 2.0 * args.steps))
-    v = base["value"]
+    import oracle
+    import tracegen as tg
+    n_total, n_obj = {"sgemm": (270532608, 3)}.get(args.workload, (None, None))
+    if args.workload == "sgemm":
+        t = tg.gemm(1024, 1024, 128, "v00", device="cpu", warp_limit=1024)  # ~2 s of oracle work per step
+    else:
+        t = make_trace(args.workload, "cpu")
+        n_total, n_obj = t.n, len(t.objects)
+
+    def step():
+        o = oracle.Oracle([x[:4] for x in t.objects])
+        o.ingest(t.records)
+        o.build()
+        o.classify()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    v = t.n * args.steps / el
+    sample = (f"first {t.n} of {n_total} records of the {args.workload} trace per step (ingest + build + "
+              f"classify, single-threaded std::set oracle)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "records": None},
-            "cpu_baseline": base, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": args.workload, "records": n_total, "objects": n_obj, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -163,6 +198,10 @@ def main():
     ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash", "segment"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="multi-GPU: one sharded job (default) or independent replicas")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="one GPU through the sharded NCCL path (checks that code path on one GPU)")
     args = ap.parse_args()
     ws, rank, local = dist_setup(args)
     if args.impl == "reference":
@@ -175,14 +214,28 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2507_18729_b200 import BOTH, Thermo
+    from paper_2507_18729_b200.thermo import nccl_unique_id
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    t = make_trace(args.workload, str(dev), rank)
+    sharded = (ws > 1 or args.force_dist) and args.mode == "sharded"
+    if args.force_dist:
+        os.environ["THERMO_FORCE_COMM"] = "1"
+    t = make_trace(args.workload, str(dev), rank, ws if sharded else 1)
     n = t.n
     stream = torch.cuda.current_stream(dev)
     dedup = {"auto": 0, "sort": 1, "hash": 2, "segment": 3}[args.dedup]
-    th = Thermo(device=local, stream=stream.cuda_stream, max_launches=max(1, int(t.meta.get("launches", 1))),
-                max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), dedup=dedup)
+    cfg = dict(max_launches=max(1, int(t.meta.get("launches", 1))),
+               max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), dedup=dedup)
+    parallelism = "single"
+    if sharded:
+        from paper_2507_18729_b200.dist import broadcast_bytes
+        uid = broadcast_bytes(nccl_unique_id() if rank == 0 else None) if ws > 1 else nccl_unique_id()
+        th = Thermo.dist(uid, rank, ws, device=local, stream=stream.cuda_stream, **cfg)
+        parallelism = f"sharded x{ws}: sector owners, one NCCL all-to-all of keys + all-reduce of sums"
+    else:
+        th = Thermo(device=local, stream=stream.cuda_stream, **cfg)
+        if ws > 1:
+            parallelism = f"replicas x{ws}"
     th.register_objects(t.objects)
 
     def step(recs):
@@ -258,7 +311,7 @@ def main():
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
             "algorithmic_bytes_per_launch": 16 * n, "ms_per_launch": dec}
     pipe = None
-    if args.workload in ALGO_BYTES:
+    if args.workload in ALGO_BYTES and ws == 1:
         a = ALGO_BYTES[args.workload]
         b = 16 * a["N"] + 16 * a["U"] + 4 * a["cells"]
         pipe = {"algorithmic_bytes": b, "achieved_GBps": b / (ms / 1e3) / 1e9,
@@ -266,10 +319,10 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "records": n, "objects": len(t.objects),
+            "config": {"workload": args.workload, "records": n * ws, "objects": len(t.objects),
                        "dedup": {1: "sort", 2: "hash", 3: "segment"}.get(st["dedup_used"], "?"),
                        "l2": "inputs larger than L2 (16 B x records >> 126 MB), no flush",
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "single"},
+                       "records_per_gpu": n, "parallelism": parallelism},
             "roofline": roof, "pipeline_roofline": pipe, "phase_ms": ph_mean, "dominant_phase": dominant,
             "clocks": clocks, "gpu_launches": launches,
             "stats": {k: st[k] for k in ("keys_emitted", "pc_keys_emitted", "distinct_pairs", "distinct_pc_pairs",

@@ -140,3 +140,19 @@ def test_shards_empty_rank():
     sl = [t.records, t.records[:0], t.records[:0], t.records[:0]]
     ref = single(t, [t.records], 0, oracle.ALL_LAUNCHES, 1)
     compare(t, ref, sharded(t, sl, 0, oracle.ALL_LAUNCHES, 1))
+
+
+def test_nccl_transport_single_rank(monkeypatch):
+    """The NCCL transport (thermo_create_dist) with one rank, forced on: init,
+    all-reduce, all-gather and the all-to-all's self copy through NCCL on one
+    GPU, against a plain context."""
+    monkeypatch.setenv("THERMO_FORCE_COMM", "1")
+    from paper_2507_18729_b200 import Thermo
+    from paper_2507_18729_b200.thermo import nccl_unique_id
+    t = tg.random_trace(n=30000, seed=11, n_warps=100, n_launches=2, max_len=300000)
+    th = Thermo.dist(nccl_unique_id(), 0, 1, max_launches=2, max_warps_per_launch=1 << 22)
+    th.register_objects(t.objects)
+    th.ingest(t.records.cuda().contiguous())
+    th.build(BOTH, oracle.ALL_LAUNCHES)
+    ref = single(t, [t.records], 0, oracle.ALL_LAUNCHES, 2)
+    compare(t, ref, [th])

@@ -112,7 +112,8 @@ def fig6(n_warps: int = 2, offset: int = 16, device="cpu") -> Trace:
 # --------------------------------------------------------------------------
 # gemm_v00 / gemm_v01 (Listing 1; block 32x32)
 # --------------------------------------------------------------------------
-def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 26, warp_limit=None) -> Trace:
+def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 26, warp_limit=None,
+         warp_range=None) -> Trace:
     """Naive SGEMM trace, one C element per thread, fp32 row-major.
 
     v00: C_row = bx*32 + tx, C_col = by*32 + ty (Listing 1).  v01 swaps them
@@ -130,16 +131,20 @@ def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 
     n_warps = (M // 32) * (N // 32) * 32
     if warp_limit is not None:  # prefix of the trace (first warp_limit warps)
         n_warps = min(n_warps, warp_limit)
+    w_lo, w_hi = 0, n_warps
+    if warp_range is not None:  # the warps [lo, hi) of the trace (one rank's slice)
+        w_lo, w_hi = max(0, warp_range[0]), min(n_warps, warp_range[1])
+        w_hi = max(w_lo, w_hi)
     ipw = 2 * K + 2                       # instructions per warp
-    n_rec = n_warps * ipw * 32
+    n_rec = (w_hi - w_lo) * ipw * 32
     out = torch.empty((n_rec, 4), dtype=torch.int32, device=dev)
     lane = _lanes(dev)
     t = torch.arange(ipw, dtype=torch.int64, device=dev)
     k_of_t = torch.clamp(t // 2, max=K - 1)
     warps_per_chunk = max(1, chunk_records // (ipw * 32))
     pos = 0
-    for w0 in range(0, n_warps, warps_per_chunk):
-        gw = torch.arange(w0, min(n_warps, w0 + warps_per_chunk), dtype=torch.int64, device=dev)
+    for w0 in range(w_lo, w_hi, warps_per_chunk):
+        gw = torch.arange(w0, min(w_hi, w0 + warps_per_chunk), dtype=torch.int64, device=dev)
         b, ty = gw // 32, gw % 32
         bx, by = b % gdx, b // gdx
         if variant == "v00":
@@ -165,7 +170,7 @@ def gemm(M=1024, N=1024, K=128, variant="v00", device="cpu", chunk_records=1 << 
         pos += rec.shape[0]
     assert pos == n_rec
     return Trace(f"gemm_{variant}-{M}x{N}x{K}", objects, out,
-                 meta=dict(M=M, N=N, K=K, variant=variant, warps=n_warps))
+                 meta=dict(M=M, N=N, K=K, variant=variant, warps=n_warps, warp_range=(w_lo, w_hi)))
 
 
 # --------------------------------------------------------------------------
