@@ -126,13 +126,23 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 }
 
 // ---- 3. scatter keys into their sector's segment ------------------------------------
-__global__ void seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl, ull* __restrict__ cur,
-                                   ull* __restrict__ out) {
-  const ull stride = (ull)gridDim.x * blockDim.x;
-  for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const ull k = keys[i];
-    const ull pos = atomicAdd(&cur[key_g(k, kl)], 1ull);
-    out[pos] = k;
+// 8 keys per thread with their 8 cursor atomics in flight together: the
+// atomics' latency (contended cursors of hot sectors), not bandwidth, bounds it
+constexpr int kScatterPer = 8;
+__global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
+                                                          ull* __restrict__ cur, ull* __restrict__ out) {
+  const ull tile = (ull)blockDim.x * kScatterPer;
+  for (ull t0 = (ull)blockIdx.x * tile; t0 < n; t0 += (ull)gridDim.x * tile) {
+    ull k[kScatterPer], pos[kScatterPer];
+    const ull i0 = t0 + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) k[u] = i0 + (ull)u * blockDim.x < n ? keys[i0 + (ull)u * blockDim.x] : 0;
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u)
+      if (i0 + (ull)u * blockDim.x < n) pos[u] = atomicAdd(&cur[key_g(k[u], kl)], 1ull);
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u)
+      if (i0 + (ull)u * blockDim.x < n) out[pos[u]] = k[u];
   }
 }
 
@@ -149,9 +159,10 @@ __device__ __forceinline__ ull first_sector_at(const ull* off, ull nsec, ull pos
   return lo;
 }
 
-// stable LSD radix sort of kSegBuf u64 keys in shared memory on bits
-// [lo, lo + bits); returns the buffer holding the result
-__device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* whist, uint32_t* blk_ofs) {
+// stable LSD radix sort of R * kSegThreads u64 keys in shared memory on bits
+// [lo, lo + bits) (warp w ranks keys [w R 32, (w + 1) R 32)); returns the
+// buffer holding the result
+__device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* whist, uint32_t* blk_ofs, int R) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt_g();
   __shared__ uint32_t wsum[kSegWarps];
@@ -161,7 +172,8 @@ __device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* 
     uint32_t rank[kSegRounds];
 #pragma unroll
     for (int r = 0; r < kSegRounds; ++r) {  // warp w ranks its own contiguous keys
-      const uint32_t idx = (uint32_t)w * kSegRounds * 32 + r * 32 + lane;
+      if (r >= R) break;
+      const uint32_t idx = (uint32_t)(w * R + r) * 32 + lane;
       const uint32_t d = (uint32_t)(src[idx] >> shift) & 255u;
       const unsigned peers = __match_any_sync(GFULL, d);
       const int leader = __ffs(peers) - 1;
@@ -196,7 +208,8 @@ __device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* 
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kSegRounds; ++r) {
-      const uint32_t idx = (uint32_t)w * kSegRounds * 32 + r * 32 + lane;
+      if (r >= R) break;
+      const uint32_t idx = (uint32_t)(w * R + r) * 32 + lane;
       const ull k = src[idx];
       const uint32_t d = (uint32_t)(k >> shift) & 255u;
       dst[blk_ofs[d] + whist[w * 256 + d] + rank[r]] = k;
@@ -246,12 +259,14 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
   if (s0 >= s1) return;
   const ull k0 = off[s0];
   const uint32_t nk = (uint32_t)(off[s1] - k0);  // < kSegBuf
+  const int R = (int)((nk + kSegThreads - 1) / kSegThreads);  // rounds of 256 keys actually used
+  const uint32_t npad = (uint32_t)R * kSegThreads;
   int ls = 0;
   while ((1ull << ls) < (s1 - s0)) ++ls;
   const uint32_t LWP = kl.L + kl.W + kl.P;
   // local key: [g - s0 : ls][launch, warp, pcid : LWP][mask : 8]; filtered-out
   // launches and padding become the all-ones sentinel (sorted last)
-  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) {
+  for (uint32_t i = threadIdx.x; i < npad; i += kSegThreads) {
     ull v = ~0ull;
     if (i < nk) {
       const ull k = seg[k0 + i];
@@ -262,11 +277,11 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
   }
   __syncthreads();
   // runs of (g, launch, warp) only need those bits sorted; the pc id bits below stay unsorted
-  ull* src = smem_radix_sort(buf0, buf1, 8 + (int)kl.P, ls + (int)(kl.L + kl.W), whist, blk_ofs);
+  ull* src = smem_radix_sort(buf0, buf1, 8 + (int)kl.P, ls + (int)(kl.L + kl.W), whist, blk_ofs, R);
   // ---- (a) runs of equal (g, launch, warp): distinct warps per sector / word ----
   const int RS = 8 + (int)kl.P;
   ull distinct = 0;
-  for (uint32_t base = 0; base < kSegBuf; base += kSegThreads) {
+  for (uint32_t base = 0; base < npad; base += kSegThreads) {
     const uint32_t i = base + threadIdx.x;
     const ull key = src[i];
     const bool valid = key != ~0ull;
@@ -275,7 +290,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
     const bool head = valid && pre != prev;
     uint32_t m = (uint32_t)(key & 0xFF);
     if (head)
-      for (uint32_t j = i + 1; j < kSegBuf && (src[j] >> RS) == pre; ++j) m |= (uint32_t)(src[j] & 0xFF);
+      for (uint32_t j = i + 1; j < npad && (src[j] >> RS) == pre; ++j) m |= (uint32_t)(src[j] & 0xFF);
     const ull g = valid ? s0 + (key >> (LWP + 8)) : ~0ull;
     ull v = 0;
     if (head) {
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
   for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
   __syncthreads();
   const ull pmask = (1ull << kl.P) - 1;
-  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) {
+  for (uint32_t i = threadIdx.x; i < npad; i += kSegThreads) {
     const ull k = src[i];
     if (k == ~0ull) continue;
     const uint32_t hkey = (uint32_t)(((k >> (LWP + 8)) << kl.P) | ((k >> 8) & pmask));
@@ -403,7 +418,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull ns
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
                           DevCounters* ctr, int num_sms, cudaStream_t s) {
   if (n) {
-    const unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
+    const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
     seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cur, out);
   }
   const size_t smem = segment_chunk_smem();
