@@ -214,8 +214,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
 
 
 size_t decode_smem(const DecodeArgs& a) {
-  return (size_t)a.obj.n * 3 * sizeof(ull) + 2 * kInstrSlots * sizeof(ull) + kPcSlots * sizeof(ull) +
-         kInstrSlots * sizeof(uint32_t) + 16 + (size_t)kDecWarps * kWarpRegion;
+  return kOffObj + (size_t)a.obj.n * 3 * sizeof(ull);
 }
 
 

@@ -239,6 +239,14 @@ struct InstrCache {
 constexpr int kRingChunks = 8;          // fast kernel: per-warp record ring of 8 x 32 records (4 KB)
 constexpr int kAhead = 6;               // chunks in flight ahead of the current one (cp.async)
 constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16;
+// fixed-size parts first, at compile-time offsets (addresses are immediates,
+// nothing to keep in registers); the object table (3 x n u64) last
+constexpr size_t kOffIval = 0;                                         // [kInstrSlots][2] u64
+constexpr size_t kOffPc = kOffIval + 2 * kInstrSlots * sizeof(ull);    // [kPcSlots] u64
+constexpr size_t kOffIkey = kOffPc + kPcSlots * sizeof(ull);           // [kInstrSlots] u32
+constexpr size_t kOffWarp = (kOffIkey + kInstrSlots * sizeof(uint32_t) + 15) & ~(size_t)15;  // [kDecWarps]
+constexpr size_t kOffObj = kOffWarp + (size_t)kDecWarps * kWarpRegion;  // lo, hi, soff [n] u64 each
+static_assert(kOffWarp % 16 == 0 && kWarpRegion % 16 == 0, "128-bit ring loads need 16-byte alignment");
 struct Smem {
   ull *lo, *hi, *soff, *ival, *pc;
   unsigned char* warp;  // [kDecWarps][kWarpRegion]
@@ -247,14 +255,13 @@ struct Smem {
 __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs& a) {
   const uint32_t nobj = a.obj.n;
   Smem m;
-  m.lo = reinterpret_cast<ull*>(smem);
+  m.ival = reinterpret_cast<ull*>(smem + kOffIval);
+  m.pc = reinterpret_cast<ull*>(smem + kOffPc);
+  m.ikey = reinterpret_cast<uint32_t*>(smem + kOffIkey);
+  m.warp = smem + kOffWarp;
+  m.lo = reinterpret_cast<ull*>(smem + kOffObj);
   m.hi = m.lo + nobj;
   m.soff = m.hi + nobj;
-  m.ival = m.soff + nobj;                   // [kInstrSlots][2]
-  m.pc = m.ival + 2 * kInstrSlots;          // [kPcSlots]
-  m.ikey = reinterpret_cast<uint32_t*>(m.pc + kPcSlots);
-  // 16-byte aligned: the fast kernel's record ring is read with 128-bit loads
-  m.warp = reinterpret_cast<unsigned char*>(((uintptr_t)(m.ikey + kInstrSlots) + 15) & ~(uintptr_t)15);
   for (uint32_t i = threadIdx.x; i < nobj; i += blockDim.x) {
     m.lo[i] = a.obj.lo[i];
     m.hi[i] = a.obj.hi[i];

@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       }
       // ---- word mask, restricted to the object's words (G9) ----
       const uint32_t words = ((x & 3u) + size + 3u) >> 2;
-      const uint32_t ma = act ? (((1u << words) - 1u) << ((x >> 2) & 7u)) : 0u;
+      const uint32_t ma = (((1u << words) - 1u) << ((x >> 2) & 7u)) & (0u - (uint32_t)act);
       const uint32_t fa = (oid >= 0) ? (ma & (xs == tail_s ? tail_m : 0xFFu)) : 0u;
       if (launch0 != cur_launch) {
         if (cur_launch != 0xFFFFFFFFu) {
