@@ -90,11 +90,13 @@ __device__ __forceinline__ bool win_has(const WinEnt& e, uint32_t H, uint32_t xs
 // record ring: chunk c = records [32c, 32c + 32) of the range (offsets from its
 // first record) lives in ring slot c % kRingChunks; lane l copies record
 // 32c + l with cp.async, zero-filled at or past the range end
-__device__ __forceinline__ void ring_issue(uint4* ring, const uint4* rbase, uint32_t c, uint32_t rlen, int lane) {
-  const uint32_t pos = c * 32 + lane;
-  const uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (pos & (kRingChunks * 32 - 1)));
-  const bool in = pos < rlen;
-  const uint4* src = rbase + (in ? pos : 0u);
+// ring_lane: shared address of this lane's slot in chunk slot 0; src_lane:
+// the range's record `lane`
+__device__ __forceinline__ void ring_issue(uint32_t ring_lane, const uint4* src_lane, uint32_t c, uint32_t rlen,
+                                           int lane) {
+  const bool in = c * 32 + lane < rlen;
+  const uint32_t dst = ring_lane + (c & (kRingChunks - 1)) * 512;
+  const uint4* src = in ? src_lane + c * 32 : src_lane;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(in ? 16 : 0) : "memory");
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   ull* const gnk = &a.ctr->n_keys;
   Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0};
   uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
+  const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(ring + lane);
 
   InstrCache icache;
   icache.init();
@@ -150,15 +153,16 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
     const uint4* const rbase = a.recs + p0;
     // keep kAhead chunks in flight ahead of the one holding the view (~3 KB per warp)
     uint32_t issued = 0;
-    for (int k = 0; k <= kAhead; ++k) ring_issue(ring, rbase, issued++, rlen, lane);
+    const uint4* const src_lane = rbase + lane;
+    for (int k = 0; k <= kAhead; ++k) ring_issue(ring_lane, src_lane, issued++, rlen, lane);
     uint32_t off = 0;  // the view's first record, from p0
     while (off < rlen) {
-      if (issued <= (off >> 5) + kAhead) ring_issue(ring, rbase, issued++, rlen, lane);
+      if (issued <= (off >> 5) + kAhead) ring_issue(ring_lane, src_lane, issued++, rlen, lane);
       asm volatile("cp.async.wait_group %0;\n" ::"n"(kAhead - 1) : "memory");  // the view's 2 chunks landed
       __syncwarp();
       const uint32_t rem = rlen - off;
-      uint4 cur = make_uint4(0, 0, 0, 0);
-      if ((uint32_t)lane < rem) cur = ring[(off + lane) & (kRingChunks * 32 - 1)];
+      // records at or past the range end were zero-filled by cp.async
+      const uint4 cur = ring[(off + lane) & (kRingChunks * 32 - 1)];
       // ---- view = one warp instruction: records [off, off + len) ----
       const unsigned sb = __ballot_sync(FULL, (cur.y >> 23) & 1u) & ~1u;
       uint32_t len = sb ? (uint32_t)(__ffs(sb) - 1) : 32u;
