@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
   while ((1u << steps) < nobj) ++steps;
   const uint32_t LW = a.kl.L + a.kl.W, P = a.kl.P;
 
-  Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0};
+  Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0, a.seg_cnt, 8 + a.kl.P + a.kl.L + a.kl.W};
   InstrCache icache;
   icache.init();
   ull n_invalid = 0, n_oor = 0, n_mapped = 0, n_unmapped = 0;

@@ -119,16 +119,24 @@ __device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, boo
 
 
 // per-warp staging buffer in shared memory; flushed to global with one atomic
+// (seg_cnt != null: also count the flushed keys per sector, the SEGMENT
+// path's histogram, so that build does not re-read the keys for it)
 struct Stage {
   ull* s;        // smem [kStage]
   uint32_t cnt;  // warp-uniform
+  uint32_t* seg_cnt;
+  uint32_t gshift;  // key >> gshift = sector id
   __device__ __forceinline__ void flush(ull* g, ull* gcount, int lane) {
     __syncwarp();
     if (cnt == 0) return;
     ull base = 0;
     if (lane == 0) base = atomicAdd(gcount, (ull)cnt);
     base = __shfl_sync(FULL, base, 0);
-    for (uint32_t i = lane; i < cnt; i += 32) g[base + i] = s[i];
+    for (uint32_t i = lane; i < cnt; i += 32) {
+      const ull k = s[i];
+      g[base + i] = k;
+      if (seg_cnt) atomicAdd(&seg_cnt[k >> gshift], 1u);
+    }
     __syncwarp();
     cnt = 0;
   }

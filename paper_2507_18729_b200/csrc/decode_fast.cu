@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   const uint32_t max_launches = a.max_launches, max_warps = a.max_warps;
   ull* const gkeys = a.keys;
   ull* const gnk = &a.ctr->n_keys;
-  Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0};
+  Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0, a.seg_cnt, 8 + a.kl.P + a.kl.L + a.kl.W};
   uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
   const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(ring + lane);
 

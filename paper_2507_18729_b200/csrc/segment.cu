@@ -386,29 +386,40 @@ static size_t segment_chunk_smem() { return (size_t)2 * kSegBuf * sizeof(ull) + 
 ull segment_chunk_cap() { return kSegCap; }
 
 // phases 1-2; syncs once so the caller can read the largest per-sector count
-cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
-                            cudaStream_t s, uint32_t* max_per_sector) {
+cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
   cudaError_t e;
   if (ws.cap_sec < nsec + 1) {
     cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum);
-    ws.cap_sec = nsec + 1;
+    ws.cnt = nullptr; ws.off = ws.cur = ws.bsum = nullptr;
+    ws.cap_sec = 0;
     if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
     if ((e = cudaMalloc(&ws.off, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
-    if (!ws.maxc && (e = cudaMalloc(&ws.maxc, sizeof(uint32_t)))) return e;
+    ws.cap_sec = nsec + 1;
   }
-  cudaMemsetAsync(ws.cnt, 0, (nsec + 1) * sizeof(uint32_t), s);
+  if (!ws.maxc && (e = cudaMalloc(&ws.maxc, sizeof(uint32_t)))) return e;
+  return cudaSuccess;
+}
+
+cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
+                            cudaStream_t s, uint32_t* max_per_sector, bool counted) {
+  cudaError_t e;
+  if ((e = segment_reserve(ws, nsec))) return e;
   cudaMemsetAsync(ws.maxc, 0, sizeof(uint32_t), s);
-  if (n) {
-    const unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
-    seg_hist_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cnt);
+  if (!counted) {
+    cudaMemsetAsync(ws.cnt, 0, (nsec + 1) * sizeof(uint32_t), s);
+    if (n) {
+      const unsigned grid = (unsigned)std::min<ull>((n + 255) / 256, (ull)num_sms * 16);
+      seg_hist_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cnt);
+      ws.launches += 1;
+    }
   }
   const ull nb = (nsec + kScanBlock - 1) / kScanBlock;
   seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
   seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
   seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.cur);
-  ws.launches += 4;
+  ws.launches += 3;
   if ((e = cudaMemcpyAsync(max_per_sector, ws.maxc, sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) return e;
   return cudaStreamSynchronize(s);
 }

@@ -104,6 +104,7 @@ struct thermo_ctx {
   ull records = 0;
   float ms_ingest = 0, ms_build = 0, ms_classify = 0;
   bool hist_valid = false;
+  bool seg_counted = false;  // the decoder counts keys per sector (SEGMENT histogram, one rank)
 
   // sharded mode (row e, shard.cu); comm == nullptr: one rank
   Comm* comm = nullptr;
@@ -223,6 +224,7 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.instr_ctr = ctx->d_instr;
   a.launch_ctr = ctx->d_launch_ctr;
   a.deferred = ctx->d_deferred;
+  a.seg_cnt = ctx->seg_counted ? ctx->seg.cnt : nullptr;
   launch_decode(a, ctx->num_sms, ctx->stream);
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());
@@ -590,6 +592,7 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   CK(dalloc(&ctx->d_pc_keys_tab, ctx->pc_cap));
   CK(dalloc(&ctx->d_pc_vals, ctx->pc_cap));
   CK(dalloc(&ctx->d_site_of, c.max_pcs));
+  CK(segment_reserve(ctx->seg, soff));
   if (ctx->comm) {
     CK(dalloc(&ctx->d_pcmap, c.max_pcs));
     CK(dalloc(&ctx->d_site_glob, c.max_pcs));
@@ -614,6 +617,8 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
   ctx->records = 0;
   ctx->state = 1;
   ctx->hist_valid = false;
+  ctx->seg_counted = !ctx->comm && (ctx->cfg.dedup == THERMO_DEDUP_AUTO || ctx->cfg.dedup == THERMO_DEDUP_SEGMENT);
+  if (ctx->seg_counted) CK(cudaMemsetAsync(ctx->seg.cnt, 0, (ctx->S_tot + 1) * sizeof(uint32_t), ctx->stream));
   ctx->n_exch = 0;
   ctx->pc_mapped = 0;
   ctx->glob_sites.clear();
@@ -753,7 +758,8 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     // sector holds more keys than a shared-memory chunk
     CK(cudaEventRecord(ctx->evp[0], s));
     uint32_t maxc = 0;
-    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc);
+    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc,
+                        ctx->seg_counted);
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment prepare: ") + cudaGetErrorString(e));
     if (maxc < segment_chunk_cap()) {
       if (ctx->sw.alt_cap < ctx->n_keys) {

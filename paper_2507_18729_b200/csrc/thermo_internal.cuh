@@ -93,6 +93,7 @@ struct DecodeArgs {
   ull* instr_ctr;         // [max_launches * n_obj * 2] (instrs, misaligned)
   ull* launch_ctr;        // [max_launches * 2] (unmapped words, mapped word accesses)
   ull* deferred;          // [n] p << 7 | stats_only << 6 | len of deferred views
+  uint32_t* seg_cnt;      // [S_tot] keys per sector (SEGMENT histogram), or null
 };
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------
@@ -125,8 +126,10 @@ struct SegWorkspace {
   ull cap_sec = 0;
   ull launches = 0;
 };
+// counted: ws.cnt already holds the keys per sector (counted by the decoder)
+cudaError_t segment_reserve(SegWorkspace& ws, ull nsec);
 cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
-                            cudaStream_t s, uint32_t* max_per_sector);
+                            cudaStream_t s, uint32_t* max_per_sector, bool counted);
 // scatter + per-chunk dedup: dense counts (a5) and, if pc_hist != null, the
 // per-pc histograms (a6) of the chunk's sectors
 cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull nsec, uint32_t filter,
