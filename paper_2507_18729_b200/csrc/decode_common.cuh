@@ -147,11 +147,9 @@ struct Stage {
   do {                                                                    \
     const bool has_ = (HAS);                                              \
     const unsigned b_ = __ballot_sync(FULL, has_);                        \
-    if (b_) {                                                             \
-      if (has_) (st).s[(st).cnt + __popc(b_ & lane_lt)] = (KEY);          \
-      (st).cnt += __popc(b_);                                             \
-      if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane); \
-    }                                                                     \
+    if (has_) (st).s[(st).cnt + __popc(b_ & lane_lt)] = (KEY);            \
+    (st).cnt += __popc(b_);                                               \
+    if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane);   \
   } while (0)
 
 // (launch, pc) -> dense pc id; inserts on first sight (G11)

@@ -262,12 +262,12 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         const bool hit0 = c0 == ck, hit1 = c1 == ck;
         // a replaced entry leaves as a key
         STAGE_PUSH(st, has & !hit0 & !hit1 & (m1 != 0), entry_key(c1, m1, tag, SH, P), gkeys, gnk);
-        if (has) {
-          const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : 0u);
-          if (!hit0) { c1 = c0; m1 = m0; }
-          c0 = ck;
-          m0 = mprev | mk;
-        }
+        const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : 0u);
+        const bool shift = has & !hit0;  // entry 0 moves to slot 1 (selects, no branch)
+        c1 = shift ? c0 : c1;
+        m1 = shift ? m0 : m1;
+        c0 = has ? ck : c0;
+        m0 = has ? (mprev | mk) : m0;
       }
       // ---- instruction statistics (G24) ----
       const uint32_t fa0 = __shfl_sync(FULL, fa, 0);
