@@ -225,7 +225,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
     dedup = {"auto": 0, "sort": 1, "hash": 2, "segment": 3}[args.dedup]
     cfg = dict(max_launches=max(1, int(t.meta.get("launches", 1))),
-               max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), dedup=dedup)
+               max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))),
+               max_pcs=int(t.meta.get("pcs", 256)), dedup=dedup)
     parallelism = "single"
     if sharded:
         from paper_2507_18729_b200.dist import broadcast_bytes

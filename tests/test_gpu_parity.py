@@ -175,3 +175,47 @@ def test_gemm_full_size_closed_form_and_sample():
     for row, o, s in zip(ref, oi, se):
         b = th.heatmap(int(o), BOTH).reshape(-1, 9)[s]
         assert np.array_equal(b, row), (o, s)
+
+
+def test_stencil_full_size_closed_form_and_sample():
+    """BJ configs[2] at full size (8192^2 column-mapped 5-point stencil,
+    402,456,600 records): the closed forms on every deep-interior word/sector
+    of `in` and every interior cell of `out`, the oracle on sampled sectors
+    (boundaries included)."""
+    N = 8192
+    t = tg.stencil(N, device="cuda")
+    assert t.n == 6 * (N - 2) ** 2
+    from paper_2507_18729_b200 import Thermo
+    # 2^24 sectors + 2^21 warps + 64 pc ids fit the 56-bit key prefix
+    th = Thermo(max_launches=1, max_warps_per_launch=1 << 21, max_pcs=64)
+    th.register_objects(t.objects)
+    th.ingest(t.records)
+    th.build()
+    w = th.heatmap(0, WORD).reshape(N, N).astype(np.int64)
+    s = th.heatmap(0, SECTOR).reshape(N, N // 8).astype(np.int64)
+    i = np.arange(N)[:, None]
+    edge = (i % 32 == 31).astype(np.int64) + (i % 32 == 0).astype(np.int64)
+    assert np.array_equal(w[2:N - 2, 2:N - 2], np.broadcast_to(3 + edge, (N, N))[2:N - 2, 2:N - 2])
+    # sectors whose 8 words are all deep interior: columns 8k..8k+7 with 2 <= 8k, 8k+7 <= N-3
+    assert np.array_equal(s[2:N - 2, 1:N // 8 - 1], np.broadcast_to(10 + 8 * edge, (N, N // 8))[2:N - 2, 1:N // 8 - 1])
+    wo = th.heatmap(1, WORD).reshape(N, N)
+    so = th.heatmap(1, SECTOR).reshape(N, N // 8)
+    assert (wo[1:N - 1, 1:N - 1] == 1).all() and (so[1:N - 1, 1:N // 8 - 1] == 8).all()
+    assert (wo[0] == 0).all() and (wo[N - 1] == 0).all()
+    # oracle on sampled sectors, boundaries included
+    rng = np.random.default_rng(7)
+    nsec = N * N // 8
+    picks = [np.concatenate([rng.choice(nsec, 24, replace=False), [0, N // 8 - 1, nsec - 1]]) for _ in range(2)]
+    oi = np.concatenate([np.full(len(p), k) for k, p in enumerate(picks)])
+    se = np.concatenate(picks)
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.restrict(oi, se)
+    recs = t.records.cpu()
+    del t
+    for a in range(0, recs.shape[0], 1 << 25):
+        orc.ingest(recs[a:a + (1 << 25)])
+    orc.build()
+    ref = orc.sample(oi, se)
+    for row, o, sct in zip(ref, oi, se):
+        b = th.heatmap(int(o), BOTH).reshape(-1, 9)[sct]
+        assert np.array_equal(b, row), (o, sct)
