@@ -245,9 +245,35 @@ void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, Ob
 }
 
 // ---- a6: per-PC histograms ---------------------------------------------------------
+// per-block bin table in shared memory (a few hundred hot (pc, level) bins take
+// every update; only the table's overflow goes to the global histogram)
+constexpr int kPcTab = 1024;
+__device__ __forceinline__ void pc_bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, uint32_t bin, uint32_t v) {
+  uint32_t h = (bin * 0x9E3779B1u) >> (32 - 10);
+  for (int probe = 0; probe < 16; ++probe) {
+    uint32_t cur = tbin[h];
+    if (cur == 0xFFFFFFFFu) {
+      cur = atomicCAS(&tbin[h], 0xFFFFFFFFu, bin);
+      if (cur == 0xFFFFFFFFu) cur = bin;
+    }
+    if (cur == bin) { atomicAdd(&tcnt[h], v); return; }
+    h = (h + 1) & (kPcTab - 1);
+  }
+  atomicAdd(&g[bin], (ull)v);
+}
+__device__ __forceinline__ void pc_tab_init(uint32_t* tbin, uint32_t* tcnt) {
+  for (int i = threadIdx.x; i < kPcTab; i += blockDim.x) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
+  __syncthreads();
+}
+__device__ __forceinline__ void pc_tab_flush(const uint32_t* tbin, const uint32_t* tcnt, ull* g) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPcTab; i += blockDim.x)
+    if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&g[tbin[i]], (ull)tcnt[i]);
+}
+
 __device__ __forceinline__ void pc_contrib(ull pre, uint32_t m, bool head, KeyLayout kl, const uint32_t* site_of,
                                            uint32_t filter, const uint32_t* wc, const uint32_t* sc, ull* pc_hist,
-                                           ull& distinct) {
+                                           ull& distinct, uint32_t* tbin, uint32_t* tcnt) {
   const ull g = pre & ((1ull << kl.S) - 1);
   const uint32_t pcid = (uint32_t)(pre >> kl.S);
   bool ok = head;
@@ -258,14 +284,14 @@ __device__ __forceinline__ void pc_contrib(ull pre, uint32_t m, bool head, KeyLa
   {
     const uint32_t bin = ok ? (pcid * 2 + 1) * kLevels + level_of(sc[g]) : 0xFFFFFFFFu;
     const unsigned mm = __match_any_sync(CFULL, bin);
-    if (ok && (__ffs(mm) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&pc_hist[bin], (ull)__popc(mm));
+    if (ok && (__ffs(mm) - 1) == (int)(threadIdx.x & 31)) pc_bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
   }
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
     const bool hb = ok && ((m >> b) & 1u);
     const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of(wc[8 * g + b]) : 0xFFFFFFFFu;
     const unsigned mm = __match_any_sync(CFULL, bin);
-    if (hb && (__ffs(mm) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&pc_hist[bin], (ull)__popc(mm));
+    if (hb && (__ffs(mm) - 1) == (int)(threadIdx.x & 31)) pc_bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
   }
 }
 
@@ -274,6 +300,8 @@ __global__ void __launch_bounds__(256) pc_hist_sorted_kernel(const ull* __restri
                                                              const uint32_t* __restrict__ wc,
                                                              const uint32_t* __restrict__ sc,
                                                              ull* __restrict__ pc_hist, DevCounters* ctr) {
+  __shared__ uint32_t tbin[kPcTab], tcnt[kPcTab];
+  pc_tab_init(tbin, tcnt);
   const int lane = threadIdx.x & 31;
   const ull nw = (n + 31) / 32;
   const ull wstride = ((ull)gridDim.x * blockDim.x) >> 5;
@@ -293,10 +321,11 @@ __global__ void __launch_bounds__(256) pc_hist_sorted_kernel(const ull* __restri
         m |= (uint32_t)(kj & 0xFF);
       }
     }
-    pc_contrib(pre, m, head, kl, site_of, filter, wc, sc, pc_hist, distinct);
+    pc_contrib(pre, m, head, kl, site_of, filter, wc, sc, pc_hist, distinct, tbin, tcnt);
   }
   for (int d = 16; d; d >>= 1) distinct += __shfl_xor_sync(CFULL, distinct, d);
   if (lane == 0 && distinct) atomicAdd(&ctr->distinct_pc, distinct);
+  pc_tab_flush(tbin, tcnt, pc_hist);
 }
 
 void launch_pc_hist_sorted(const ull* pckeys, ull n, KeyLayout kl, const uint32_t* site_of, uint32_t launch_filter,
@@ -313,15 +342,19 @@ __global__ void __launch_bounds__(256) pc_hist_hash_kernel(const ull* __restrict
                                                            const uint32_t* __restrict__ wc,
                                                            const uint32_t* __restrict__ sc,
                                                            ull* __restrict__ pc_hist, DevCounters* ctr) {
+  __shared__ uint32_t tbin[kPcTab], tcnt[kPcTab];
+  pc_tab_init(tbin, tcnt);
   const ull stride = (ull)gridDim.x * blockDim.x;
   const ull nthreads = (cap + 255) / 256 * 256;
   ull distinct = 0;
   for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < nthreads; i += stride) {
     const ull v = i < cap ? table[i] : kEmptyKey;
-    pc_contrib(v >> 8, (uint32_t)(v & 0xFF), v != kEmptyKey, kl, site_of, filter, wc, sc, pc_hist, distinct);
+    pc_contrib(v >> 8, (uint32_t)(v & 0xFF), v != kEmptyKey, kl, site_of, filter, wc, sc, pc_hist, distinct, tbin,
+               tcnt);
   }
   for (int d = 16; d; d >>= 1) distinct += __shfl_xor_sync(CFULL, distinct, d);
   if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&ctr->distinct_pc, distinct);
+  pc_tab_flush(tbin, tcnt, pc_hist);
 }
 
 void launch_pc_hist_hash(const ull* table, ull cap, KeyLayout kl, const uint32_t* site_of, uint32_t launch_filter,

@@ -82,9 +82,12 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
   const ull gwarp = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
   for (ull v = gwarp; v < n_views; v += nwarps) {
-    // deferred view: p << 7 | stats_only << 6 | len.  stats_only: the fast
-    // kernel already emitted this view's keys and word counters; only the
-    // instruction statistics remain (a non-monotone instruction)
+    // deferred view: p << 7 | stats_only << 6 | len (len <= 32).  stats_only:
+    // the fast kernel already emitted this view's keys and word counters; only
+    // the instruction statistics remain (a non-monotone instruction).  A view
+    // may hold several whole instructions (short ones packed together by the
+    // fast kernel): they start at the view's first record and at every
+    // instr_start record inside it (G24)
     const ull e = a.deferred[v];
     const ull p = e >> 7;
     const bool keys_too = ((e >> 6) & 1u) == 0;
@@ -168,33 +171,53 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
       STAGE_PUSH(st, ha, (pa << 8) | mA, a.keys, &a.ctr->n_keys);
       STAGE_PUSH(st, hb, (pb << 8) | mB, a.keys, &a.ctr->n_keys);
     }
-    // instruction statistics, general case (G24)
+    // instruction statistics, general case (G24), per
+    // instruction of the view: lanes [s, e) between consecutive heads
+    const unsigned hb = __ballot_sync(FULL, act && (lane == 0 || ((cur.y >> 23) & 1u)));
     const unsigned vbm = __ballot_sync(FULL, valid);
     if (vbm) {
-      const int f = __ffs(vbm) - 1;
+      const unsigned le = lane_lt | (1u << lane);
+      const int s0 = 31 - __clz(hb & le);  // this lane's instruction starts here (lane 0 is a head)
+      const unsigned after = hb & ~le;
+      const int e0 = after ? __ffs(after) - 1 : 32;
+      const unsigned segm = (e0 >= 32 ? FULL : ((1u << e0) - 1u)) & ~((1u << s0) - 1u);
+      const unsigned svalid = vbm & segm;
+      const int f = svalid ? __ffs(svalid) - 1 : lane;
       const int i_obj = __shfl_sync(FULL, first_obj, f);
       const uint32_t i_launch = __shfl_sync(FULL, launch, f);
-      if (i_obj >= 0) {
-        const ull mn = warp_min64(valid ? lo : ~0ull);
-        const ull mx = warp_max64(valid ? hi : 0ull);
-        uint32_t distinct;
-        if (__ballot_sync(FULL, valid && strad) == 0) {
-          const unsigned m = __match_any_sync(FULL, valid ? sa : (0xFFFF000000000000ull | (ull)lane));
-          distinct = __popc(__ballot_sync(FULL, valid && (__ffs(m) - 1 == lane)));
-        } else {
-          bool dup_a = false, dup_b = !strad;
-          for (int j = 0; j < 32; ++j) {
-            const ull aj = __shfl_sync(FULL, sa, j), bj = __shfl_sync(FULL, sbk, j);
-            const bool vj = __shfl_sync(FULL, valid, j);
-            if (vj && j < lane) {
-              dup_a |= (sa == aj) || (sa == bj);
-              dup_b |= (sbk == aj) || (sbk == bj);
-            }
+      // min / max byte over the instruction's valid records: segmented scans
+      ull mn = valid ? lo : ~0ull, mx = valid ? hi : 0ull;
+      for (int d = 1; d < 32; d <<= 1) {
+        const ull omn = __shfl_down_sync(FULL, mn, d), omx = __shfl_down_sync(FULL, mx, d);
+        if (lane + d < e0) { mn = omn < mn ? omn : mn; mx = omx > mx ? omx : mx; }
+      }
+      // (lane s0 now holds its instruction's min and max)
+      uint32_t distinct;
+      if (__ballot_sync(FULL, valid && strad) == 0) {
+        const unsigned m = __match_any_sync(FULL, valid ? sa : (0xFFFF000000000000ull | (ull)lane));
+        distinct = __popc(__ballot_sync(FULL, valid && (__ffs(m & segm) - 1 == lane)) & segm);
+      } else {
+        bool dup_a = false, dup_b = !strad;
+        for (int j = 0; j < 32; ++j) {
+          const ull aj = __shfl_sync(FULL, sa, j), bj = __shfl_sync(FULL, sbk, j);
+          const bool vj = __shfl_sync(FULL, valid, j);
+          if (vj && j < lane && j >= s0) {
+            dup_a |= (sa == aj) || (sa == bj);
+            dup_b |= (sbk == aj) || (sbk == bj);
           }
-          distinct = __popc(__ballot_sync(FULL, valid && !dup_a)) + __popc(__ballot_sync(FULL, valid && !dup_b));
         }
-        const bool mis = distinct > (mx - mn + 1 + 31) / 32;
-        icache.add(i_launch * nobj + (uint32_t)i_obj + 1u, mis, sm.ikey, sm.ival, a.instr_ctr, lane);
+        distinct = __popc(__ballot_sync(FULL, valid && !dup_a) & segm) +
+                   __popc(__ballot_sync(FULL, valid && !dup_b) & segm);
+      }
+      const bool mis = svalid && i_obj >= 0 && distinct > (mx - mn + 1 + 31) / 32;
+      const bool counted = svalid && i_obj >= 0;
+      // one counter update per instruction, in order (warp-uniform loop over the heads)
+      for (unsigned m = hb & __ballot_sync(FULL, counted && lane == s0); m; m &= m - 1) {
+        const int h = __ffs(m) - 1;
+        const int o = __shfl_sync(FULL, i_obj, h);
+        const uint32_t la = __shfl_sync(FULL, i_launch, h);
+        const bool mh = __shfl_sync(FULL, mis, h);
+        icache.add(la * nobj + (uint32_t)o + 1u, mh, sm.ikey, sm.ival, a.instr_ctr, lane);
       }
     }
   }

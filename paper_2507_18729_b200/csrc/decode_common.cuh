@@ -244,6 +244,7 @@ struct InstrCache {
 // (site -> pc id) cache
 constexpr int kRingChunks = 8;          // fast kernel: per-warp record ring of 8 x 32 records (4 KB)
 constexpr int kAhead = 6;               // chunks in flight ahead of the current one (cp.async)
+constexpr uint32_t kShortView = 8;      // instructions shorter than this are packed for the general kernel
 constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16;
 // fixed-size parts first, at compile-time offsets (addresses are immediates,
 // nothing to keep in registers); the object table (3 x n u64) last

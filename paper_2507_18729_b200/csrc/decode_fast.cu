@@ -167,6 +167,19 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       const unsigned sb = __ballot_sync(FULL, (cur.y >> 23) & 1u) & ~1u;
       uint32_t len = sb ? (uint32_t)(__ffs(sb) - 1) : 32u;
       len = rem < len ? rem : len;
+      if (len < kShortView) {
+        // short instructions (divergent loops, e.g. SpMV rows): pack the whole
+        // instructions of the next 32 records into one general-path view
+        const uint32_t span = rem <= 32 ? rem : (sb ? 31u - __clz(sb) : 0u);  // to the last head / range end
+        if (span > len) {
+          if (lane == 0) {
+            const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);
+            a.deferred[slot] = ((p0 + off) << 7) | span;
+          }
+          off += span;
+          continue;
+        }
+      }
       const uint32_t offn = off + len;
 
       const bool act = lane < (int)len;

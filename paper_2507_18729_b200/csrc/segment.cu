@@ -36,19 +36,26 @@ __global__ void seg_hist_kernel(const ull* __restrict__ keys, ull n, KeyLayout k
 }
 
 // ---- 2. exclusive scan of the S_tot counts (3 phases) ----------------------------
+// a "big" sector (>= kSegCap keys) does not fit a chunk: its keys go to a
+// separate buffer (hash path) and its segment here is empty
+__device__ __forceinline__ uint32_t seg_len(uint32_t c) { return c >= (uint32_t)kSegCap ? 0u : c; }
+
 __global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __restrict__ bsum,
-                                uint32_t* __restrict__ maxc) {
+                                uint32_t* __restrict__ maxc, ull* __restrict__ nbig) {
   __shared__ ull s[kSegWarps];
   __shared__ uint32_t smax[kSegWarps];
   const ull base = (ull)blockIdx.x * kScanBlock;
-  ull t = 0;
+  ull t = 0, big = 0;
   uint32_t mx = 0;
   for (int i = threadIdx.x; i < kScanBlock; i += kSegThreads) {
     const ull j = base + i;
     const uint32_t v = j < n ? in[j] : 0u;
-    t += v;
+    t += seg_len(v);
+    big += v - seg_len(v);
     mx = v > mx ? v : mx;
   }
+  for (int d = 16; d; d >>= 1) big += __shfl_xor_sync(GFULL, big, d);
+  if ((threadIdx.x & 31) == 0 && big) atomicAdd(nbig, big);
   for (int d = 16; d; d >>= 1) {
     t += __shfl_xor_sync(GFULL, t, d);
     const uint32_t o = __shfl_xor_sync(GFULL, mx, d);
@@ -104,7 +111,7 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
-    v[k] = j < n ? in[j] : 0u;
+    v[k] = j < n ? seg_len(in[j]) : 0u;
     t += v[k];
   }
   ull incl = t;
@@ -130,19 +137,36 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 // atomics' latency (contended cursors of hot sectors), not bandwidth, bounds it
 constexpr int kScatterPer = 8;
 __global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
-                                                          ull* __restrict__ cur, ull* __restrict__ out) {
+                                                          ull* __restrict__ cur, ull* __restrict__ out,
+                                                          const uint32_t* __restrict__ cnt, ull* __restrict__ big,
+                                                          ull* __restrict__ nbig_ctr) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const ull tile = (ull)blockDim.x * kScatterPer;
   for (ull t0 = (ull)blockIdx.x * tile; t0 < n; t0 += (ull)gridDim.x * tile) {
     ull k[kScatterPer], pos[kScatterPer];
     const ull i0 = t0 + threadIdx.x;
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) k[u] = i0 + (ull)u * blockDim.x < n ? keys[i0 + (ull)u * blockDim.x] : 0;
+    bool isbig[kScatterPer];
 #pragma unroll
-    for (int u = 0; u < kScatterPer; ++u)
-      if (i0 + (ull)u * blockDim.x < n) pos[u] = atomicAdd(&cur[key_g(k[u], kl)], 1ull);
+    for (int u = 0; u < kScatterPer; ++u) {
+      const bool in = i0 + (ull)u * blockDim.x < n;
+      isbig[u] = in && cnt[key_g(k[u], kl)] >= (uint32_t)kSegCap;
+      if (in && !isbig[u]) pos[u] = atomicAdd(&cur[key_g(k[u], kl)], 1ull);
+    }
 #pragma unroll
-    for (int u = 0; u < kScatterPer; ++u)
-      if (i0 + (ull)u * blockDim.x < n) out[pos[u]] = k[u];
+    for (int u = 0; u < kScatterPer; ++u) {
+      const unsigned bb = __ballot_sync(GFULL, isbig[u]);  // big keys: one append per warp
+      if (bb) {
+        ull b0 = 0;
+        if (lane == __ffs(bb) - 1) b0 = atomicAdd(nbig_ctr, (ull)__popc(bb));
+        b0 = __shfl_sync(GFULL, b0, __ffs(bb) - 1);
+        if (isbig[u]) big[b0 + __popc(bb & lt)] = k[u];
+      }
+      if (i0 + (ull)u * blockDim.x < n && !isbig[u]) out[pos[u]] = k[u];
+    }
   }
 }
 
@@ -398,15 +422,15 @@ cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
     if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
     ws.cap_sec = nsec + 1;
   }
-  if (!ws.maxc && (e = cudaMalloc(&ws.maxc, sizeof(uint32_t)))) return e;
+  if (!ws.maxc && (e = cudaMalloc(&ws.maxc, 4 * sizeof(ull)))) return e;  // maxc, big total, big cursor
   return cudaSuccess;
 }
 
 cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
-                            cudaStream_t s, uint32_t* max_per_sector, bool counted) {
+                            cudaStream_t s, uint32_t* max_per_sector, ull* n_big, bool counted) {
   cudaError_t e;
   if ((e = segment_reserve(ws, nsec))) return e;
-  cudaMemsetAsync(ws.maxc, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(ws.maxc, 0, 4 * sizeof(ull), s);  // maxc, big-key total, big-key cursor
   if (!counted) {
     cudaMemsetAsync(ws.cnt, 0, (nsec + 1) * sizeof(uint32_t), s);
     if (n) {
@@ -416,21 +440,27 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
     }
   }
   const ull nb = (nsec + kScanBlock - 1) / kScanBlock;
-  seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
+  seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc,
+                                                       reinterpret_cast<ull*>(ws.maxc) + 1);
   seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
   seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.cur);
   ws.launches += 3;
-  if ((e = cudaMemcpyAsync(max_per_sector, ws.maxc, sizeof(uint32_t), cudaMemcpyDeviceToHost, s))) return e;
-  return cudaStreamSynchronize(s);
+  ull hv[2];
+  if ((e = cudaMemcpyAsync(hv, ws.maxc, 2 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
+  if ((e = cudaStreamSynchronize(s))) return e;
+  *max_per_sector = (uint32_t)hv[0];
+  *n_big = hv[1];
+  return cudaSuccess;
 }
 
 // phases 3-4: keys -> out (grouped by sector) -> dense counts (+ per-pc histograms)
-cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull nsec, uint32_t filter,
+cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout kl, ull nsec, uint32_t filter,
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
                           DevCounters* ctr, int num_sms, cudaStream_t s) {
   if (n) {
     const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
-    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cur, out);
+    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cur, out, ws.cnt, big,
+                                            reinterpret_cast<ull*>(ws.maxc) + 2);
   }
   const size_t smem = segment_chunk_smem();
   static bool attr = false;

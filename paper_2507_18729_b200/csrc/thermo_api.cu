@@ -617,7 +617,8 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
   ctx->records = 0;
   ctx->state = 1;
   ctx->hist_valid = false;
-  ctx->seg_counted = !ctx->comm && (ctx->cfg.dedup == THERMO_DEDUP_AUTO || ctx->cfg.dedup == THERMO_DEDUP_SEGMENT);
+  ctx->seg_counted = !ctx->comm && ctx->S_tot <= (1ull << 25) &&
+                     (ctx->cfg.dedup == THERMO_DEDUP_AUTO || ctx->cfg.dedup == THERMO_DEDUP_SEGMENT);
   if (ctx->seg_counted) CK(cudaMemsetAsync(ctx->seg.cnt, 0, (ctx->S_tot + 1) * sizeof(uint32_t), ctx->stream));
   ctx->n_exch = 0;
   ctx->pc_mapped = 0;
@@ -748,38 +749,74 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
-  uint32_t mode = ctx->cfg.dedup == THERMO_DEDUP_AUTO ? THERMO_DEDUP_SEGMENT : ctx->cfg.dedup;
+  // AUTO, chosen by measurement: the SEGMENT counting sort keeps
+  // its per-sector cursors cache-resident up to ~2^25 sectors (SGEMM 5.3 ms vs
+  // HASH 6.3 ms; stencil 2^24 sectors 48 vs 62 ms); beyond, its scatter
+  // degenerates into random HBM atomics and the hash set wins (SpMV s=24,
+  // 2^26 sectors: 170 vs 228 ms)
+  uint32_t mode = ctx->cfg.dedup;
+  if (mode == THERMO_DEDUP_AUTO) mode = ctx->S_tot <= (1ull << 25) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
   bool pc_done = false;
   // ---- a4 dedup + a5 count (+ a6 per-pc on the segment path) ----
   if (mode == THERMO_DEDUP_SEGMENT) {
-    // counting sort by sector; falls back to the onesweep path when one
-    // sector holds more keys than a shared-memory chunk
+    // counting sort by sector + per-chunk shared-memory dedup; the keys of
+    // sectors too big for a chunk (hot sectors: >= 2048 warps x pcs) take the
+    // hash path below
     CK(cudaEventRecord(ctx->evp[0], s));
     uint32_t maxc = 0;
-    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc,
+    ull n_big = 0;
+    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc, &n_big,
                         ctx->seg_counted);
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment prepare: ") + cudaGetErrorString(e));
-    if (maxc < segment_chunk_cap()) {
-      if (ctx->sw.alt_cap < ctx->n_keys) {
-        dfree(ctx->sw.alt);
-        ctx->sw.alt_cap = ctx->n_keys + ctx->n_keys / 8 + 1024;
-        CK(dalloc(&ctx->sw.alt, ctx->sw.alt_cap));
-      }
-      CK(cudaEventRecord(ctx->evp[1], s));
-      e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, kl, ctx->S_tot, launch_filter, ctx->seg, ctx->d_wc,
-                        ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
-                        ctx->num_sms, s);
-      if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
-      ctx->launches += ctx->seg.launches;
-      ctx->seg.launches = 0;
-      pc_done = true;
-    } else {
-      mode = THERMO_DEDUP_SORT;
-      ctx->launches += ctx->seg.launches;
-      ctx->seg.launches = 0;
+    if (ctx->sw.alt_cap < ctx->n_keys) {
+      dfree(ctx->sw.alt);
+      ctx->sw.alt_cap = ctx->n_keys + ctx->n_keys / 8 + 1024;
+      CK(dalloc(&ctx->sw.alt, ctx->sw.alt_cap));
     }
+    if (n_big && ctx->pckeys_cap < n_big) {  // the big keys' buffer (the pc-key buffer is free here)
+      dfree(ctx->d_pckeys);
+      ctx->pckeys_cap = n_big + n_big / 8 + 1024;
+      CK(dalloc(&ctx->d_pckeys, ctx->pckeys_cap));
+    }
+    CK(cudaEventRecord(ctx->evp[1], s));
+    e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, ctx->d_pckeys, kl, ctx->S_tot, launch_filter, ctx->seg,
+                      ctx->d_wc, ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
+                      ctx->num_sms, s);
+    if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
+    ctx->launches += ctx->seg.launches;
+    ctx->seg.launches = 0;
+    if (n_big) {
+      // (sector, launch, warp) dedup of the big keys in an HBM hash set, counted
+      // into the same dense arrays (their sectors are disjoint from the chunks')
+      const ull cap = next_pow2(std::max<ull>(1024, 2 * n_big));
+      if (ctx->table_cap < cap) {
+        dfree(ctx->d_table);
+        ctx->table_cap = cap;
+        CK(dalloc(&ctx->d_table, cap));
+      }
+      CK(cudaMemsetAsync(ctx->d_table, 0xFF, cap * 8, s));
+      launch_hash_insert(ctx->d_pckeys, n_big, ctx->d_table, cap - 1, kl.P, ctx->d_ctr, ctx->num_sms, s);
+      launch_count_hash(ctx->d_table, cap, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
+      ctx->launches += 2;
+      if (ctx->cfg.track_pc) {  // and their (pc, sector) facts, after the counts are final
+        launch_pc_extract(ctx->d_pckeys, n_big, kl, ctx->sw.alt, ctx->num_sms, s);  // (chunks are done with alt)
+        const ull pcap = next_pow2(std::max<ull>(1024, 2 * n_big));
+        if (ctx->pctable_cap < pcap) {
+          dfree(ctx->d_pctable);
+          ctx->pctable_cap = pcap;
+          CK(dalloc(&ctx->d_pctable, pcap));
+        }
+        CK(cudaMemsetAsync(ctx->d_pctable, 0xFF, pcap * 8, s));
+        launch_hash_insert(ctx->sw.alt, n_big, ctx->d_pctable, pcap - 1, 0, ctx->d_ctr, ctx->num_sms, s);
+        launch_pc_hist_hash(ctx->d_pctable, pcap, kl, site_tab, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_pchist,
+                            ctx->d_ctr, ctx->num_sms, s);
+        ctx->launches += 3;
+      }
+    }
+    pc_done = true;
+    (void)maxc;
   }
   ctx->dedup_used = mode;
   if (mode == THERMO_DEDUP_SORT) {

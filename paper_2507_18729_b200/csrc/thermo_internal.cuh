@@ -122,17 +122,19 @@ struct SegWorkspace {
   ull* off = nullptr;        // [S_tot + 1] exclusive prefix (off[S_tot] = total)
   ull* cur = nullptr;        // [S_tot + 1] scatter cursors
   ull* bsum = nullptr;       // scan block sums
-  uint32_t* maxc = nullptr;  // max keys in one sector
+  uint32_t* maxc = nullptr;  // [4 u64]: max keys in one sector, big-sector keys, big cursor
   ull cap_sec = 0;
   ull launches = 0;
 };
 // counted: ws.cnt already holds the keys per sector (counted by the decoder)
 cudaError_t segment_reserve(SegWorkspace& ws, ull nsec);
+// n_big: keys of sectors too big for a chunk (they go to the hash path)
 cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegWorkspace& ws, int num_sms,
-                            cudaStream_t s, uint32_t* max_per_sector, bool counted);
+                            cudaStream_t s, uint32_t* max_per_sector, ull* n_big, bool counted);
 // scatter + per-chunk dedup: dense counts (a5) and, if pc_hist != null, the
 // per-pc histograms (a6) of the chunk's sectors
-cudaError_t segment_count(const ull* keys, ull n, ull* out, KeyLayout kl, ull nsec, uint32_t filter,
+// big: receives the keys of the big sectors (capacity n_big from prepare)
+cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout kl, ull nsec, uint32_t filter,
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
                           DevCounters* ctr, int num_sms, cudaStream_t s);
 ull segment_chunk_cap();

@@ -219,3 +219,36 @@ def test_stencil_full_size_closed_form_and_sample():
     for row, o, sct in zip(ref, oi, se):
         b = th.heatmap(int(o), BOTH).reshape(-1, 9)[sct]
         assert np.array_equal(b, row), (o, sct)
+
+
+def _hot_sector_trace(n=40000, hot_warps=6000, seed=3):
+    """A hot object (2 sectors read by thousands of warps, more keys than a
+    SEGMENT chunk holds) beside a spread one; instructions of 1-3 records
+    (packed into multi-instruction views by the fast decoder)."""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    objects = [(0x100000, 64, 0, 7, "hot"), (0x200000, 1 << 16, 0, 8, "spread")]
+    hot = torch.rand(n, generator=g) < 0.5
+    addr = torch.where(hot, 0x100000 + 4 * torch.randint(0, 16, (n,), generator=g),
+                       0x200000 + 4 * torch.randint(0, 1 << 14, (n,), generator=g))
+    warp = torch.where(hot, torch.randint(0, hot_warps, (n,), generator=g), torch.randint(0, 100, (n,), generator=g))
+    # instructions: a record starts one with probability 1/2 and then shares the warp/pc of its head
+    istart = (torch.rand(n, generator=g) < 0.5).to(torch.int64)
+    istart[0] = 1
+    iid = torch.cumsum(istart, 0) - 1
+    heads = torch.nonzero(istart).flatten()
+    warp = warp[heads][iid]
+    hot = hot[heads][iid]
+    addr = torch.where(hot, 0x100000 + (addr & 63), 0x200000 + (addr & 0xFFFF))
+    pc = torch.where(hot, 0x500, 0x510 + 16 * (iid % 3))
+    rec = tg.pack_records(addr, 2, 0, 0, istart, warp, pc, 0)
+    return tg.Trace("hot-sector", objects, rec, meta=dict(warps=hot_warps, launches=1))
+
+
+@pytest.mark.parametrize("dedup", [0, 1, 2, 3])
+def test_hot_sector_and_short_instructions(dedup):
+    t = _hot_sector_trace()
+    orc, th = run_both(t, dedup=dedup)
+    compare(orc, th, t)
+    if dedup in (0, 3):
+        assert th.stats()["dedup_used"] == 3  # SEGMENT with its big-sector side path, no fallback
