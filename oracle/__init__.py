@@ -81,6 +81,7 @@ def _load():
         L.orc_build.argtypes = [vp, u32]
         L.orc_word_counts.argtypes = [vp, u32, vp]
         L.orc_sector_counts.argtypes = [vp, u32, vp]
+        L.orc_access_counts.argtypes = [vp, u32, vp]
         L.orc_sample.argtypes = [vp, vp, vp, sz, vp]
         L.orc_hist.argtypes = [vp, u32, ctypes.c_int, vp]
         L.orc_n_pcs.restype = sz
@@ -148,6 +149,12 @@ class Oracle:
     def sector_counts(self, o) -> np.ndarray:
         out = np.zeros(self.n_sectors(o), dtype=np.uint32)
         _load().orc_sector_counts(self._h, o, _ptr(out))
+        return out
+
+    def access_counts(self, o) -> np.ndarray:
+        """Lane accesses per word of object index o, all launches (G27)."""
+        out = np.zeros(self.n_words(o), dtype=np.uint32)
+        _load().orc_access_counts(self._h, o, _ptr(out))
         return out
 
     def sample(self, obj_idx, sectors) -> np.ndarray:

@@ -93,6 +93,9 @@ struct Oracle {
   std::unordered_map<uint64_t, std::set<uint64_t>> wset;
   // per-PC: (launch<<32 | pc) -> set of (o, w)        (G11)
   std::map<uint64_t, std::set<std::pair<uint32_t, uint64_t>>> pcset;
+  // access counts: lane accesses per word,
+  // over every ingested launch (G27)
+  std::unordered_map<uint64_t, uint64_t> access;
   // misalignment counters per (launch, o)   (G24)
   std::map<std::pair<uint32_t, uint32_t>, std::pair<uint64_t, uint64_t>> instr;
   // stats
@@ -165,6 +168,7 @@ struct Oracle {
         uint64_t wl = w - objs[o].base / 4;  // object-local word index
         if (restricted && !allow.count({uint32_t(o), wl / 8})) continue;
         wset[wkey(uint32_t(o), wl)].insert((uint64_t(r.launch) << 32) | r.warp);
+        access[wkey(uint32_t(o), wl)] += 1;  // every access, not distinct warps (Fig. 3 baseline)
         pcset[(uint64_t(r.launch) << 32) | r.pc].insert({uint32_t(o), wl});
       }
     }
@@ -289,6 +293,17 @@ void orc_sector_counts(void* h, uint32_t o, uint32_t* out) {
   Oracle* p = static_cast<Oracle*>(h);
   std::copy(p->sector_count[o].begin(), p->sector_count[o].end(), out);
 }
+// access counts of object index `o`: number of (record, word) pairs per word,
+// all launches (the metric Fig. 3 shows to be blind to sharing)
+void orc_access_counts(void* h, uint32_t o, uint32_t* out) {
+  Oracle* p = static_cast<Oracle*>(h);
+  const uint64_t nw = (p->objs[o].len + 3) / 4;
+  for (uint64_t w = 0; w < nw; ++w) {
+    auto it = p->access.find(Oracle::wkey(o, w));
+    out[w] = it == p->access.end() ? 0u : uint32_t(it->second);
+  }
+}
+
 // counts of selected (object index, local sector) pairs: out[9*i .. 9*i+8] =
 // 8 word counts then the sector count (words past n_words read as 0)
 void orc_sample(void* h, const uint32_t* obj_idx, const uint64_t* sectors, size_t n, uint32_t* out) {

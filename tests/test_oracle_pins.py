@@ -48,9 +48,9 @@ def test_fig3_discrimination():
         wc, sc = o.word_counts(0), o.sector_counts(0)
         assert (wc[:8] == g["word_temp"]).all()
         assert sc[0] == g["sector_temp"]
-        # access counts (the baseline metric the paper argues against)
-        f = R.fields(t.records)
-        acc = np.bincount((f["addr"] - t.objects[0][0]) // 4, minlength=8)[:8]
+        # access counts (the baseline metric the paper argues against): the
+        # oracle's access counts against the figure's values
+        acc = o.access_counts(0)[:8]
         assert (acc == g["access_per_word"]).all() and acc.sum() == g["access_per_sector"]
     assert labels_of(run(tg.fig3("b")), 0) == ["FalseSharing"]
     assert labels_of(run(tg.fig3("a")), 0) == []
@@ -372,3 +372,26 @@ def test_indicators_from_brute_counts():
                 assert (ind["dom_gap"], ind["dom_count"]) == (vals[j], cnt[j])
             else:
                 assert (ind["dom_gap"], ind["dom_count"]) == (0, 0)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_access_counts_brute_force_and_bounds(seed):
+    """Access counts: brute force over the records'
+    touched words (all launches), and temperature <= accesses, equal zeros."""
+    t = tg.random_trace(n=6000, seed=seed, n_launches=3)
+    o = run(t, launch_filter=1)  # the launch filter does not apply to accesses
+    f = R.fields(t.records)
+    for k, (base, ln, space, _id, _l) in enumerate(t.objects):
+        nw = (ln + 3) // 4
+        ref = np.zeros(nw, dtype=np.int64)
+        for a, sz, sp, ok in zip(f["addr"], f["size"], f["space"], f["valid"]):
+            if not ok or sp != space:
+                continue
+            for w in range(a >> 2, ((a + sz - 1) >> 2) + 1):
+                if base <= 4 * w < base + ln:
+                    ref[w - base // 4] += 1
+        acc = o.access_counts(k)
+        assert np.array_equal(acc, ref)
+        o_all = run(t)
+        wc = o_all.word_counts(k)
+        assert (wc <= acc).all() and ((wc == 0) == (acc == 0)).all()
