@@ -116,7 +116,8 @@ typedef struct {
   uint32_t max_pcs;               /* >= 1; distinct (launch, pc) pairs (<= 65536)    */
   uint32_t dedup;                 /* thermo_dedup                                    */
   uint32_t track_pc;              /* 1: maintain per-PC histograms (G11)             */
-  uint32_t reserved0;
+  uint32_t track_access;          /* 1: also count lane accesses per word (the Fig. 3
+                                     baseline; thermo_query_access)       */
   uint64_t expected_pairs;        /* hash sizing hint: distinct (sector,warp) pairs; 0 = auto */
 } thermo_config;
 
@@ -300,6 +301,17 @@ thermo_status thermo_query_heatmap(thermo_ctx *ctx, uint32_t object_id, thermo_g
 /* Level histogram (THERMO_LEVELS bins, HOST buffer) of one object over all its
  * n_words words (THERMO_WORD) or n_sectors sectors (THERMO_SECTOR); level-0
  * counts untouched ones.  Errors: EINVAL, ESTATE. */
+/*
+ * Access counts (Fig. 3: equal access counts,
+ * different temperatures): out[w] = number of (record, word) pairs touching
+ * word w of object `object_id`, over every ingested launch (G27; the build's
+ * launch filter does not apply), n_words values.  Needs a context created
+ * with track_access = 1.  Sharded mode: this rank's records only -- the job's
+ * counts are the element-wise sum over ranks.  Available after ingest.
+ * Errors: ESTATE (track_access off), EINVAL (unknown id), ERANGE (cap), ECUDA.
+ */
+thermo_status thermo_query_access(thermo_ctx *ctx, uint32_t object_id, uint32_t *out, size_t cap, size_t *n_out);
+
 thermo_status thermo_query_histogram(thermo_ctx *ctx, uint32_t object_id, thermo_granularity g,
                                      uint64_t hist[THERMO_LEVELS]);
 

@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
       }
     }
     if (!keys_too) { fa = fb = 0; }  // keys and counters came from the fast kernel
+    if (a.acc) {  // access counts (track_access)
+      for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * ga + (__ffs(m) - 1)], 1u);
+      for (uint32_t m = fb; m; m &= m - 1) atomicAdd(&a.acc[8ull * gb + (__ffs(m) - 1)], 1u);
+    }
     // pc id of each lane (usually one per view)
     uint32_t pcid = 0;
     if (a.track_pc) {

@@ -247,6 +247,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       bool has = fa != 0;
       uint32_t mk = fa;
       const uint32_t g = sbase + ((xs - blo) >> 5);
+      if (a.acc) {  // access counts: every lane's every mapped word (before the merge)
+        for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * g + (__ffs(m) - 1)], 1u);
+      }
       adjacent_merge32(g, mk, has, lane);
       if (__any_sync(FULL, has)) {
         const ull lw = ((ull)launch0 << W) | z0;

@@ -105,6 +105,7 @@ struct thermo_ctx {
   float ms_ingest = 0, ms_build = 0, ms_classify = 0;
   bool hist_valid = false;
   bool seg_counted = false;  // the decoder counts keys per sector (SEGMENT histogram, one rank)
+  uint32_t* d_acc = nullptr;  // [8 S_tot] lane accesses per word (track_access)
 
   // sharded mode (row e, shard.cu); comm == nullptr: one rank
   Comm* comm = nullptr;
@@ -225,6 +226,7 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.launch_ctr = ctx->d_launch_ctr;
   a.deferred = ctx->d_deferred;
   a.seg_cnt = ctx->seg_counted ? ctx->seg.cnt : nullptr;
+  a.acc = ctx->d_acc;
   launch_decode(a, ctx->num_sms, ctx->stream);
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());
@@ -478,7 +480,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
-                  ctx->d_launch_g};
+                  ctx->d_launch_g, ctx->d_acc};
   for (void* b : bufs) dfree(b);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_pinned[i]) cudaFreeHost(ctx->h_pinned[i]);
@@ -593,6 +595,8 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   CK(dalloc(&ctx->d_pc_vals, ctx->pc_cap));
   CK(dalloc(&ctx->d_site_of, c.max_pcs));
   CK(segment_reserve(ctx->seg, soff));
+  if (c.track_access && dalloc(&ctx->d_acc, 8 * soff) != cudaSuccess)
+    return fail(ctx, THERMO_ENOMEM, "access-count array");
   if (ctx->comm) {
     CK(dalloc(&ctx->d_pcmap, c.max_pcs));
     CK(dalloc(&ctx->d_site_glob, c.max_pcs));
@@ -620,6 +624,7 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
   ctx->seg_counted = !ctx->comm && ctx->S_tot <= (1ull << 25) &&
                      (ctx->cfg.dedup == THERMO_DEDUP_AUTO || ctx->cfg.dedup == THERMO_DEDUP_SEGMENT);
   if (ctx->seg_counted) CK(cudaMemsetAsync(ctx->seg.cnt, 0, (ctx->S_tot + 1) * sizeof(uint32_t), ctx->stream));
+  if (ctx->d_acc) CK(cudaMemsetAsync(ctx->d_acc, 0, 8 * ctx->S_tot * sizeof(uint32_t), ctx->stream));
   ctx->n_exch = 0;
   ctx->pc_mapped = 0;
   ctx->glob_sites.clear();
@@ -934,6 +939,21 @@ thermo_status thermo_query_heatmap(thermo_ctx* ctx, uint32_t object_id, thermo_g
       for (int b = 0; b < 8; ++b)
         if (8 * s2 + b >= nw) out[9 * s2 + b] = 0;
   }
+  return THERMO_OK;
+}
+
+thermo_status thermo_query_access(thermo_ctx* ctx, uint32_t object_id, uint32_t* out, size_t cap, size_t* n_out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (!ctx->d_acc) return fail(ctx, THERMO_ESTATE, "context created with track_access = 0");
+  auto it = ctx->id_to_reg.find(object_id);
+  if (it == ctx->id_to_reg.end()) return fail(ctx, THERMO_EINVAL, "unknown object id");
+  const uint32_t j = ctx->reg_to_sorted[it->second];
+  const ull nw = ctx->h_nwords[j], so = ctx->h_soff[j];
+  if (n_out) *n_out = nw;
+  if (!out || cap < nw) return fail(ctx, THERMO_ERANGE, "output capacity too small");
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(out, ctx->d_acc + 8 * so, nw * 4, cudaMemcpyDeviceToHost));
   return THERMO_OK;
 }
 

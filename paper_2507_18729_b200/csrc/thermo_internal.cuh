@@ -94,6 +94,7 @@ struct DecodeArgs {
   ull* launch_ctr;        // [max_launches * 2] (unmapped words, mapped word accesses)
   ull* deferred;          // [n] p << 7 | stats_only << 6 | len of deferred views
   uint32_t* seg_cnt;      // [S_tot] keys per sector (SEGMENT histogram), or null
+  uint32_t* acc;          // [8 S_tot] lane accesses per word (track_access), or null
 };
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------

@@ -36,7 +36,7 @@ class thermo_object(ctypes.Structure):
 
 class thermo_config(ctypes.Structure):
     _fields_ = [("max_launches", u32), ("max_warps_per_launch", u32), ("max_pcs", u32), ("dedup", u32),
-                ("track_pc", u32), ("reserved0", u32), ("expected_pairs", u64)]
+                ("track_pc", u32), ("track_access", u32), ("expected_pairs", u64)]
 
 
 PARAM_FIELDS = ("theta_hot", "alpha_num", "alpha_den", "beta_num", "beta_den", "fs_min", "smem_cap",
@@ -77,7 +77,7 @@ EXPORTS = ("thermo_default_config", "thermo_default_params", "thermo_abi_version
            "thermo_create_dist", "thermo_nccl_unique_id", "thermo_destroy", "thermo_reset",
            "thermo_register_objects", "thermo_ingest_trace", "thermo_build_heatmap", "thermo_query_heatmap",
            "thermo_query_histogram", "thermo_query_per_pc", "thermo_classify", "thermo_get_stats",
-           "thermo_last_error", "thermo_create_local_shards", "thermo_sharding")
+           "thermo_last_error", "thermo_create_local_shards", "thermo_sharding", "thermo_query_access")
 
 _lib = None
 
@@ -108,6 +108,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.thermo_build_heatmap.argtypes = [vp, ctypes.c_int, u32]
     L.thermo_query_heatmap.argtypes = [vp, u32, ctypes.c_int, vp, sz, P(sz)]
     L.thermo_query_histogram.argtypes = [vp, u32, ctypes.c_int, vp]
+    L.thermo_query_access.argtypes = [vp, u32, vp, sz, P(sz)]
     L.thermo_query_per_pc.argtypes = [vp, ctypes.c_int, P(thermo_pc_hist), sz, P(sz)]
     L.thermo_classify.argtypes = [vp, P(thermo_params), P(thermo_indicators), sz, P(sz)]
     L.thermo_get_stats.argtypes = [vp, P(thermo_stats)]
@@ -138,11 +139,11 @@ def label_names(bits: int) -> list[str]:
 
 
 def _config(max_launches: int = 1, max_warps_per_launch: int = 1 << 20, max_pcs: int = 4096,
-            dedup: int = DEDUP_AUTO, track_pc: bool = True) -> thermo_config:
+            dedup: int = DEDUP_AUTO, track_pc: bool = True, track_access: bool = False) -> thermo_config:
     cfg = thermo_config()
     load().thermo_default_config(ctypes.byref(cfg))
     cfg.max_launches, cfg.max_warps_per_launch, cfg.max_pcs = max_launches, max_warps_per_launch, max_pcs
-    cfg.dedup, cfg.track_pc = dedup, int(bool(track_pc))
+    cfg.dedup, cfg.track_pc, cfg.track_access = dedup, int(bool(track_pc)), int(bool(track_access))
     return cfg
 
 
@@ -257,6 +258,14 @@ class Thermo:
         out = np.zeros(n.value, dtype=np.uint32)
         self._ck(self.L.thermo_query_heatmap(self.h, object_id, granularity, out.ctypes.data, n.value,
                                              ctypes.byref(n)))
+        return out
+
+    def access(self, object_id: int) -> np.ndarray:
+        """Lane accesses per word (thermo_query_access; track_access=True)."""
+        n = sz()
+        self.L.thermo_query_access(self.h, object_id, None, 0, ctypes.byref(n))
+        out = np.zeros(n.value, dtype=np.uint32)
+        self._ck(self.L.thermo_query_access(self.h, object_id, out.ctypes.data, n.value, ctypes.byref(n)))
         return out
 
     def histogram(self, object_id: int, granularity: int) -> np.ndarray:

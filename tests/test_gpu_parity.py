@@ -252,3 +252,27 @@ def test_hot_sector_and_short_instructions(dedup):
     compare(orc, th, t)
     if dedup in (0, 3):
         assert th.stats()["dedup_used"] == 3  # SEGMENT with its big-sector side path, no fallback
+
+
+@pytest.mark.parametrize("case", ["tiny", "fig3a", "fig3b", "gemm", "stencil", "random", "hot"])
+def test_access_counts(case):
+    """Access counts: lane accesses per word, every
+    launch, through thermo_query_access, against the oracle."""
+    from paper_2507_18729_b200 import Thermo
+    t = {"tiny": lambda: tg.tiny("B"), "fig3a": lambda: tg.fig3("a"), "fig3b": lambda: tg.fig3("b"),
+         "gemm": lambda: tg.gemm(128, 96, 40, "v01"), "stencil": lambda: tg.stencil(96),
+         "random": lambda: tg.random_trace(n=30000, seed=8, n_warps=300, n_launches=3),
+         "hot": lambda: _hot_sector_trace()}[case]()
+    ml = max(1, int(t.meta.get("launches", 1)))
+    th = Thermo(max_launches=ml, max_warps_per_launch=1 << 22, track_access=True)
+    th.register_objects(t.objects)
+    calls = t.calls() if case != "random" else [t.records[a:b] for a, b in tg.split_calls(t.n, t.records, 3)]
+    for c in calls:
+        th.ingest(c.cuda().contiguous())
+    orc = oracle.run([o[:4] for o in t.objects], calls, 1 if case == "random" else oracle.ALL_LAUNCHES)
+    for k, obj in enumerate(t.objects):
+        assert np.array_equal(th.access(obj[3]), orc.access_counts(k)), (case, obj[4])
+    th.build(BOTH)  # the heat map is unaffected by track_access
+    orc2 = oracle.run([o[:4] for o in t.objects], calls)
+    for k, obj in enumerate(t.objects):
+        assert np.array_equal(th.heatmap(obj[3], WORD), orc2.word_counts(k))
