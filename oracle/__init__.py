@@ -78,6 +78,7 @@ def _load():
         L.orc_free.argtypes = [vp]
         L.orc_restrict.argtypes = [vp, vp, vp, sz]
         L.orc_ingest.argtypes = [vp, vp, sz]
+        L.orc_block_scope.argtypes = [vp, u32, u32]
         L.orc_build.argtypes = [vp, u32]
         L.orc_word_counts.argtypes = [vp, u32, vp]
         L.orc_sector_counts.argtypes = [vp, u32, vp]
@@ -125,6 +126,10 @@ class Oracle:
         oi = np.ascontiguousarray(obj_idx, dtype=np.uint32)
         se = np.ascontiguousarray(sectors, dtype=np.uint64)
         _load().orc_restrict(self._h, _ptr(oi), _ptr(se), len(oi))
+
+    def block_scope(self, warps_per_block: int, block: int):
+        """Keep only the records of one sampled block; call before ingest."""
+        _load().orc_block_scope(self._h, warps_per_block, block)
 
     def ingest(self, records):
         """records: anything exposing 16-byte records (numpy/torch int32 [n,4])."""

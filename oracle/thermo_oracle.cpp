@@ -85,6 +85,10 @@ typedef unsigned __int128 u128;
 
 struct Oracle {
   std::vector<Obj> objs;  // in registration order
+  // sampled-block scope: block_warps != 0 keeps
+  // only the records of global block `block_id` (warp / block_warps); the others
+  // were never traced
+  uint32_t block_warps = 0, block_id = 0;
   // restriction (sampled mode): only these (object index, local sector) pairs
   bool restricted = false;
   std::set<std::pair<uint32_t, uint64_t>> allow;
@@ -145,6 +149,7 @@ struct Oracle {
       // a longer run without instr_start is split every 32 records (G24)
       if (k == 0 || r.instr_start || pos == 32) { close_instr(); in_instr = true; pos = 0; }
       ++pos;
+      if (block_warps && r.warp / block_warps != block_id) continue;  // outside the sampled block
       if (!r.valid) { ++n_invalid; continue; }
       // ---- instruction extent (Fig.6) ----
       uint64_t lo = (uint64_t(r.space) << 48) | r.addr;
@@ -276,6 +281,13 @@ void orc_restrict(void* h, const uint32_t* obj_idx, const uint64_t* sectors, siz
   Oracle* o = static_cast<Oracle*>(h);
   o->restricted = true;
   for (size_t i = 0; i < n; ++i) o->allow.insert({obj_idx[i], sectors[i]});
+}
+
+// sampled-block scope: only block `block` of `warps_per_block` warps
+void orc_block_scope(void* h, uint32_t warps_per_block, uint32_t block) {
+  Oracle* o = static_cast<Oracle*>(h);
+  o->block_warps = warps_per_block;
+  o->block_id = block;
 }
 
 void orc_ingest(void* h, const void* recs, size_t n) {

@@ -395,3 +395,33 @@ def test_access_counts_brute_force_and_bounds(seed):
         o_all = run(t)
         wc = o_all.word_counts(k)
         assert (wc <= acc).all() and ((wc == 0) == (acc == 0)).all()
+
+
+@pytest.mark.parametrize("block", [0, 3])
+def test_block_scope(block):
+    """Sampled-block mode: the oracle's block
+    scope equals the trace pre-filtered to that block's warps, and -- warp ids
+    being < 64 inside one block -- the paper's own per-sector bitmask algorithm
+     on those records."""
+    t = tg.gemm(64, 64, 16, "v00")           # block 32x32: 32 warps per block
+    o = oracle.Oracle(objs(t))
+    o.block_scope(32, block)
+    o.ingest(t.records)
+    o.build()
+    f = R.fields(t.records)
+    keep = (f["warp"] // 32) == block
+    sub = t.records[torch.from_numpy(np.nonzero(keep)[0])]
+    assert sub.shape[0] > 0
+    p = oracle.Oracle(objs(t))
+    p.ingest(sub)
+    p.build()
+    loc = sub.clone()
+    loc[:, 2] = loc[:, 2] % 32                # warp index inside the block (P:291)
+    ref = R.paper_bitmask(loc)
+    for k, (base, ln, space, _id, _l) in enumerate(t.objects):
+        assert np.array_equal(o.word_counts(k), p.word_counts(k))
+        assert np.array_equal(o.sector_counts(k), p.sector_counts(k))
+        sc = o.sector_counts(k)
+        for s in range(len(sc)):
+            want = ref.get((space, (base >> 5) + s), [0] * 9)
+            assert sc[s] == want[8]
