@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define THERMO_ABI_VERSION 1u
+#define THERMO_ABI_VERSION 2u
 #define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
 #define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
 #define THERMO_MAX_OBJECTS 1024
@@ -119,6 +119,12 @@ typedef struct {
   uint32_t track_access;          /* 1: also count lane accesses per word (the Fig. 3
                                      baseline; thermo_query_access)       */
   uint64_t expected_pairs;        /* hash sizing hint: distinct (sector,warp) pairs; 0 = auto */
+  uint32_t block_warps;           /* sampled-block mode:
+                                     0 = the whole grid; else warps per thread block, and
+                                     only records of warps in block `block_id`
+                                     (warp / block_warps == block_id) are reduced -- the
+                                     others are treated as never traced              */
+  uint32_t block_id;
 } thermo_config;
 
 /*

@@ -194,6 +194,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       // uniform instruction (upper address bits included), no sector straddle
       const bool odd = act & ((cur.z != z0) | (cur.w != w0) | (((cur.y ^ y0) & 0xFF7FFFFFu) != 0) |
                               ((x & 31u) + size > 32u));
+      if (a.block_warps && z0 / a.block_warps != a.block_id && __ballot_sync(FULL, odd) == 0) {
+        off = offn;  // an instruction of a warp outside the sampled block: never traced
+        continue;
+      }
       if (!ok0 || __ballot_sync(FULL, odd) != 0) {
         if (lane == 0) {  // defer the view to the general kernel
           const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);

@@ -227,6 +227,8 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.deferred = ctx->d_deferred;
   a.seg_cnt = ctx->seg_counted ? ctx->seg.cnt : nullptr;
   a.acc = ctx->d_acc;
+  a.block_warps = ctx->cfg.block_warps;
+  a.block_id = ctx->cfg.block_id;
   launch_decode(a, ctx->num_sms, ctx->stream);
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());

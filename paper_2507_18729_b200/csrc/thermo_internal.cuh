@@ -95,6 +95,7 @@ struct DecodeArgs {
   ull* deferred;          // [n] p << 7 | stats_only << 6 | len of deferred views
   uint32_t* seg_cnt;      // [S_tot] keys per sector (SEGMENT histogram), or null
   uint32_t* acc;          // [8 S_tot] lane accesses per word (track_access), or null
+  uint32_t block_warps, block_id;  // sampled-block mode (0: whole grid)
 };
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------

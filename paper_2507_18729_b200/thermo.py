@@ -36,7 +36,8 @@ class thermo_object(ctypes.Structure):
 
 class thermo_config(ctypes.Structure):
     _fields_ = [("max_launches", u32), ("max_warps_per_launch", u32), ("max_pcs", u32), ("dedup", u32),
-                ("track_pc", u32), ("track_access", u32), ("expected_pairs", u64)]
+                ("track_pc", u32), ("track_access", u32), ("expected_pairs", u64),
+                ("block_warps", u32), ("block_id", u32)]
 
 
 PARAM_FIELDS = ("theta_hot", "alpha_num", "alpha_den", "beta_num", "beta_den", "fs_min", "smem_cap",
@@ -139,11 +140,13 @@ def label_names(bits: int) -> list[str]:
 
 
 def _config(max_launches: int = 1, max_warps_per_launch: int = 1 << 20, max_pcs: int = 4096,
-            dedup: int = DEDUP_AUTO, track_pc: bool = True, track_access: bool = False) -> thermo_config:
+            dedup: int = DEDUP_AUTO, track_pc: bool = True, track_access: bool = False, block_warps: int = 0,
+            block_id: int = 0) -> thermo_config:
     cfg = thermo_config()
     load().thermo_default_config(ctypes.byref(cfg))
     cfg.max_launches, cfg.max_warps_per_launch, cfg.max_pcs = max_launches, max_warps_per_launch, max_pcs
     cfg.dedup, cfg.track_pc, cfg.track_access = dedup, int(bool(track_pc)), int(bool(track_access))
+    cfg.block_warps, cfg.block_id = block_warps, block_id  # sampled-block mode (0: whole grid)
     return cfg
 
 

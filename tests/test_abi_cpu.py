@@ -50,13 +50,13 @@ def test_defaults(lib):
     p = thermo.default_params()
     import oracle
     assert p == oracle.DEFAULT_PARAMS   # same S:347 defaults on both sides
-    assert lib.thermo_abi_version() == 1
+    assert lib.thermo_abi_version() == 2
 
 
 def test_struct_sizes():
     from paper_2507_18729_b200 import thermo
     assert ctypes.sizeof(thermo.thermo_object) == 24
-    assert ctypes.sizeof(thermo.thermo_config) == 32
+    assert ctypes.sizeof(thermo.thermo_config) == 40
     assert ctypes.sizeof(thermo.thermo_params) == 22 * 8
     assert ctypes.sizeof(thermo.thermo_indicators) == 8 + 16 * 8
     assert ctypes.sizeof(thermo.thermo_pc_hist) == 8 + 33 * 8

@@ -276,3 +276,22 @@ def test_access_counts(case):
     orc2 = oracle.run([o[:4] for o in t.objects], calls)
     for k, obj in enumerate(t.objects):
         assert np.array_equal(th.heatmap(obj[3], WORD), orc2.word_counts(k))
+
+
+@pytest.mark.parametrize("block", [0, 5])
+def test_sampled_block_mode(block):
+    """Sampled-block mode: only one thread
+    block's warps are reduced; everything against the oracle's block scope,
+    on a fuzz trace (mixed/invalid records, general path) and on SGEMM."""
+    from paper_2507_18729_b200 import Thermo
+    for t, bw in ((tg.gemm(128, 96, 40, "v00"), 32),
+                  (tg.random_trace(n=30000, seed=13, n_warps=400, n_launches=1), 16)):
+        th = Thermo(max_launches=1, max_warps_per_launch=1 << 22, block_warps=bw, block_id=block)
+        th.register_objects(t.objects)
+        th.ingest(t.records.cuda().contiguous())
+        th.build(BOTH)
+        orc = oracle.Oracle([o[:4] for o in t.objects])
+        orc.block_scope(bw, block)
+        orc.ingest(t.records)
+        orc.build()
+        compare(orc, th, t)
