@@ -79,6 +79,7 @@ def _load():
         L.orc_restrict.argtypes = [vp, vp, vp, sz]
         L.orc_ingest.argtypes = [vp, vp, sz]
         L.orc_block_scope.argtypes = [vp, u32, u32]
+        L.orc_ingest_warp.argtypes = [vp, vp, sz]
         L.orc_build.argtypes = [vp, u32]
         L.orc_word_counts.argtypes = [vp, u32, vp]
         L.orc_sector_counts.argtypes = [vp, u32, vp]
@@ -126,6 +127,12 @@ class Oracle:
         oi = np.ascontiguousarray(obj_idx, dtype=np.uint32)
         se = np.ascontiguousarray(sectors, dtype=np.uint64)
         _load().orc_restrict(self._h, _ptr(oi), _ptr(se), len(oi))
+
+    def ingest_warp(self, records):
+        """Warp-instruction records (272 bytes each; int32 [n, 68]) as one call."""
+        a = np.ascontiguousarray(_as_numpy(records))
+        assert a.nbytes % 272 == 0
+        _load().orc_ingest_warp(self._h, _ptr(a), a.nbytes // 272)
 
     def block_scope(self, warps_per_block: int, block: int):
         """Keep only the records of one sampled block; call before ingest."""

@@ -283,6 +283,41 @@ void orc_restrict(void* h, const uint32_t* obj_idx, const uint64_t* sectors, siz
   for (size_t i = 0; i < n; ++i) o->allow.insert({obj_idx[i], sectors[i]});
 }
 
+// warp-instruction records (include/thermo.h
+// thermo_warp_record): one warp instruction with its 32 lane addresses
+// is, by definition, the per-lane records of its active lanes in lane order,
+// the first carrying instr_start; written out here and ingested as one call.
+void orc_ingest_warp(void* h, const void* recs, size_t n) {
+  const unsigned char* p = static_cast<const unsigned char*>(recs);
+  std::vector<unsigned char> lanes;
+  lanes.reserve(n * 32 * 16);
+  for (size_t i = 0; i < n; ++i) {
+    const unsigned char* r = p + 272 * i;
+    uint32_t warp, site, active, flags;
+    std::memcpy(&warp, r, 4);
+    std::memcpy(&site, r + 4, 4);
+    std::memcpy(&active, r + 8, 4);
+    std::memcpy(&flags, r + 12, 4);
+    bool first = true;
+    for (int l = 0; l < 32; ++l) {
+      if (!((active >> l) & 1u)) continue;
+      uint64_t addr;
+      std::memcpy(&addr, r + 16 + 8 * l, 8);
+      const uint64_t reserved = ((addr >> 48) != 0 || (flags >> 7) != 0) ? 1 : 0;
+      const uint64_t af = (addr & ((uint64_t(1) << 48) - 1)) | (uint64_t(flags & 7) << 48) |
+                          (uint64_t((flags >> 3) & 3) << 51) | (uint64_t((flags >> 5) & 3) << 53) |
+                          (uint64_t(first ? 1 : 0) << 55) | (reserved << 56);
+      first = false;
+      unsigned char q[16];
+      std::memcpy(q, &af, 8);
+      std::memcpy(q + 8, &warp, 4);
+      std::memcpy(q + 12, &site, 4);
+      lanes.insert(lanes.end(), q, q + 16);
+    }
+  }
+  static_cast<Oracle*>(h)->ingest(lanes.data(), lanes.size() / 16);
+}
+
 // sampled-block scope: only block `block` of `warps_per_block` warps
 void orc_block_scope(void* h, uint32_t warps_per_block, uint32_t block) {
   Oracle* o = static_cast<Oracle*>(h);

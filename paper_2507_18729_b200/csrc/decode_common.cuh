@@ -303,6 +303,73 @@ __device__ __forceinline__ void flush_launch_ctr(ull* lc, uint32_t launch, ull& 
   unmapped = mapped = 0;
 }
 
+// ---- window-interval object cache (fast decode kernels) ----
+// one interval of a 4 GiB window: [blo, blo + bn) in 32-bit offsets
+struct WinEnt {
+  uint32_t H;       // window id (space << 16 | addr[32,48)); 0xFFFFFFFF = empty
+  uint32_t blo, bn;
+  uint32_t sbase;   // sector id of the sector at blo (objects)
+  uint32_t tail_s;  // offset of the object's partial last sector, 1 if none
+  uint32_t tail_m;  // its allowed words
+  int oid;          // object index, -1 for a gap
+};
+
+// the interval of window H holding the sector at offset xs (xs % 32 == 0)
+__device__ __forceinline__ WinEnt win_lookup(const ull* s_lo, const ull* s_hi, const ull* s_soff, uint32_t n,
+                                             int steps, uint32_t H, uint32_t xs) {
+  const ull wlo = (ull)H << 32, wend = wlo + (1ull << 32);
+  const ull X = wlo | xs;
+  int i = -1;  // last object with lo <= X
+  {
+    uint32_t lo = 0, hi = n;
+    for (int k = 0; k < steps; ++k) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const bool le = s_lo[mid] <= X;
+      lo = le ? mid : lo;
+      hi = le ? hi : mid;
+    }
+    if (n > 0 && s_lo[lo] <= X) i = (int)lo;
+  }
+  WinEnt e;
+  e.H = H;
+  e.tail_s = 1;
+  e.tail_m = 0xFFu;
+  ull a, b;
+  if (i >= 0 && X < s_hi[i]) {  // a sector of object i
+    const ull olo = s_lo[i], ohi = s_hi[i];
+    const ull ohi32 = (ohi + 31) & ~31ull;
+    a = olo > wlo ? olo : wlo;
+    b = ohi32 < wend ? ohi32 : wend;
+    e.oid = i;
+    e.sbase = (uint32_t)(s_soff[i] + ((a - olo) >> 5));
+    const ull ts = ohi & ~31ull;
+    if ((ohi & 31) && ts >= wlo && ts < wend) {
+      e.tail_s = (uint32_t)(ts - wlo);
+      e.tail_m = (1u << (((uint32_t)(ohi & 31) + 3) >> 2)) - 1u;
+    }
+  } else {  // the gap between objects i and i + 1
+    const ull glo = i >= 0 ? ((s_hi[i] + 31) & ~31ull) : 0ull;
+    const ull ghi = (uint32_t)(i + 1) < n ? s_lo[i + 1] : ~0ull;
+    a = glo > wlo ? glo : wlo;
+    b = ghi < wend ? ghi : wend;
+    e.oid = -1;
+    e.sbase = 0;
+  }
+  e.blo = (uint32_t)(a - wlo);
+  const ull len = b > a ? b - a : 0;
+  e.bn = len > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)len;  // xs - blo <= 0xFFFFFFE0 then always passes
+  return e;
+}
+
+__device__ __forceinline__ bool win_has(const WinEnt& e, uint32_t H, uint32_t xs) {
+  return (e.H == H) & (xs - e.blo < e.bn);
+}
+
+// full key of a lane entry (pc id << 32 | g) -> mask: [g][launch, warp][pc id][mask]
+__device__ __forceinline__ ull entry_key(ull c, uint32_t m, ull tag, uint32_t SH, uint32_t P) {
+  return ((((c & 0xFFFFFFFFull) << SH) | (tag << P) | (c >> 32)) << 8) | m;
+}
+
 size_t decode_smem(const DecodeArgs& a);
 
 }  // namespace thermo

@@ -425,3 +425,61 @@ def test_block_scope(block):
         for s in range(len(sc)):
             want = ref.get((space, (base >> 5) + s), [0] * 9)
             assert sc[s] == want[8]
+
+
+def _expand_warp_records(recs):
+    """Independent Python expansion of warp-instruction records into per-lane
+    records (thermo.h thermo_warp_record): active lanes in order, the first
+    with instr_start; address bits >= 48 or reserved flags make a lane invalid."""
+    a = np.ascontiguousarray(recs.numpy()).view(np.uint32).reshape(-1, 68)
+    out = []
+    for r in a:
+        warp, site, active, flags = int(r[0]), int(r[1]), int(r[2]), int(r[3])
+        first = True
+        for l in range(32):
+            if not (active >> l) & 1:
+                continue
+            addr = int(r[4 + 2 * l]) | (int(r[5 + 2 * l]) << 32)
+            resv = 1 if (addr >> 48) or (flags >> 7) else 0
+            af = (addr & ((1 << 48) - 1)) | ((flags & 7) << 48) | (((flags >> 3) & 3) << 51) | \
+                 (((flags >> 5) & 3) << 53) | ((1 if first else 0) << 55) | (resv << 56)
+            first = False
+            out.append([af & 0xFFFFFFFF, af >> 32, warp, site])
+    return torch.from_numpy(np.array(out, dtype=np.uint64).astype(np.uint32).view(np.int32).reshape(-1, 4))
+
+
+def _same(o1, o2, nobj):
+    for k in range(nobj):
+        assert np.array_equal(o1.word_counts(k), o2.word_counts(k))
+        assert np.array_equal(o1.sector_counts(k), o2.sector_counts(k))
+    assert o1.classify() == o2.classify()
+    assert o1.stats() == o2.stats()
+    p1, p2 = o1.per_pc(), o2.per_pc()
+    assert [(r[0], r[1]) for r in p1] == [(r[0], r[1]) for r in p2]
+    for a, b in zip(p1, p2):
+        assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_warp_records_equal_their_lane_expansion(seed):
+    """Warp-instruction records: by definition the
+    per-lane records of the active lanes; the oracle's ingest_warp against an
+    independent expansion fed to the per-lane oracle."""
+    objects, recs = tg.random_warp_trace(n_instr=1500, seed=seed, n_launches=2)
+    ow = oracle.Oracle([o[:4] for o in objects])
+    ow.ingest_warp(recs)
+    ow.build()
+    ol = oracle.Oracle([o[:4] for o in objects])
+    ol.ingest(_expand_warp_records(recs))
+    ol.build()
+    _same(ow, ol, len(objects))
+
+
+@pytest.mark.parametrize("make", [lambda: tg.tiny("B"), lambda: tg.gemm(64, 64, 16, "v00"), lambda: tg.stencil(64)])
+def test_to_warp_records_roundtrip(make):
+    """Uniform per-lane traces convert to warp records with the same heat map."""
+    t = make()
+    ow = oracle.Oracle(objs(t))
+    ow.ingest_warp(tg.to_warp_records(t.records))
+    ow.build()
+    _same(ow, run(t), len(t.objects))

@@ -96,6 +96,51 @@ def from_instructions(lane_addr, active, warp, pc, kind, log2size, space=0, laun
         col(warp).reshape(-1)[sel], col(pc).reshape(-1)[sel], col(launch).reshape(-1)[sel])
 
 
+def pack_warp_records(lane_addr, active, warp, site, flags) -> torch.Tensor:
+    """Warp-instruction records (include/thermo.h thermo_warp_record, 272 B =
+    int32 [I, 68]): warp, site, active mask, flags, then 32 u64 lane addresses.
+    lane_addr int64 [I, 32]; active bool [I, 32]; warp/site/flags int64 [I]."""
+    I = lane_addr.shape[0]
+    dev = lane_addr.device
+    out = torch.zeros((I, 68), dtype=torch.int32, device=dev)
+    bits = (active.to(torch.int64) << torch.arange(32, device=dev, dtype=torch.int64)).sum(1)
+    out[:, 0] = _u32_to_i32(torch.as_tensor(warp, device=dev).to(torch.int64).expand(I))
+    out[:, 1] = _u32_to_i32(torch.as_tensor(site, device=dev).to(torch.int64).expand(I))
+    out[:, 2] = _u32_to_i32(bits)
+    out[:, 3] = _u32_to_i32(torch.as_tensor(flags, device=dev).to(torch.int64).expand(I))
+    a = lane_addr.to(torch.int64)
+    out[:, 4::2] = _u32_to_i32(a & 0xFFFFFFFF)
+    out[:, 5::2] = _u32_to_i32((a >> 32) & 0xFFFFFFFF)
+    return out
+
+
+def to_warp_records(records: torch.Tensor) -> torch.Tensor:
+    """Per-lane records -> warp-instruction records, one per instruction (its
+    records become lanes 0..len-1).  Every instruction must be <= 32 records
+    with one warp, site, size, kind and space, and no reserved bits."""
+    r = records.to(torch.int64) & 0xFFFFFFFF
+    n = r.shape[0]
+    dev = records.device
+    hi = r[:, 1]
+    head = ((hi >> 23) & 1).bool()
+    head[0] = True
+    iid = torch.cumsum(head.to(torch.int64), 0) - 1
+    hidx = torch.nonzero(head).flatten()
+    pos = torch.arange(n, device=dev) - hidx[iid]
+    assert int(pos.max()) < 32, "instructions longer than 32 records"
+    for c, m in ((2, 0xFFFFFFFF), (3, 0xFFFFFFFF), (1, 0x7F0000)):
+        assert bool(((r[:, c] & m) == (r[hidx, c] & m)[iid]).all()), "non-uniform instruction"
+    assert bool(((hi >> 24) == 0).all()), "reserved bits"
+    I = hidx.shape[0]
+    addr = torch.zeros((I, 32), dtype=torch.int64, device=dev)
+    act = torch.zeros((I, 32), dtype=torch.bool, device=dev)
+    addr[iid, pos] = ((hi & 0xFFFF) << 32) | r[:, 0]
+    act[iid, pos] = True
+    h = hi[hidx]
+    flags = ((h >> 16) & 7) | (((h >> 19) & 3) << 3) | (((h >> 21) & 3) << 5)
+    return pack_warp_records(addr, act, r[hidx, 2], r[hidx, 3], flags)
+
+
 def instr_starts(records: torch.Tensor) -> torch.Tensor:
     """Indices of records whose instr_start bit is set (record 0 always starts)."""
     s = ((records[:, 1].to(torch.int64) >> 23) & 1).to(torch.bool)
@@ -141,11 +186,12 @@ def _lsr(z: torch.Tensor, k: int) -> torch.Tensor:
 
 from .workloads import (  # noqa: E402
     tiny, fig3, fig6, gemm, stencil, spmv, strided_gather, smem_thread_local,
-    smem_warp_broadcast, random_trace, synthetic, WORKLOADS,
+    smem_warp_broadcast, random_trace, synthetic, random_warp_trace, WORKLOADS,
 )
 
 __all__ = [
     "Trace", "pack_records", "from_instructions", "shuffle_instructions", "split_calls",
+    "pack_warp_records", "to_warp_records", "random_warp_trace",
     "instr_starts", "splitmix64", "tiny", "fig3", "fig6", "gemm", "stencil", "spmv",
     "strided_gather", "smem_thread_local", "smem_warp_broadcast", "random_trace",
     "synthetic", "WORKLOADS",

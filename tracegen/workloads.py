@@ -453,6 +453,59 @@ def random_trace(n=20000, seed=1, n_objects=5, n_warps=50, n_launches=3, n_pcs=7
                  meta=dict(warps=n_warps, launches=n_launches))
 
 
+def random_warp_trace(n_instr=3000, seed=1, n_objects=5, n_warps=60, n_launches=2, n_pcs=5, device="cpu",
+                      max_len=3000):
+    """Random warp-instruction records (thermo_warp_record): random active
+    masks (empty and full included), sizes 1-16 B at random offsets (unaligned,
+    straddling), addresses inside, near and outside the objects, some invalid
+    flags / address bits >= 48.  Returns (Trace-like objects, int32 [n, 68])."""
+    from . import pack_warp_records
+    g = torch.Generator().manual_seed(seed)
+
+    def ri(lo, hi, size):
+        return torch.randint(lo, hi, size, generator=g, dtype=torch.int64)
+
+    objects = []
+    bases = {0: 0x100000, 1: 0x2000}
+    for o in range(n_objects):
+        space = 1 if o % 4 == 3 else 0
+        ln = int(ri(1, max_len, (1,)))
+        base = bases[space] + 32 * int(ri(0, 4, (1,)))
+        objects.append((base, ln, space, 200 + o, f"w{o}"))
+        bases[space] = _align(base + ln + 1, 32) + 32 * int(ri(0, 3, (1,)))
+    I = n_instr
+    oi = ri(0, n_objects, (I,))
+    base = torch.tensor([o[0] for o in objects])[oi]
+    ln = torch.tensor([o[1] for o in objects])[oi]
+    space = torch.tensor([o[2] for o in objects])[oi]
+    l2s = ri(0, 5, (I,))
+    kind = ri(0, 3, (I,))
+    mode = ri(0, 4, (I,))   # 0 contiguous, 1 strided, 2 random, 3 broadcast
+    lane = torch.arange(32, dtype=torch.int64)
+    start = (torch.rand(I, generator=g) * (ln + 40).to(torch.float64)).to(torch.int64) - 20
+    stride = ri(1, 300, (I,))
+    rnd = (torch.rand((I, 32), generator=g) * (ln + 64).to(torch.float64)[:, None]).to(torch.int64) - 32
+    off = torch.where((mode == 0)[:, None], start[:, None] + lane[None, :] * (1 << l2s)[:, None],
+          torch.where((mode == 1)[:, None], start[:, None] + lane[None, :] * stride[:, None],
+          torch.where((mode == 2)[:, None], rnd, start[:, None].expand(I, 32))))
+    addr = torch.clamp(base[:, None] + off, min=0)
+    hi_bad = torch.rand((I, 32), generator=g) < 0.002
+    addr = torch.where(hi_bad, addr | (1 << 50), addr)
+    am = torch.rand(I, generator=g)
+    active = torch.rand((I, 32), generator=g) < am[:, None]
+    active[ri(0, I, (I // 20,))] = True
+    active[ri(0, I, (I // 40,))] = False
+    warp = ri(0, n_warps, (I,))
+    launch = ri(0, n_launches, (I,))
+    pc = ri(1, n_pcs + 1, (I,)) * 16
+    flags = l2s | (kind << 3) | (space << 5)
+    bad = torch.rand(I, generator=g) < 0.01
+    flags = torch.where(bad, flags | (1 << 7), flags)
+    flags = torch.where(torch.rand(I, generator=g) < 0.01, (flags & ~7) | 6, flags)  # size code 6: invalid
+    recs = pack_warp_records(addr, active, warp, (pc >> 4) | (launch << 20), flags)
+    return objects, recs.to(device)
+
+
 # --------------------------------------------------------------------------
 # synthetic multi-kernel trace over 64 objects (SURVEY §8d item 5)
 # --------------------------------------------------------------------------
