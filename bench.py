@@ -200,6 +200,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
                     help="multi-GPU: one sharded job (default) or independent replicas")
+    ap.add_argument("--format", default="lane", choices=["lane", "warp"],
+                    help="record format: 16-B per-lane records (default, the contract) or 272-B "
+                         "warp-instruction records (SURVEY §8f item 4)")
     ap.add_argument("--force-dist", action="store_true",
                     help="one GPU through the sharded NCCL path (checks that code path on one GPU)")
     args = ap.parse_args()
@@ -239,9 +242,19 @@ def main():
             parallelism = f"replicas x{ws}"
     th.register_objects(t.objects)
 
+    ingest = th.ingest
+    inputs = t.records
+    if args.format == "warp":  # warp-instruction records of the same trace
+        import tracegen as tg
+        inputs = tg.to_warp_records(t.records)
+        t.records = None
+        torch.cuda.empty_cache()
+        ingest = th.ingest_warp
+    in_bytes = inputs.numel() * 4
+
     def step(recs):
         th.reset()
-        th.ingest(recs)
+        ingest(recs)
         th.build(BOTH)
         return th.classify()
 
@@ -251,7 +264,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(max(3, args.warmup)):
-        step(t.records)
+        step(inputs)
     st0 = th.stats()
     launches0 = st0["kernel_launches"]
     dec_ms, phase = [], {k: [] for k in ("ms_decode", "ms_dedup", "ms_count", "ms_hist", "ms_pc", "ms_indicators")}
@@ -260,7 +273,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            step(t.records)
+            step(inputs)
             s = th.stats()
             for k in phase:
                 phase[k].append(s[k])
@@ -280,8 +293,8 @@ def main():
     # ---- e2e: same step through the C ABI with a pinned HOST trace ----
     e2e = None
     if not args.no_e2e:
-        host = torch.empty_like(t.records, device="cpu").pin_memory()
-        host.copy_(t.records)
+        host = torch.empty_like(inputs, device="cpu").pin_memory()
+        host.copy_(inputs)
         step(host)
         barrier()
         t0 = time.perf_counter()
@@ -291,7 +304,7 @@ def main():
         barrier()
         el = (time.perf_counter() - t0) / k2
         d2h = len(res) * 136
-        e2e = {"value": n * ws / el, "unit": UNIT, "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": d2h,
+        e2e = {"value": n * ws / el, "unit": UNIT, "h2d_bytes_per_step": in_bytes, "d2h_bytes_per_step": d2h,
                "ms_per_step": el * 1e3}
         del host
 
@@ -300,17 +313,18 @@ def main():
     dec = statistics.mean(phase["ms_decode"])
     ph_mean = {k: statistics.mean(v) for k, v in phase.items()}
     dominant = max(ph_mean, key=ph_mean.get)
-    achieved = 16.0 * n / (dec / 1e3) / 1e9
+    achieved = in_bytes / (dec / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload)
+            traffic = json.load(open(tp)).get(args.workload if args.format == "lane" else args.workload + "-warp")
         except Exception:
             traffic = None
-    roof = {"bound": "hbm", "kernel": "decode_kernel (a2+a3)", "achieved": achieved, "peak": peak,
+    roof = {"bound": "hbm", "kernel": "decode_kernel (a2+a3)" if args.format == "lane" else "decode_warp_kernel (a2+a3)",
+            "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-            "algorithmic_bytes_per_launch": 16 * n, "ms_per_launch": dec}
+            "algorithmic_bytes_per_launch": in_bytes, "ms_per_launch": dec}
     pipe = None
     if args.workload in ALGO_BYTES and ws == 1:
         a = ALGO_BYTES[args.workload]
@@ -320,7 +334,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": args.workload, "records": n * ws, "objects": len(t.objects),
+            "config": {"workload": args.workload, "records": n * ws, "format": args.format, "objects": len(t.objects),
                        "dedup": {1: "sort", 2: "hash", 3: "segment"}.get(st["dedup_used"], "?"),
                        "l2": "inputs larger than L2 (16 B x records >> 126 MB), no flush",
                        "records_per_gpu": n, "parallelism": parallelism},

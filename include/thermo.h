@@ -68,6 +68,24 @@ typedef struct {
 } thermo_record;
 
 /*
+ * Warp-instruction record (the
+ * collector's native unit, one warp instruction with its 32 lane addresses).
+ * By definition it stands for the per-lane thermo_records of its active lanes
+ * in lane order, the first one carrying instr_start, each with
+ *   addr_flags = addr[0,48) | log2size | kind | space | instr_start | reserved,
+ * where reserved != 0 (an invalid record) iff addr has bits >= 48 set or
+ * flags has bits >= 7 set.  272 bytes, 16-byte aligned.  Full warps take
+ * 8.5 B per lane instead of 16.
+ */
+typedef struct {
+  uint32_t warp;       /* global warp id within its launch                          */
+  uint32_t site;       /* [0,20) pc >> 4 | [20,32) launch id                        */
+  uint32_t active;     /* bit l: lane l executed the access                         */
+  uint32_t flags;      /* [0,3) log2(size) | [3,5) kind | [5,7) space | [7,32) 0    */
+  uint64_t addr[32];   /* byte address of lane l (inactive lanes: ignored)          */
+} thermo_warp_record;
+
+/*
  * A registered data object ("memory registration"; P:329 region
  * config).  base must be 32-byte aligned (G9), len > 0, base + len <= 2^48, and
  * objects of one space must not overlap.  id is the caller's handle
@@ -307,6 +325,18 @@ thermo_status thermo_query_heatmap(thermo_ctx *ctx, uint32_t object_id, thermo_g
 /* Level histogram (THERMO_LEVELS bins, HOST buffer) of one object over all its
  * n_words words (THERMO_WORD) or n_sectors sectors (THERMO_SECTOR); level-0
  * counts untouched ones.  Errors: EINVAL, ESTATE. */
+/*
+ * Ingest n warp-instruction records (device or host pointer; host records are
+ * copied once).  Same result as thermo_ingest_trace on the per-lane records
+ * they stand for; each record is one instruction (G24).  Instructions the fast
+ * path does not take (invalid header, lanes in different 4 GiB windows,
+ * straddling accesses) are reduced through their per-lane records.  Device
+ * memory: up to 32 n per-lane records of spill space.  stats.records counts
+ * lane records.  Errors: EINVAL (NULL, misaligned, n >= 2^27), ESTATE, ENOMEM,
+ * ECUDA.
+ */
+thermo_status thermo_ingest_warp_trace(thermo_ctx *ctx, const thermo_warp_record *recs, size_t n);
+
 /*
  * Access counts (Fig. 3: equal access counts,
  * different temperatures): out[w] = number of (record, word) pairs touching

@@ -106,6 +106,9 @@ struct thermo_ctx {
   bool hist_valid = false;
   bool seg_counted = false;  // the decoder counts keys per sector (SEGMENT histogram, one rank)
   uint32_t* d_acc = nullptr;  // [8 S_tot] lane accesses per word (track_access)
+  uint4* d_spill = nullptr;   // per-lane records of spilled warp instructions
+  size_t spill_cap = 0;
+  ull* d_wctr = nullptr;      // [2] spilled records, lane records seen
 
   // sharded mode (row e, shard.cu); comm == nullptr: one rank
   Comm* comm = nullptr;
@@ -192,6 +195,8 @@ thermo_status grow_keys(thermo_ctx* ctx, ull** buf, size_t* cap, ull need, ull k
   return THERMO_OK;
 }
 
+DecodeArgs decode_args(thermo_ctx* ctx);
+
 // decode one device-resident call (records[0] starts an instruction)
 thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   if (n == 0) return THERMO_OK;
@@ -209,11 +214,22 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   }
   CK(cudaMemsetAsync(&ctx->d_ctr->n_deferred, 0, sizeof(ull), ctx->stream));
   launch_find_heads(recs, n, kRangeLen, (uint32_t)n_ranges, ctx->d_heads, ctx->stream);
-  DecodeArgs a{};
+  DecodeArgs a = decode_args(ctx);
   a.recs = recs;
   a.n = n;
   a.heads = ctx->d_heads;
   a.n_ranges = (uint32_t)n_ranges;
+  launch_decode(a, ctx->num_sms, ctx->stream);
+  launch_decode_general(a, ctx->num_sms, ctx->stream);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evp[7], ctx->stream));
+  ctx->launches += 3;
+  return THERMO_OK;
+}
+
+// the parts of the decode arguments that do not depend on the records
+DecodeArgs decode_args(thermo_ctx* ctx) {
+  DecodeArgs a{};
   a.obj = obj_table(ctx);
   a.kl = ctx->kl;
   a.max_launches = ctx->cfg.max_launches;
@@ -229,12 +245,7 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.acc = ctx->d_acc;
   a.block_warps = ctx->cfg.block_warps;
   a.block_id = ctx->cfg.block_id;
-  launch_decode(a, ctx->num_sms, ctx->stream);
-  launch_decode_general(a, ctx->num_sms, ctx->stream);
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->evp[7], ctx->stream));
-  ctx->launches += 3;
-  return THERMO_OK;
+  return a;
 }
 
 thermo_status sync_counts(thermo_ctx* ctx) {
@@ -482,7 +493,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
-                  ctx->d_launch_g, ctx->d_acc};
+                  ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr};
   for (void* b : bufs) dfree(b);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_pinned[i]) cudaFreeHost(ctx->h_pinned[i]);
@@ -720,6 +731,68 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
   if (on_device) cudaEventElapsedTime(&ctx->ms_phase[0], ctx->evp[6], ctx->evp[7]);
   else ctx->ms_phase[0] = ctx->ms_ingest;
   ctx->records += n;
+  ctx->state = 2;
+  ctx->hist_valid = false;
+  ctx->have_glob = false;
+  return THERMO_OK;
+}
+
+thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record* recs, size_t n) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state < 1) return fail(ctx, THERMO_ESTATE, "register objects first");
+  if (n == 0) return THERMO_OK;
+  if (!recs) return fail(ctx, THERMO_EINVAL, "recs is NULL");
+  if (reinterpret_cast<uintptr_t>(recs) & 15) return fail(ctx, THERMO_EINVAL, "recs must be 16-byte aligned");
+  if (n >= (1ull << 27)) return fail(ctx, THERMO_EINVAL, "a warp-record ingest call holds < 2^27 instructions");
+  cudaPointerAttributes attr;
+  bool on_device = false;
+  if (cudaPointerGetAttributes(&attr, recs) == cudaSuccess) {
+    on_device = attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+  } else {
+    cudaGetLastError();
+  }
+  cudaStream_t s = ctx->stream;
+  const uint4* drec = reinterpret_cast<const uint4*>(recs);
+  uint4* tmp = nullptr;
+  if (!on_device) {  // host records: one device copy (convenience; the measured path is device-resident)
+    CK(dalloc(&tmp, n * 17));
+    CK(cudaMemcpyAsync(tmp, recs, n * 272, cudaMemcpyHostToDevice, s));
+    drec = tmp;
+  }
+  const ull lanes_max = 32 * (ull)n;
+  st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * lanes_max + 64, ctx->n_keys);
+  if (st) { dfree(tmp); return st; }
+  if (ctx->spill_cap < lanes_max) {  // worst case: every instruction spills
+    dfree(ctx->d_spill);
+    ctx->d_spill = nullptr;
+    ctx->spill_cap = 0;
+    if (dalloc(&ctx->d_spill, lanes_max) != cudaSuccess) { dfree(tmp); return fail(ctx, THERMO_ENOMEM, "spill"); }
+    ctx->spill_cap = lanes_max;
+  }
+  if (!ctx->d_wctr) CK(dalloc(&ctx->d_wctr, 2));
+  CK(cudaEventRecord(ctx->ev0, s));
+  CK(cudaEventRecord(ctx->evp[6], s));
+  CK(cudaMemsetAsync(ctx->d_wctr, 0, 2 * sizeof(ull), s));
+  DecodeArgs a = decode_args(ctx);
+  launch_decode_warp(a, drec, n, ctx->d_spill, ctx->d_wctr, ctx->num_sms, s);
+  ctx->launches += 1;
+  CK(cudaGetLastError());
+  ull wc[2];
+  CK(cudaMemcpyAsync(wc, ctx->d_wctr, sizeof wc, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  dfree(tmp);
+  if (wc[0]) {  // spilled instructions: their per-lane records through the per-lane kernels
+    st = decode_device(ctx, ctx->d_spill, wc[0]);
+    if (st) return st;
+  }
+  CK(cudaEventRecord(ctx->evp[7], s));
+  CK(cudaEventRecord(ctx->ev1, s));
+  st = sync_counts(ctx);
+  if (st) return st;
+  cudaEventElapsedTime(&ctx->ms_ingest, ctx->ev0, ctx->ev1);
+  cudaEventElapsedTime(&ctx->ms_phase[0], ctx->evp[6], ctx->evp[7]);
+  ctx->records += wc[1];
   ctx->state = 2;
   ctx->hist_valid = false;
   ctx->have_glob = false;

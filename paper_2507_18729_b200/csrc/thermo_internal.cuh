@@ -103,6 +103,10 @@ void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_range
                        cudaStream_t s);
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
 void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s);
+// warp-instruction records (decode_warp.cu); spill_ctr[0] = spilled per-lane
+// records written to spill, spill_ctr[1] += lane records seen
+void launch_decode_warp(const DecodeArgs& a, const uint4* wrec, ull n_instr, uint4* spill, ull* spill_ctr,
+                        int num_sms, cudaStream_t s);
 
 // onesweep LSD radix sort of u64 keys on bits [lo_bit, lo_bit + nbits)
 struct SortWorkspace {

@@ -78,7 +78,8 @@ EXPORTS = ("thermo_default_config", "thermo_default_params", "thermo_abi_version
            "thermo_create_dist", "thermo_nccl_unique_id", "thermo_destroy", "thermo_reset",
            "thermo_register_objects", "thermo_ingest_trace", "thermo_build_heatmap", "thermo_query_heatmap",
            "thermo_query_histogram", "thermo_query_per_pc", "thermo_classify", "thermo_get_stats",
-           "thermo_last_error", "thermo_create_local_shards", "thermo_sharding", "thermo_query_access")
+           "thermo_last_error", "thermo_create_local_shards", "thermo_sharding", "thermo_query_access",
+           "thermo_ingest_warp_trace")
 
 _lib = None
 
@@ -106,6 +107,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.thermo_reset.argtypes = [vp]
     L.thermo_register_objects.argtypes = [vp, P(thermo_object), sz]
     L.thermo_ingest_trace.argtypes = [vp, vp, sz]
+    L.thermo_ingest_warp_trace.argtypes = [vp, vp, sz]
     L.thermo_build_heatmap.argtypes = [vp, ctypes.c_int, u32]
     L.thermo_query_heatmap.argtypes = [vp, u32, ctypes.c_int, vp, sz, P(sz)]
     L.thermo_query_histogram.argtypes = [vp, u32, ctypes.c_int, vp]
@@ -248,6 +250,11 @@ class Thermo:
             ptr, n = a.ctypes.data, a.nbytes // 16
             self._keep = a
         self._ck(self.L.thermo_ingest_trace(self.h, vp(ptr), n))
+
+    def ingest_warp(self, records):
+        """Warp-instruction records: torch int32 [n, 68] (272-byte thermo_warp_record), device or host."""
+        assert records.is_contiguous() and records.shape[-1] == 68 and records.dtype.itemsize == 4
+        self._ck(self.L.thermo_ingest_warp_trace(self.h, vp(records.data_ptr()), records.shape[0]))
 
     def ingest_ptr(self, ptr: int, n: int):
         self._ck(self.L.thermo_ingest_trace(self.h, vp(ptr), n))

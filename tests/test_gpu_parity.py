@@ -295,3 +295,41 @@ def test_sampled_block_mode(block):
         orc.ingest(t.records)
         orc.build()
         compare(orc, th, t)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("dedup", [0, 1, 2])
+def test_warp_records_random(seed, dedup):
+    """Warp-instruction records through
+    thermo_ingest_warp_trace against the oracle's ingest_warp: random active
+    masks, unaligned/straddling sizes, lanes outside objects, invalid flags and
+    address bits >= 48 (spilled to the per-lane kernels), 2 launches."""
+    from paper_2507_18729_b200 import Thermo
+    objects, recs = tg.random_warp_trace(n_instr=4000 + 300 * seed, seed=seed, n_launches=2, max_len=20000)
+    t = tg.Trace("warp-random", objects, recs, meta=dict(launches=2))
+    th = Thermo(max_launches=2, max_warps_per_launch=1 << 22, dedup=dedup, track_access=True)
+    th.register_objects(objects)
+    half = recs.shape[0] // 2
+    th.ingest_warp(recs[:half].cuda().contiguous())
+    th.ingest_warp(recs[half:].contiguous())  # host pointer
+    th.build(BOTH)
+    orc = oracle.Oracle([o[:4] for o in objects])
+    orc.ingest_warp(recs[:half])
+    orc.ingest_warp(recs[half:])
+    orc.build()
+    compare(orc, th, t)
+    for k, o in enumerate(objects):
+        assert np.array_equal(th.access(o[3]), orc.access_counts(k))
+
+
+@pytest.mark.parametrize("make", [lambda: tg.tiny("B"), lambda: tg.gemm(128, 96, 40, "v00"), lambda: tg.stencil(96),
+                                  lambda: tg.spmv(10, 8)])
+def test_warp_records_workloads(make):
+    t = make()
+    w = tg.to_warp_records(t.records)
+    from paper_2507_18729_b200 import Thermo
+    th = gpu_ctx(t)
+    th.ingest_warp(w.cuda())
+    th.build(BOTH)
+    orc = oracle.run([o[:4] for o in t.objects], [t.records])
+    compare(orc, th, t)
