@@ -84,6 +84,8 @@ def _load():
         L.orc_word_counts.argtypes = [vp, u32, vp]
         L.orc_sector_counts.argtypes = [vp, u32, vp]
         L.orc_access_counts.argtypes = [vp, u32, vp]
+        L.orc_runs.restype = sz
+        L.orc_runs.argtypes = [vp, u32, vp, vp, vp, sz]
         L.orc_sample.argtypes = [vp, vp, vp, sz, vp]
         L.orc_hist.argtypes = [vp, u32, ctypes.c_int, vp]
         L.orc_n_pcs.restype = sz
@@ -168,6 +170,16 @@ class Oracle:
         out = np.zeros(self.n_words(o), dtype=np.uint32)
         _load().orc_access_counts(self._h, o, _ptr(out))
         return out
+
+    def runs(self, o):
+        """Run-compressed rows of object index o: (start [R], count [R], temps [R, 9])."""
+        L = _load()
+        n = L.orc_runs(self._h, o, None, None, None, 0)
+        st = np.zeros(n, dtype=np.uint64)
+        ct = np.zeros(n, dtype=np.uint64)
+        tp = np.zeros((n, 9), dtype=np.uint32)
+        L.orc_runs(self._h, o, _ptr(st), _ptr(ct), _ptr(tp), n)
+        return st, ct, tp
 
     def sample(self, obj_idx, sectors) -> np.ndarray:
         oi = np.ascontiguousarray(obj_idx, dtype=np.uint32)

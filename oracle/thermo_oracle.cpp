@@ -351,6 +351,37 @@ void orc_access_counts(void* h, uint32_t o, uint32_t* out) {
   }
 }
 
+// run compression of object `o`'s rows (Fig. 4 caption:
+// "consecutive memory regions with identical temperatures are compressed, and
+// the number of occurrences is indicated"): maximal runs of
+// consecutive sectors whose 9-tuples (8 word temperatures, words past the
+// object's end as 0, then the sector's) are identical, untouched sectors
+// included.  Writes up to cap runs (start sector, count, 9 temps); returns
+// the number of runs.
+size_t orc_runs(void* h, uint32_t o, uint64_t* start, uint64_t* count, uint32_t* temps, size_t cap) {
+  Oracle* p = static_cast<Oracle*>(h);
+  const uint64_t ns = p->sector_count[o].size(), nw = p->word_count[o].size();
+  size_t n = 0;
+  uint32_t prev[9] = {0};
+  for (uint64_t s = 0; s < ns; ++s) {
+    uint32_t t[9];
+    for (int b = 0; b < 8; ++b) t[b] = 8 * s + b < nw ? p->word_count[o][8 * s + b] : 0;
+    t[8] = p->sector_count[o][s];
+    if (s > 0 && std::equal(t, t + 9, prev)) {
+      if (n - 1 < cap) count[n - 1] += 1;
+    } else {
+      if (n < cap) {
+        start[n] = s;
+        count[n] = 1;
+        std::copy(t, t + 9, temps + 9 * n);
+      }
+      ++n;
+    }
+    std::copy(t, t + 9, prev);
+  }
+  return n;
+}
+
 // counts of selected (object index, local sector) pairs: out[9*i .. 9*i+8] =
 // 8 word counts then the sector count (words past n_words read as 0)
 void orc_sample(void* h, const uint32_t* obj_idx, const uint64_t* sectors, size_t n, uint32_t* out) {

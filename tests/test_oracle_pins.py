@@ -483,3 +483,28 @@ def test_to_warp_records_roundtrip(make):
     ow.ingest_warp(tg.to_warp_records(t.records))
     ow.build()
     _same(ow, run(t), len(t.objects))
+
+
+def test_runs_closed_forms_and_round_trip():
+    """Run compression (Fig. 4): gemm_v00's A is
+    one run of identical hot sectors, Fig. 3(b) one row; expanding the runs of
+    random traces gives back the dense rows exactly; runs are maximal."""
+    t = tg.gemm(64, 64, 16, "v00")
+    o = run(t)
+    st, ct, tp = o.runs(0)                       # A: every sector 64 warps (N = 64)
+    assert len(st) == 1 and ct[0] == o.n_sectors(0) and (tp[0] == 64).all()
+    st, ct, tp = run(tg.fig3("b")).runs(0)     # the shared sector, then the untouched rest
+    assert list(tp[0]) == [1] * 8 + [8] and ct[0] == 1 and (len(st) == 1 or not tp[1:].any())
+    for seed in (1, 2):
+        r = tg.random_trace(n=5000, seed=seed)
+        o = run(r)
+        for k in range(len(r.objects)):
+            st, ct, tp = o.runs(k)
+            rows = np.repeat(tp, ct.astype(np.int64), axis=0)
+            wc = o.word_counts(k)
+            dense = np.zeros((o.n_sectors(k), 9), dtype=np.uint32)
+            dense[:, :8].flat[:len(wc)] = wc
+            dense[:, 8] = o.sector_counts(k)
+            assert np.array_equal(rows, dense)
+            assert (st == np.concatenate([[0], np.cumsum(ct)[:-1]])).all()
+            assert all((tp[i] != tp[i + 1]).any() for i in range(len(tp) - 1))  # maximal
