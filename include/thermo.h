@@ -326,6 +326,30 @@ thermo_status thermo_query_heatmap(thermo_ctx *ctx, uint32_t object_id, thermo_g
  * n_words words (THERMO_WORD) or n_sectors sectors (THERMO_SECTOR); level-0
  * counts untouched ones.  Errors: EINVAL, ESTATE. */
 /*
+ * One run of the run-compressed heat map (Fig. 4 caption:
+ * "consecutive memory regions with identical temperatures are compressed, and
+ * the number of occurrences is indicated"): `count` consecutive sectors from
+ * object-local sector `start` whose rows are all temp[0..7] (word
+ * temperatures, words past the object's end 0) and temp[8] (sector).
+ */
+typedef struct {
+  uint64_t start;
+  uint64_t count;
+  uint32_t temp[9];
+  uint32_t reserved;
+} thermo_run;
+
+/*
+ * Run-compressed rows of object `object_id` after a build: maximal runs of
+ * consecutive sectors with identical rows, untouched sectors included, in
+ * sector order; expanding them gives thermo_query_heatmap(BOTH) exactly.  out
+ * NULL or cap too small: *n_out = number of runs and ERANGE (out non-NULL).
+ * Not available in the sharded mode (rows are partitioned; assemble them).
+ * Errors: ESTATE, EINVAL, ERANGE, ECUDA.
+ */
+thermo_status thermo_query_runs(thermo_ctx *ctx, uint32_t object_id, thermo_run *out, size_t cap, size_t *n_out);
+
+/*
  * Ingest n warp-instruction records (device or host pointer; host records are
  * copied once).  Same result as thermo_ingest_trace on the per-lane records
  * they stand for; each record is one instruction (G24).  Instructions the fast

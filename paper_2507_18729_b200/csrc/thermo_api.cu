@@ -1032,6 +1032,33 @@ thermo_status thermo_query_access(thermo_ctx* ctx, uint32_t object_id, uint32_t*
   return THERMO_OK;
 }
 
+thermo_status thermo_query_runs(thermo_ctx* ctx, uint32_t object_id, thermo_run* out, size_t cap, size_t* n_out) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
+  if (ctx->comm) return fail(ctx, THERMO_ESTATE, "sharded mode: rows are partitioned across ranks");
+  auto it = ctx->id_to_reg.find(object_id);
+  if (it == ctx->id_to_reg.end()) return fail(ctx, THERMO_EINVAL, "unknown object id");
+  const uint32_t j = ctx->reg_to_sorted[it->second];
+  const ull ns = ctx->h_soff[j + 1] - ctx->h_soff[j], so = ctx->h_soff[j], nw = ctx->h_nwords[j];
+  uint32_t* scratch = nullptr;
+  CK(dalloc(&scratch, (ns + 2047) / 2048 + 1));
+  ull n = 0;
+  cudaError_t e = compress_runs(ctx->d_wc, ctx->d_sc, so, ns, nw, scratch, ctx->d_tmp, nullptr, 0, &n, ctx->stream);
+  if (e) { dfree(scratch); return fail(ctx, THERMO_ECUDA, std::string("runs: ") + cudaGetErrorString(e)); }
+  if (n_out) *n_out = n;
+  if (!out || cap < n) { dfree(scratch); return fail(ctx, THERMO_ERANGE, "output capacity too small"); }
+  thermo_run* d_out = nullptr;
+  if (dalloc(&d_out, n) != cudaSuccess) { dfree(scratch); return fail(ctx, THERMO_ENOMEM, "runs"); }
+  e = compress_runs(ctx->d_wc, ctx->d_sc, so, ns, nw, scratch, ctx->d_tmp, d_out, n, &n, ctx->stream);
+  if (!e) e = cudaMemcpyAsync(out, d_out, n * sizeof(thermo_run), cudaMemcpyDeviceToHost, ctx->stream);
+  if (!e) e = cudaStreamSynchronize(ctx->stream);
+  dfree(scratch);
+  dfree(d_out);
+  if (e) return fail(ctx, THERMO_ECUDA, std::string("runs: ") + cudaGetErrorString(e));
+  return THERMO_OK;
+}
+
 thermo_status thermo_query_histogram(thermo_ctx* ctx, uint32_t object_id, thermo_granularity g,
                                      uint64_t hist[THERMO_LEVELS]) {
   thermo_status st = pre(ctx);

@@ -197,6 +197,11 @@ enum IndField {
   F_PAD1, F_PAD2, F_PAD3
 };
 void launch_indicators(const IndicatorArgs& a, int num_sms, cudaStream_t s);
+
+// run compression of one object's rows (export.cu): sectors [g0, g0 + ns) of the
+// dense arrays, nw words; scratch: ceil(ns / 2048) u32; out NULL = count only
+cudaError_t compress_runs(const uint32_t* wc, const uint32_t* sc, ull g0, ull ns, ull nw, uint32_t* scratch,
+                          ull* d_total, thermo_run* out, ull out_cap, ull* n_runs, cudaStream_t s);
 // the same in steps, for the sharded mode (partial sums combined in between):
 // tiles (mode 0: sums + votes, 1: verify), stitch, finalize
 void launch_indicator_tiles(const IndicatorArgs& a, int mode, cudaStream_t s);

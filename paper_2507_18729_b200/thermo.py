@@ -79,7 +79,7 @@ EXPORTS = ("thermo_default_config", "thermo_default_params", "thermo_abi_version
            "thermo_register_objects", "thermo_ingest_trace", "thermo_build_heatmap", "thermo_query_heatmap",
            "thermo_query_histogram", "thermo_query_per_pc", "thermo_classify", "thermo_get_stats",
            "thermo_last_error", "thermo_create_local_shards", "thermo_sharding", "thermo_query_access",
-           "thermo_ingest_warp_trace")
+           "thermo_ingest_warp_trace", "thermo_query_runs")
 
 _lib = None
 
@@ -112,6 +112,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.thermo_query_heatmap.argtypes = [vp, u32, ctypes.c_int, vp, sz, P(sz)]
     L.thermo_query_histogram.argtypes = [vp, u32, ctypes.c_int, vp]
     L.thermo_query_access.argtypes = [vp, u32, vp, sz, P(sz)]
+    L.thermo_query_runs.argtypes = [vp, u32, vp, sz, P(sz)]
     L.thermo_query_per_pc.argtypes = [vp, ctypes.c_int, P(thermo_pc_hist), sz, P(sz)]
     L.thermo_classify.argtypes = [vp, P(thermo_params), P(thermo_indicators), sz, P(sz)]
     L.thermo_get_stats.argtypes = [vp, P(thermo_stats)]
@@ -277,6 +278,17 @@ class Thermo:
         out = np.zeros(n.value, dtype=np.uint32)
         self._ck(self.L.thermo_query_access(self.h, object_id, out.ctypes.data, n.value, ctypes.byref(n)))
         return out
+
+    def runs(self, object_id: int):
+        """Run-compressed rows (thermo_query_runs): (start [R], count [R], temps [R, 9])."""
+        n = sz()
+        self.L.thermo_query_runs(self.h, object_id, None, 0, ctypes.byref(n))
+        raw = np.zeros((max(1, n.value), 14), dtype=np.uint32)  # 56-byte thermo_run
+        self._ck(self.L.thermo_query_runs(self.h, object_id, raw.ctypes.data, n.value, ctypes.byref(n)))
+        raw = raw[:n.value]
+        start = raw[:, 0].astype(np.uint64) | (raw[:, 1].astype(np.uint64) << np.uint64(32))
+        count = raw[:, 2].astype(np.uint64) | (raw[:, 3].astype(np.uint64) << np.uint64(32))
+        return start, count, raw[:, 4:13].copy()
 
     def histogram(self, object_id: int, granularity: int) -> np.ndarray:
         out = np.zeros(LEVELS, dtype=np.uint64)

@@ -333,3 +333,15 @@ def test_warp_records_workloads(make):
     th.build(BOTH)
     orc = oracle.run([o[:4] for o in t.objects], [t.records])
     compare(orc, th, t)
+
+
+@pytest.mark.parametrize("i", [0, 1, 4, 6, 7, 8, 9])
+def test_run_compression(i):
+    """Run-compressed rows (Fig. 4) through
+    thermo_query_runs against the oracle's runs."""
+    t = SMALL[i]()
+    orc, th = run_both(t)
+    for k, obj in enumerate(t.objects):
+        a, b = th.runs(obj[3]), orc.runs(k)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y), (t.name, obj[4])
