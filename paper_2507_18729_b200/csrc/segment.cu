@@ -137,9 +137,9 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 // atomics' latency (contended cursors of hot sectors), not bandwidth, bounds it
 constexpr int kScatterPer = 8;
 __global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
-                                                          ull* __restrict__ cur, ull* __restrict__ out,
-                                                          const uint32_t* __restrict__ cnt, ull* __restrict__ big,
-                                                          ull* __restrict__ nbig_ctr) {
+                                                          const ull* __restrict__ off, ull* __restrict__ cur,
+                                                          ull* __restrict__ out, const uint32_t* __restrict__ cnt,
+                                                          ull* __restrict__ big, ull* __restrict__ nbig_ctr) {
   const int lane = threadIdx.x & 31;
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
@@ -154,7 +154,9 @@ __global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict_
     for (int u = 0; u < kScatterPer; ++u) {
       const bool in = i0 + (ull)u * blockDim.x < n;
       isbig[u] = in && cnt[key_g(k[u], kl)] >= (uint32_t)kSegCap;
-      if (in && !isbig[u]) pos[u] = atomicAdd(&cur[key_g(k[u], kl)], 1ull);
+      // the key's chunk = where its sector's segment starts; chunk cursors stay
+      // cache-resident however many sectors there are
+      if (in && !isbig[u]) pos[u] = atomicAdd(&cur[off[key_g(k[u], kl)] / (ull)kSegCap], 1ull);
     }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
@@ -182,6 +184,13 @@ __device__ __forceinline__ ull first_sector_at(const ull* off, ull nsec, ull pos
   }
   return lo;
 }
+
+// chunk cursors: chunk c's keys start where its first sector's segment does
+__global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, ull nchunks, ull* __restrict__ cur) {
+  const ull c = (ull)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nchunks) cur[c] = off[first_sector_at(off, nsec, c * kSegCap)];
+}
+
 
 // stable LSD radix sort of R * kSegThreads u64 keys in shared memory on bits
 // [lo, lo + bits) (warp w ranks keys [w R 32, (w + 1) R 32)); returns the
@@ -459,7 +468,9 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
                           DevCounters* ctr, int num_sms, cudaStream_t s) {
   if (n) {
     const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
-    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.cur, out, ws.cnt, big,
+    const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
+    seg_chunk_cursor_kernel<<<(unsigned)((nch + 255) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur);
+    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.off, ws.cur, out, ws.cnt, big,
                                             reinterpret_cast<ull*>(ws.maxc) + 2);
   }
   const size_t smem = segment_chunk_smem();
