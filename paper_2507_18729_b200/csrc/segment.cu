@@ -186,9 +186,15 @@ __device__ __forceinline__ ull first_sector_at(const ull* off, ull nsec, ull pos
 }
 
 // chunk cursors: chunk c's keys start where its first sector's segment does
-__global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, ull nchunks, ull* __restrict__ cur) {
+// (and each chunk's first sector, so the chunk kernel needs no search)
+__global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, ull nchunks, ull* __restrict__ cur,
+                                        ull* __restrict__ cs0) {
   const ull c = (ull)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < nchunks) cur[c] = off[first_sector_at(off, nsec, c * kSegCap)];
+  if (c <= nchunks) {
+    const ull s = first_sector_at(off, nsec, c * kSegCap);
+    cs0[c] = s;
+    if (c < nchunks) cur[c] = off[s];
+  }
 }
 
 
@@ -274,7 +280,8 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
                                                                ull nsec, KeyLayout kl, uint32_t filter,
                                                                uint32_t* __restrict__ wc, uint32_t* __restrict__ sc,
                                                                const uint32_t* __restrict__ site_of,
-                                                               ull* __restrict__ pc_hist, DevCounters* ctr) {
+                                                               ull* __restrict__ pc_hist, DevCounters* ctr,
+                                                               const ull* __restrict__ cs0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ull* buf0 = reinterpret_cast<ull*>(smem_raw);                      // [kSegBuf]
   ull* buf1 = buf0 + kSegBuf;                                        // [kSegBuf]
@@ -284,8 +291,8 @@ __global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __res
   const int lane = threadIdx.x & 31;
   const ull c = blockIdx.x;
   if (threadIdx.x == 0) {
-    s_range[0] = first_sector_at(off, nsec, c * kSegCap);
-    s_range[1] = first_sector_at(off, nsec, (c + 1) * kSegCap);
+    s_range[0] = cs0[c];
+    s_range[1] = cs0[c + 1];
   }
   __syncthreads();
   const ull s0 = s_range[0], s1 = s_range[1];
@@ -422,12 +429,13 @@ ull segment_chunk_cap() { return kSegCap; }
 cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
   cudaError_t e;
   if (ws.cap_sec < nsec + 1) {
-    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum);
-    ws.cnt = nullptr; ws.off = ws.cur = ws.bsum = nullptr;
+    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum); cudaFree(ws.cs0);
+    ws.cnt = nullptr; ws.off = ws.cur = ws.bsum = ws.cs0 = nullptr;
     ws.cap_sec = 0;
     if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
     if ((e = cudaMalloc(&ws.off, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cs0, (nsec + 2) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
     ws.cap_sec = nsec + 1;
   }
@@ -469,7 +477,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   if (n) {
     const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
     const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
-    seg_chunk_cursor_kernel<<<(unsigned)((nch + 255) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur);
+    seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
     seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.off, ws.cur, out, ws.cnt, big,
                                             reinterpret_cast<ull*>(ws.maxc) + 2);
   }
@@ -482,7 +490,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   const ull chunks = (n + kSegCap - 1) / kSegCap;
   if (chunks)
     seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
-                                                                  pc_hist, ctr);
+                                                                  pc_hist, ctr, ws.cs0);
   ws.launches += 2;
   return cudaGetLastError();
 }

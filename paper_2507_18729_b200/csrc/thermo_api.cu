@@ -491,7 +491,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
                   ctx->d_table, ctx->d_pctable, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
-                  ctx->seg.bsum, ctx->seg.maxc, ctx->d_stage[0],
+                  ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
                   ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr};
   for (void* b : bufs) dfree(b);

@@ -126,7 +126,8 @@ ull* radix_sort_keys(ull* keys, ull n, int lo_bit, int nbits, SortWorkspace& ws,
 struct SegWorkspace {
   uint32_t* cnt = nullptr;   // [S_tot + 1] keys per sector
   ull* off = nullptr;        // [S_tot + 1] exclusive prefix (off[S_tot] = total)
-  ull* cur = nullptr;        // [S_tot + 1] scatter cursors
+  ull* cur = nullptr;        // [S_tot + 1] scatter cursors (one per chunk)
+  ull* cs0 = nullptr;        // [S_tot + 2] first sector of each chunk (+ end)
   ull* bsum = nullptr;       // scan block sums
   uint32_t* maxc = nullptr;  // [4 u64]: max keys in one sector, big-sector keys, big cursor
   ull cap_sec = 0;
