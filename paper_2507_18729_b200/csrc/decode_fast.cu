@@ -40,7 +40,9 @@ __device__ __forceinline__ void ring_issue(uint32_t ring_lane, const uint4* src_
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int MINB>
+// FEAT: compile-time features (1: access counts, 2: sampled-block filter), so
+// the common configuration carries none of their per-view tests
+template <int MINB, int FEAT>
 __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem sm = smem_setup(smem, a);
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       // uniform instruction (upper address bits included), no sector straddle
       const bool odd = act & ((cur.z != z0) | (cur.w != w0) | (((cur.y ^ y0) & 0xFF7FFFFFu) != 0) |
                               ((x & 31u) + size > 32u));
-      if (a.block_warps && z0 / a.block_warps != a.block_id && __ballot_sync(FULL, odd) == 0) {
+      if ((FEAT & 2) && z0 / a.block_warps != a.block_id && __ballot_sync(FULL, odd) == 0) {
         off = offn;  // an instruction of a warp outside the sampled block: never traced
         continue;
       }
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       bool has = fa != 0;
       uint32_t mk = fa;
       const uint32_t g = sbase + ((xs - blo) >> 5);
-      if (a.acc) {  // access counts: every lane's every mapped word (before the merge)
+      if (FEAT & 1) {  // access counts: every lane's every mapped word (before the merge)
         for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * g + (__ffs(m) - 1)], 1u);
       }
       adjacent_merge32(g, mk, has, lane);
@@ -264,33 +266,32 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   smem_flush_instr(sm, a.instr_ctr);
 }
 
-template <int MINB>
+template <int FEAT>
 static void launch_decode_t(const DecodeArgs& a, int num_sms, cudaStream_t s, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(decode_kernel<3, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<MINB>, kDecWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<3, FEAT>, kDecWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const ull want = ((ull)a.n_ranges + kDecWarps - 1) / kDecWarps;
   ull grid = (ull)num_sms * per_sm;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
-  decode_kernel<MINB><<<(unsigned)grid, kDecWarps * 32, smem, s>>>(a);
+  decode_kernel<3, FEAT><<<(unsigned)grid, kDecWarps * 32, smem, s>>>(a);
 }
 
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
   const size_t smem = decode_smem(a);
-  static int minb = -1;
-  if (minb < 0) {
-    const char* e = getenv("THERMO_DECODE_MINB");
-    minb = e ? atoi(e) : 3;
+  const int feat = (a.acc ? 1 : 0) | (a.block_warps ? 2 : 0);
+  switch (feat) {
+    case 0: launch_decode_t<0>(a, num_sms, s, smem); break;
+    case 1: launch_decode_t<1>(a, num_sms, s, smem); break;
+    case 2: launch_decode_t<2>(a, num_sms, s, smem); break;
+    default: launch_decode_t<3>(a, num_sms, s, smem); break;
   }
-  if (minb == 2) launch_decode_t<2>(a, num_sms, s, smem);
-  else if (minb == 4) launch_decode_t<4>(a, num_sms, s, smem);
-  else launch_decode_t<3>(a, num_sms, s, smem);
 }
 
 }  // namespace thermo

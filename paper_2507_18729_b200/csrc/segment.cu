@@ -102,7 +102,7 @@ __global__ void seg_scan_blocks(ull* bsum, ull nb, ull* total) {
 
 // off[j] = exclusive prefix of cnt; cur[j] = off[j] (scatter cursors)
 __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum,
-                               ull* __restrict__ off, ull* __restrict__ cur) {
+                               ull* __restrict__ off) {
   __shared__ ull ws[kSegWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
@@ -127,7 +127,7 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
-    if (j < n) { off[j] = pre; cur[j] = pre; }
+    if (j < n) off[j] = pre;
     pre += v[k];
   }
 }
@@ -460,7 +460,7 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
   seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc,
                                                        reinterpret_cast<ull*>(ws.maxc) + 1);
   seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
-  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.cur);
+  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off);
   ws.launches += 3;
   ull hv[2];
   if ((e = cudaMemcpyAsync(hv, ws.maxc, 2 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
