@@ -343,6 +343,14 @@ def main():
             "stats": {k: st[k] for k in ("keys_emitted", "pc_keys_emitted", "distinct_pairs", "distinct_pc_pairs",
                                           "n_pcs")},
             "e2e": e2e}
+    if sharded:  # NVLink roofline of the key all-to-all (row e), slowest rank
+        xt = torch.tensor([st["ms_exchange"], float(st["exchange_bytes"])], device=dev, dtype=torch.float64)
+        if ws > 1:
+            dist.all_reduce(xt, op=dist.ReduceOp.MAX)
+        xms, xb = float(xt[0]), float(xt[1])
+        line["nvlink"] = {"exchange_ms": xms, "bytes_sent_per_rank": xb,
+                          "achieved": xb / (xms / 1e3) / 1e9 if xms > 0 else None, "peak": 900.0, "unit": "GB/s",
+                          "frac": (xb / (xms / 1e3) / 1e9) / 900.0 if xms > 0 else None}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:

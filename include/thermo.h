@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define THERMO_ABI_VERSION 2u
+#define THERMO_ABI_VERSION 3u
 #define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
 #define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
 #define THERMO_MAX_OBJECTS 1024
@@ -214,6 +214,10 @@ typedef struct {
    * (a4+a6), indicators (a7) */
   double ms_decode, ms_dedup, ms_count, ms_hist, ms_pc, ms_indicators;
   uint64_t kernel_launches;    /* libthermo kernels launched since create      */
+  /* sharded mode, last build: the key all-to-all's device time on this rank
+   * and the bytes it sent to other ranks (NVLink roofline of row e) */
+  double ms_exchange;
+  uint64_t exchange_bytes;
 } thermo_stats;
 
 typedef struct thermo_ctx thermo_ctx;

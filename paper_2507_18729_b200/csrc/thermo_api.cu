@@ -124,6 +124,9 @@ struct thermo_ctx {
   ull *d_instr_g = nullptr, *d_launch_g = nullptr;  // job-wide copies (after build)
   ull h_ctr_g[17] = {};                      // job-wide DevCounters + records (after build)
   bool have_glob = false;
+  cudaEvent_t evx[2] = {nullptr, nullptr};  // around the key all-to-all
+  float ms_exchange = 0;
+  ull exchange_bytes = 0;
 };
 
 namespace {
@@ -327,8 +330,18 @@ thermo_status dist_exchange(thermo_ctx* ctx, const DevCounters& hc) {
   }
   thermo_status st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_exch + total + 64, ctx->n_exch);
   if (st) return st;
+  if (!ctx->evx[0]) {
+    CK(cudaEventCreate(&ctx->evx[0]));
+    CK(cudaEventCreate(&ctx->evx[1]));
+  }
+  CK(cudaEventRecord(ctx->evx[0], s));
   DCK(c->alltoallv(ctx->sw.alt, scnt.data(), sdispl.data(), ctx->d_keys + ctx->n_exch, rcnt.data(), rdispl.data(), s));
+  CK(cudaEventRecord(ctx->evx[1], s));
   CK(cudaStreamSynchronize(s));
+  cudaEventElapsedTime(&ctx->ms_exchange, ctx->evx[0], ctx->evx[1]);
+  ctx->exchange_bytes = 0;
+  for (uint32_t q = 0; q < P; ++q)
+    if ((int)q != ctx->rank) ctx->exchange_bytes += scnt[q] * sizeof(ull);
   ctx->n_keys = ctx->n_exch + total;
   ctx->n_exch = ctx->n_keys;
   CK(cudaMemcpy(&ctx->d_ctr->n_keys, &ctx->n_keys, sizeof(ull), cudaMemcpyHostToDevice));  // later ingests append
@@ -503,6 +516,8 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
   for (int i = 0; i < 8; ++i)
     if (ctx->evp[i]) cudaEventDestroy(ctx->evp[i]);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  for (int i = 0; i < 2; ++i)
+    if (ctx->evx[i]) cudaEventDestroy(ctx->evx[i]);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1237,6 +1252,8 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
   out->ms_pc = ctx->ms_phase[4];
   out->ms_indicators = ctx->ms_phase[5];
   out->kernel_launches = ctx->launches;
+  out->ms_exchange = ctx->ms_exchange;
+  out->exchange_bytes = ctx->exchange_bytes;
   return THERMO_OK;
 }
 

@@ -70,7 +70,8 @@ class thermo_stats(ctypes.Structure):
                 ("reserved0", u32), ("ms_ingest", ctypes.c_double), ("ms_build", ctypes.c_double),
                 ("ms_classify", ctypes.c_double), ("ms_decode", ctypes.c_double), ("ms_dedup", ctypes.c_double),
                 ("ms_count", ctypes.c_double), ("ms_hist", ctypes.c_double), ("ms_pc", ctypes.c_double),
-                ("ms_indicators", ctypes.c_double), ("kernel_launches", u64)]
+                ("ms_indicators", ctypes.c_double), ("kernel_launches", u64),
+                ("ms_exchange", ctypes.c_double), ("exchange_bytes", u64)]
 
 
 # every symbol include/thermo.h declares
