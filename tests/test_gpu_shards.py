@@ -156,3 +156,29 @@ def test_nccl_transport_single_rank(monkeypatch):
     th.build(BOTH, oracle.ALL_LAUNCHES)
     ref = single(t, [t.records], 0, oracle.ALL_LAUNCHES, 2)
     compare(t, ref, [th])
+
+
+def test_shards_warp_records():
+    """Warp-instruction records (f4) ingested by 3 in-process shards: same
+    job-wide result as one context."""
+    from paper_2507_18729_b200 import Thermo
+    from paper_2507_18729_b200.dist import run_ranks
+    objects, recs = tg.random_warp_trace(n_instr=6000, seed=21, n_launches=2, max_len=300000)
+    t = tg.Trace("warp-shards", objects, recs, meta=dict(launches=2))
+    parts = [recs[i::3].contiguous() for i in range(3)]  # any split: every warp record is one instruction
+    ref = Thermo(max_launches=2, max_warps_per_launch=1 << 22)
+    ref.register_objects(objects)
+    for p in parts:
+        ref.ingest_warp(p.cuda())
+    ref.build(BOTH)
+    shards = Thermo.local_shards(3, max_launches=2, max_warps_per_launch=1 << 22)
+
+    def job(r):
+        def f():
+            shards[r].register_objects(objects)
+            shards[r].ingest_warp(parts[r].cuda())
+            shards[r].build(BOTH)
+        return f
+
+    run_ranks([job(r) for r in range(3)])
+    compare(t, ref, shards)
