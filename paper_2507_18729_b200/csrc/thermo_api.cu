@@ -18,6 +18,7 @@ namespace {
 
 constexpr ull kRangeLen = 8192;          // records per decode work range
 constexpr ull kHostChunk = 1ull << 24;   // records per staged host chunk
+constexpr ull kWarpChunk = 1ull << 20;   // warp records per staged host chunk (272 MB)
 constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors) = 1 << kShardShift
 static_assert(kTileSectors == (1ull << kShardShift), "a tile is one ownership chunk");
 
@@ -107,6 +108,7 @@ struct thermo_ctx {
   bool seg_counted = false;  // the decoder counts keys per sector (SEGMENT histogram, one rank)
   uint32_t* d_acc = nullptr;  // [8 S_tot] lane accesses per word (track_access)
   uint4* d_spill = nullptr;   // per-lane records of spilled warp instructions
+  uint4* d_wstage[2] = {nullptr, nullptr};  // host warp-record staging (kWarpChunk records each)
   size_t spill_cap = 0;
   ull* d_wctr = nullptr;      // [2] spilled records, lane records seen
 
@@ -506,7 +508,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
-                  ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr};
+                  ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr, ctx->d_wstage[0], ctx->d_wstage[1]};
   for (void* b : bufs) dfree(b);
   for (int i = 0; i < 2; ++i) {
     if (ctx->h_pinned[i]) cudaFreeHost(ctx->h_pinned[i]);
@@ -768,38 +770,61 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
     cudaGetLastError();
   }
   cudaStream_t s = ctx->stream;
-  const uint4* drec = reinterpret_cast<const uint4*>(recs);
-  uint4* tmp = nullptr;
-  if (!on_device) {  // host records: one device copy (convenience; the measured path is device-resident)
-    CK(dalloc(&tmp, n * 17));
-    CK(cudaMemcpyAsync(tmp, recs, n * 272, cudaMemcpyHostToDevice, s));
-    drec = tmp;
-  }
-  const ull lanes_max = 32 * (ull)n;
-  st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * lanes_max + 64, ctx->n_keys);
-  if (st) { dfree(tmp); return st; }
-  if (ctx->spill_cap < lanes_max) {  // worst case: every instruction spills
+  // host records: chunks of kWarpChunk instructions copied on the copy stream
+  // into two device staging buffers, each copy overlapped with the previous
+  // chunk's decode (the device path is one chunk)
+  const ull C = on_device ? (ull)n : std::min<ull>(n, kWarpChunk);
+  const ull lanes_max = 32 * C;
+  st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * 32 * (ull)n + 64, ctx->n_keys);
+  if (st) return st;
+  if (ctx->spill_cap < lanes_max) {  // worst case: every instruction of a chunk spills
     dfree(ctx->d_spill);
     ctx->d_spill = nullptr;
     ctx->spill_cap = 0;
-    if (dalloc(&ctx->d_spill, lanes_max) != cudaSuccess) { dfree(tmp); return fail(ctx, THERMO_ENOMEM, "spill"); }
+    if (dalloc(&ctx->d_spill, lanes_max) != cudaSuccess) return fail(ctx, THERMO_ENOMEM, "spill");
     ctx->spill_cap = lanes_max;
   }
+  if (!on_device)
+    for (int b = 0; b < 2; ++b)
+      if (!ctx->d_wstage[b]) CK(dalloc(&ctx->d_wstage[b], kWarpChunk * 17));
   if (!ctx->d_wctr) CK(dalloc(&ctx->d_wctr, 2));
   CK(cudaEventRecord(ctx->ev0, s));
   CK(cudaEventRecord(ctx->evp[6], s));
-  CK(cudaMemsetAsync(ctx->d_wctr, 0, 2 * sizeof(ull), s));
-  DecodeArgs a = decode_args(ctx);
-  launch_decode_warp(a, drec, n, ctx->d_spill, ctx->d_wctr, ctx->num_sms, s);
-  ctx->launches += 1;
-  CK(cudaGetLastError());
-  ull wc[2];
-  CK(cudaMemcpyAsync(wc, ctx->d_wctr, sizeof wc, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  dfree(tmp);
-  if (wc[0]) {  // spilled instructions: their per-lane records through the per-lane kernels
-    st = decode_device(ctx, ctx->d_spill, wc[0]);
-    if (st) return st;
+  const unsigned char* hsrc = reinterpret_cast<const unsigned char*>(recs);
+  auto issue_copy = [&](ull k) -> thermo_status {
+    const int b = (int)(k & 1);
+    const ull i0 = k * C, cnt = std::min<ull>(C, n - i0);
+    CK(cudaEventSynchronize(ctx->ev_used[b]));  // staging buffer b free again
+    CK(cudaMemcpyAsync(ctx->d_wstage[b], hsrc + i0 * 272, cnt * 272, cudaMemcpyHostToDevice, ctx->copy_stream));
+    CK(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+    return THERMO_OK;
+  };
+  const ull nchunks = (n + C - 1) / C;
+  if (!on_device && (st = issue_copy(0))) return st;
+  ull lanes = 0;
+  for (ull k = 0; k < nchunks; ++k) {
+    const int b = (int)(k & 1);
+    const ull i0 = k * C, cnt = std::min<ull>(C, n - i0);
+    if (!on_device && k + 1 < nchunks && (st = issue_copy(k + 1))) return st;
+    const uint4* drec = reinterpret_cast<const uint4*>(recs) + i0 * 17;
+    if (!on_device) {
+      CK(cudaStreamWaitEvent(s, ctx->ev_copied[b], 0));
+      drec = ctx->d_wstage[b];
+    }
+    CK(cudaMemsetAsync(ctx->d_wctr, 0, 2 * sizeof(ull), s));
+    DecodeArgs a = decode_args(ctx);
+    launch_decode_warp(a, drec, cnt, ctx->d_spill, ctx->d_wctr, ctx->num_sms, s);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    if (!on_device) CK(cudaEventRecord(ctx->ev_used[b], s));
+    ull wc[2];
+    CK(cudaMemcpyAsync(wc, ctx->d_wctr, sizeof wc, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (wc[0]) {  // spilled instructions: their per-lane records through the per-lane kernels
+      st = decode_device(ctx, ctx->d_spill, wc[0]);
+      if (st) return st;
+    }
+    lanes += wc[1];
   }
   CK(cudaEventRecord(ctx->evp[7], s));
   CK(cudaEventRecord(ctx->ev1, s));
@@ -807,7 +832,7 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
   if (st) return st;
   cudaEventElapsedTime(&ctx->ms_ingest, ctx->ev0, ctx->ev1);
   cudaEventElapsedTime(&ctx->ms_phase[0], ctx->evp[6], ctx->evp[7]);
-  ctx->records += wc[1];
+  ctx->records += lanes;
   ctx->state = 2;
   ctx->hist_valid = false;
   ctx->have_glob = false;

@@ -345,3 +345,25 @@ def test_run_compression(i):
         a, b = th.runs(obj[3]), orc.runs(k)
         for x, y in zip(a, b):
             assert np.array_equal(x, y), (t.name, obj[4])
+
+
+def test_gemm_full_size_warp_records_from_host():
+    """BJ configs[1] as 8.45 M warp-instruction records ingested from pinned host
+    memory (several staged chunks): the closed forms on every cell."""
+    from paper_2507_18729_b200 import Thermo
+    t = tg.gemm(1024, 1024, 128, "v00", device="cuda")
+    w = tg.to_warp_records(t.records)
+    objects = t.objects
+    del t
+    host = torch.empty_like(w, device="cpu").pin_memory()
+    host.copy_(w)
+    del w
+    th = Thermo(max_launches=1, max_warps_per_launch=1 << 20)
+    th.register_objects(objects)
+    th.ingest_warp(host)
+    th.build()
+    assert (th.heatmap(0, WORD) == 1024).all() and (th.heatmap(0, SECTOR) == 1024).all()
+    assert (th.heatmap(1, WORD) == 32).all() and (th.heatmap(1, SECTOR) == 256).all()
+    assert (th.heatmap(2, WORD) == 1).all() and (th.heatmap(2, SECTOR) == 8).all()
+    st = th.stats()
+    assert st["records"] == 270532608 and st["distinct_pairs"] == 22020096
