@@ -115,9 +115,10 @@ typedef enum {
 /* dedup paths for the main (sector, launch, warp) keys (a4):
  *   SORT     onesweep LSD radix sort on all key bits
  *   HASH     open-addressing hash set in HBM
- *   SEGMENT  counting sort by sector + per-chunk shared-memory dedup (falls
- *            back to SORT when one sector holds more keys than a chunk)
- *   AUTO     SEGMENT (chosen by measurement) */
+ *   SEGMENT  counting sort by sector + per-chunk shared-memory dedup; the
+ *            keys of sectors holding >= 2048 keys take a hash-set side path
+ *   AUTO     SEGMENT up to 2^25 registered sectors, HASH beyond (chosen by
+ *            measurement) */
 typedef enum {
   THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2, THERMO_DEDUP_SEGMENT = 3
 } thermo_dedup;
@@ -308,8 +309,9 @@ thermo_status thermo_ingest_trace(thermo_ctx *ctx, const thermo_record *recs, si
  * popcount flush): dense per-object word and sector distinct-warp counts,
  * level histograms per object and per PC.  launch_filter selects one launch
  * (the paper's per-kernel heat map, G2) or THERMO_ALL_LAUNCHES (launch-
- * qualified warps of all launches).  g selects which histograms are computed;
- * counts are always produced for both granularities.  Errors: ESTATE, ERANGE
+ * qualified warps of all launches).  g (WORD, SECTOR or BOTH) is checked and
+ * recorded; counts and histograms are always produced for both granularities.
+ * May be called again (another filter) from the retained keys.  Errors: ESTATE, ERANGE
  * (out-of-range records were ingested, or too many distinct pcs), ECUDA.
  */
 thermo_status thermo_build_heatmap(thermo_ctx *ctx, thermo_granularity g, uint32_t launch_filter);

@@ -34,14 +34,6 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
-__device__ __forceinline__ ull warp_min64(ull v) {
-  for (int d = 16; d; d >>= 1) { ull o = __shfl_xor_sync(FULL, v, d); v = o < v ? o : v; }
-  return v;
-}
-__device__ __forceinline__ ull warp_max64(ull v) {
-  for (int d = 16; d; d >>= 1) { ull o = __shfl_xor_sync(FULL, v, d); v = o > v ? o : v; }
-  return v;
-}
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16;
@@ -60,9 +52,6 @@ __device__ __forceinline__ int obj_lookup(const ull* s_lo, const ull* s_hi, uint
   return (n > 0 && x >= s_lo[lo] && x < s_hi[lo]) ? (int)lo : -1;
 }
 
-__device__ __forceinline__ bool in_obj(const ull* s_lo, const ull* s_hi, int o, ull x) {
-  return o >= 0 && x >= s_lo[o] && x < s_hi[o];
-}
 
 // word mask of a sector restricted to the object's words (tail sector of an
 // object whose length is not a multiple of 32 bytes, G9)
