@@ -367,3 +367,43 @@ def test_gemm_full_size_warp_records_from_host():
     assert (th.heatmap(2, WORD) == 1).all() and (th.heatmap(2, SECTOR) == 8).all()
     st = th.stats()
     assert st["records"] == 270532608 and st["distinct_pairs"] == 22020096
+
+
+def test_window_boundaries():
+    """Objects and instructions across 4 GiB address windows (the fast decoder
+    works on 32-bit offsets inside one window) and at the top of the 48-bit
+    space; lanes of one instruction in two windows go to the general path."""
+    import torch
+    g = torch.Generator().manual_seed(17)
+    objects = [(0xFFFFF000, 0x3000, 0, 1, "cross4G"), (0x2FFFFFFE0, 100, 0, 2, "cross8G"),
+               (0x3FFFFFF00, 0x200, 0, 3, "cross16G"), ((1 << 48) - 4096, 4096 - 8, 0, 4, "top"),
+               (0xFFFFF000, 0x2000, 1, 5, "shared-cross")]
+    n_instr = 3000
+    oi = torch.randint(0, len(objects), (n_instr,), generator=g)
+    base = torch.tensor([o[0] for o in objects])[oi]
+    ln = torch.tensor([o[1] for o in objects])[oi]
+    space = torch.tensor([o[2] for o in objects])[oi]
+    lane = torch.arange(32)
+    mode = torch.randint(0, 3, (n_instr,), generator=g)
+    start = (torch.rand(n_instr, generator=g) * (ln + 64).to(torch.float64)).to(torch.int64) - 32
+    stride = torch.randint(1, 200, (n_instr,), generator=g)
+    off = torch.where((mode == 0)[:, None], start[:, None] + 4 * lane[None, :],
+                      torch.where((mode == 1)[:, None], start[:, None] + stride[:, None] * lane[None, :],
+                                  (torch.rand((n_instr, 32), generator=g) * (ln + 64).to(torch.float64)[:, None]).to(
+                                      torch.int64) - 32))
+    addr = torch.clamp(base[:, None] + off, min=0, max=(1 << 48) - 16)
+    active = torch.rand((n_instr, 32), generator=g) < 0.8
+    active[:, 0] = True
+    l2s = torch.randint(0, 4, (n_instr,), generator=g)
+    warp = torch.randint(0, 40, (n_instr,), generator=g)
+    recs = tg.from_instructions(addr, active, warp, 0x100 + 16 * (oi % 3), 0, l2s, space)
+    t = tg.Trace("windows", objects, recs, meta=dict(launches=1))
+    for dedup in (0, 1, 2):
+        orc, th = run_both(t, dedup=dedup)
+        compare(orc, th, t)
+    # the same instructions as warp-instruction records
+    from paper_2507_18729_b200 import Thermo
+    th = gpu_ctx(t)
+    th.ingest_warp(tg.to_warp_records(recs).cuda())
+    th.build(BOTH)
+    compare(oracle.run([o[:4] for o in objects], [recs]), th, t)
