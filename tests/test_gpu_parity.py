@@ -407,3 +407,24 @@ def test_window_boundaries():
     th.ingest_warp(tg.to_warp_records(recs).cuda())
     th.build(BOTH)
     compare(oracle.run([o[:4] for o in objects], [recs]), th, t)
+
+
+@pytest.mark.parametrize("dedup", [0, 1, 2])
+def test_many_objects(dedup):
+    """1000 registered objects (near THERMO_MAX_OBJECTS): the shared-memory object
+    table, the binary searches and the interval cache at full size."""
+    t = tg.random_trace(n=40000, seed=31, n_objects=1000, n_warps=200, n_launches=2, max_len=400)
+    t.meta["launches"] = 2
+    orc, th = run_both(t, dedup=dedup)
+    compare(orc, th, t)
+    from paper_2507_18729_b200 import Thermo
+    objects, recs = tg.random_warp_trace(n_instr=3000, seed=32, n_objects=1000, max_len=400)
+    tw = tg.Trace("warp-many", objects, recs, meta=dict(launches=2))
+    th = Thermo(max_launches=2, max_warps_per_launch=1 << 22, dedup=dedup)
+    th.register_objects(objects)
+    th.ingest_warp(recs.cuda())
+    th.build(BOTH)
+    orc = oracle.Oracle([o[:4] for o in objects])
+    orc.ingest_warp(recs)
+    orc.build()
+    compare(orc, th, tw)
