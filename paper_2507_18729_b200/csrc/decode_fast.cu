@@ -266,31 +266,32 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   smem_flush_instr(sm, a.instr_ctr);
 }
 
-template <int FEAT>
+template <int MINB, int FEAT>
 static void launch_decode_t(const DecodeArgs& a, int num_sms, cudaStream_t s, size_t smem) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<3, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(decode_kernel<MINB, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<3, FEAT>, kDecWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<MINB, FEAT>, kDecWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   const ull want = ((ull)a.n_ranges + kDecWarps - 1) / kDecWarps;
   ull grid = (ull)num_sms * per_sm;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
-  decode_kernel<3, FEAT><<<(unsigned)grid, kDecWarps * 32, smem, s>>>(a);
+  decode_kernel<MINB, FEAT><<<(unsigned)grid, kDecWarps * 32, smem, s>>>(a);
 }
 
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
   const size_t smem = decode_smem(a);
   const int feat = (a.acc ? 1 : 0) | (a.block_warps ? 2 : 0);
+  static const int minb = getenv("THERMO_DEC_MINB") ? atoi(getenv("THERMO_DEC_MINB")) : 3;
   switch (feat) {
-    case 0: launch_decode_t<0>(a, num_sms, s, smem); break;
-    case 1: launch_decode_t<1>(a, num_sms, s, smem); break;
-    case 2: launch_decode_t<2>(a, num_sms, s, smem); break;
-    default: launch_decode_t<3>(a, num_sms, s, smem); break;
+    case 0: if (minb == 4) launch_decode_t<4, 0>(a, num_sms, s, smem); else launch_decode_t<3, 0>(a, num_sms, s, smem); break;
+    case 1: launch_decode_t<3, 1>(a, num_sms, s, smem); break;
+    case 2: launch_decode_t<3, 2>(a, num_sms, s, smem); break;
+    default: launch_decode_t<3, 3>(a, num_sms, s, smem); break;
   }
 }
 

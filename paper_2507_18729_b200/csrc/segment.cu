@@ -7,8 +7,8 @@
 // Why: a5 only needs the keys grouped per sector, and the sector range is
 // small (SGEMM: 163,840 sectors), so an exact counting sort by sector
 // (histogram, scan, scatter) groups them in ~3 streaming passes instead of one
-// LSD pass per 8 key bits; the (launch, warp) and (pc) dedup then runs in
-// shared memory.  Sectors with more keys than a chunk holds make the caller
+// LSD pass per 8 key bits; the (launch, warp) and (pc) dedup then runs in a
+// shared-memory hash set per chunk (one insert per key, no sort).  Sectors with more keys than a chunk holds make the caller
 // fall back to the onesweep path (thermo_api.cu).
 #include "thermo_internal.cuh"
 
@@ -18,8 +18,6 @@ constexpr unsigned GFULL = 0xFFFFFFFFu;
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kSegCap = 2048;            // chunk window (keys); a chunk holds < 2 * kSegCap keys
-constexpr int kSegBuf = 2 * kSegCap;     // shared-memory key buffer
-constexpr int kSegRounds = kSegBuf / kSegThreads;  // 32 keys per thread
 constexpr int kScanBlock = 2048;         // scan elements per block (256 threads x 8)
 
 __device__ __forceinline__ unsigned lanemask_lt_g() {
@@ -198,67 +196,6 @@ __global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, u
 }
 
 
-// stable LSD radix sort of R * kSegThreads u64 keys in shared memory on bits
-// [lo, lo + bits) (warp w ranks keys [w R 32, (w + 1) R 32)); returns the
-// buffer holding the result
-__device__ ull* smem_radix_sort(ull* src, ull* dst, int lo, int bits, uint32_t* whist, uint32_t* blk_ofs, int R) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned lt = lanemask_lt_g();
-  __shared__ uint32_t wsum[kSegWarps];
-  for (int shift = lo; shift < lo + bits; shift += 8) {
-    for (int i = threadIdx.x; i < kSegWarps * 256; i += kSegThreads) whist[i] = 0;
-    __syncthreads();
-    uint32_t rank[kSegRounds];
-#pragma unroll
-    for (int r = 0; r < kSegRounds; ++r) {  // warp w ranks its own contiguous keys
-      if (r >= R) break;
-      const uint32_t idx = (uint32_t)(w * R + r) * 32 + lane;
-      const uint32_t d = (uint32_t)(src[idx] >> shift) & 255u;
-      const unsigned peers = __match_any_sync(GFULL, d);
-      const int leader = __ffs(peers) - 1;
-      uint32_t old = 0;
-      if (lane == leader) old = whist[w * 256 + d];
-      old = __shfl_sync(GFULL, old, leader);
-      rank[r] = old + __popc(peers & lt);
-      __syncwarp();
-      if (lane == leader) whist[w * 256 + d] = old + __popc(peers);
-      __syncwarp();
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    uint32_t tot = 0;
-    for (int ww = 0; ww < kSegWarps; ++ww) {
-      const uint32_t v = whist[ww * 256 + t];
-      whist[ww * 256 + t] = tot;
-      tot += v;
-    }
-    // exclusive scan of the 256 digit totals: warp scans + warp sums
-    uint32_t incl = tot;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o = __shfl_up_sync(GFULL, incl, d);
-      if (lane >= d) incl += o;
-    }
-    if (lane == 31) wsum[w] = incl;
-    __syncthreads();
-    uint32_t wpre = 0;
-    for (int k = 0; k < w; ++k) wpre += wsum[k];
-    blk_ofs[t] = wpre + incl - tot;
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kSegRounds; ++r) {
-      if (r >= R) break;
-      const uint32_t idx = (uint32_t)(w * R + r) * 32 + lane;
-      const ull k = src[idx];
-      const uint32_t d = (uint32_t)(k >> shift) & 255u;
-      dst[blk_ofs[d] + whist[w * 256 + d] + rank[r]] = k;
-    }
-    __syncthreads();
-    ull* tmp = src; src = dst; dst = tmp;
-  }
-  return src;
-}
-
 // per-block (pc, level) bin table in shared memory: open addressing on the
 // bin id; a full table falls back to the global atomic
 constexpr int kPcBins = 512;
@@ -276,153 +213,171 @@ __device__ __forceinline__ void bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, 
   atomicAdd(&g[bin], (ull)v);
 }
 
-__global__ void __launch_bounds__(kSegThreads) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ off,
+// chunk hash set in shared memory: slot = (id << 8 | mask), id = the key's
+// (sector, launch, warp) or (sector, pc id) with the sector relative to the
+// chunk's first; insert ORs the mask into the id's slot (the OR of a
+// word's accesses is idempotent)
+constexpr int kHSlots = 5120;  // > 1.25 x the chunk's < 2 * kSegCap keys (typically ~2/3 of that)
+constexpr int kHWin = 1024;    // chunks spanning at most this many sectors count them in shared memory
+constexpr ull kHEmpty = ~0ull;
+// (a new entry appends its slot to `list`, so the scans visit occupied slots only)
+__device__ __forceinline__ void hset_or(ull* tab, uint16_t* list, uint32_t* nlist, ull id, uint32_t m) {
+  const uint32_t hx = (uint32_t)((id * 0x9E3779B97F4A7C15ull) >> 32);
+  uint32_t h = __umulhi(hx, (uint32_t)kHSlots);
+  const ull v = (id << 8) | m;
+  for (;;) {
+    ull cur = tab[h];
+    if (cur == kHEmpty) {
+      cur = atomicCAS(&tab[h], kHEmpty, v);
+      if (cur == kHEmpty) {
+        list[atomicAdd(nlist, 1u)] = (uint16_t)h;
+        return;
+      }
+    }
+    if ((cur >> 8) == id) {
+      if (((uint32_t)cur & m) != m) atomicOr(&tab[h], (ull)m);
+      return;
+    }
+    h = h + 1 == (uint32_t)kHSlots ? 0u : h + 1;
+  }
+}
+
+// chunk c owns the sectors [cs0[c], cs0[c + 1]) (those whose segment starts in
+// [c kSegCap, (c + 1) kSegCap)); their keys are seg[off[s0], off[s1]), fewer
+// than 2 kSegCap.  (a) distinct (sector, launch, warp) with OR-ed masks in a
+// shared-memory hash set -> sector count = #entries, word b's count = #entries
+// with bit b (the popcount flush of P:328, G6), summed per sector in shared
+// memory (or, for a chunk spanning > kHWin sectors, with warp-aggregated
+// global atomics); (b) distinct (sector, pc id) with OR-ed masks -> per-pc
+// level histograms (G11)
+__global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ off,
                                                                ull nsec, KeyLayout kl, uint32_t filter,
                                                                uint32_t* __restrict__ wc, uint32_t* __restrict__ sc,
                                                                const uint32_t* __restrict__ site_of,
                                                                ull* __restrict__ pc_hist, DevCounters* ctr,
                                                                const ull* __restrict__ cs0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ull* buf0 = reinterpret_cast<ull*>(smem_raw);                      // [kSegBuf]
-  ull* buf1 = buf0 + kSegBuf;                                        // [kSegBuf]
-  uint32_t* whist = reinterpret_cast<uint32_t*>(buf1 + kSegBuf);     // [kSegWarps][256]
-  __shared__ uint32_t blk_ofs[256];
-  __shared__ ull s_range[2];
+  ull* tab = reinterpret_cast<ull*>(smem_raw);                    // [kHSlots]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + kHSlots);     // [kHWin][5]: words (2b, 2b+1) as u16 pairs, sector
+  uint32_t* tbin = cnt + kHWin * 5;                               // [kPcBins]
+  uint32_t* tcnt = tbin + kPcBins;                                // [kPcBins]
+  uint16_t* list = reinterpret_cast<uint16_t*>(tcnt + kPcBins);   // [2 kSegCap] occupied slots
+  __shared__ uint32_t s_n[2];
   const int lane = threadIdx.x & 31;
   const ull c = blockIdx.x;
-  if (threadIdx.x == 0) {
-    s_range[0] = cs0[c];
-    s_range[1] = cs0[c + 1];
-  }
-  __syncthreads();
-  const ull s0 = s_range[0], s1 = s_range[1];
+  const ull s0 = cs0[c], s1 = cs0[c + 1];
   if (s0 >= s1) return;
   const ull k0 = off[s0];
-  const uint32_t nk = (uint32_t)(off[s1] - k0);  // < kSegBuf
-  const int R = (int)((nk + kSegThreads - 1) / kSegThreads);  // rounds of 256 keys actually used
-  const uint32_t npad = (uint32_t)R * kSegThreads;
-  int ls = 0;
-  while ((1ull << ls) < (s1 - s0)) ++ls;
-  const uint32_t LWP = kl.L + kl.W + kl.P;
-  // local key: [g - s0 : ls][launch, warp, pcid : LWP][mask : 8]; filtered-out
-  // launches and padding become the all-ones sentinel (sorted last)
-  for (uint32_t i = threadIdx.x; i < npad; i += kSegThreads) {
-    ull v = ~0ull;
-    if (i < nk) {
-      const ull k = seg[k0 + i];
-      if (filter == THERMO_ALL_LAUNCHES || key_launch(k, kl) == filter)
-        v = ((key_g(k, kl) - s0) << (LWP + 8)) | (k & ((1ull << (LWP + 8)) - 1));
-    }
-    buf0[i] = v;
+  const uint32_t nk = (uint32_t)(off[s1] - k0);  // < 2 kSegCap
+  const ull win = s1 - s0;
+  const bool local = win <= (ull)kHWin;
+  const uint32_t LW = kl.L + kl.W, RS = 8 + kl.P;
+  const ull lwmask = (1ull << LW) - 1;
+  for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
+  if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
+  if (local)
+    for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
+  __syncthreads();
+  // ---- (a) distinct (sector, launch, warp) ----
+  for (uint32_t i = threadIdx.x; i < nk; i += kSegThreads) {
+    const ull k = seg[k0 + i];
+    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
+    hset_or(tab, list, &s_n[0], ((key_g(k, kl) - s0) << LW) | ((k >> RS) & lwmask), (uint32_t)k & 0xFFu);
   }
   __syncthreads();
-  // runs of (g, launch, warp) only need those bits sorted; the pc id bits below stay unsorted
-  ull* src = smem_radix_sort(buf0, buf1, 8 + (int)kl.P, ls + (int)(kl.L + kl.W), whist, blk_ofs, R);
-  // ---- (a) runs of equal (g, launch, warp): distinct warps per sector / word ----
-  const int RS = 8 + (int)kl.P;
-  ull distinct = 0;
-  for (uint32_t base = 0; base < npad; base += kSegThreads) {
-    const uint32_t i = base + threadIdx.x;
-    const ull key = src[i];
-    const bool valid = key != ~0ull;
-    const ull pre = key >> RS;
-    const ull prev = i > 0 ? (src[i - 1] >> RS) : ~0ull;
-    const bool head = valid && pre != prev;
-    uint32_t m = (uint32_t)(key & 0xFF);
-    if (head)
-      for (uint32_t j = i + 1; j < npad && (src[j] >> RS) == pre; ++j) m |= (uint32_t)(src[j] & 0xFF);
-    const ull g = valid ? s0 + (key >> (LWP + 8)) : ~0ull;
-    ull v = 0;
-    if (head) {
-      v = 1ull;
+  const uint32_t nent = s_n[0];
+  for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
+    const uint32_t i = base + lane;
+    const bool occ = i < nent;
+    const ull v = occ ? tab[list[i]] : kHEmpty;
+    const uint32_t gl = occ ? (uint32_t)(v >> (8 + LW)) : 0xFFFFFFFFu;
+    const uint32_t m = occ ? (uint32_t)v & 0xFFu : 0u;
+    const unsigned peers = __match_any_sync(GFULL, gl);
+    uint32_t cb[8];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) v |= (ull)((m >> b) & 1u) << (6 * (b + 1));
-    }
-    distinct += head ? 1 : 0;
+    for (int b = 0; b < 8; ++b) cb[b] = __popc(__ballot_sync(GFULL, (m >> b) & 1u) & peers);
+    if (occ && lane == __ffs(peers) - 1) {
+      const uint32_t cs = __popc(peers);
+      if (local) {
+        uint32_t* cg = cnt + gl * 5;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const ull ov = __shfl_down_sync(GFULL, v, d);
-      const ull og = __shfl_down_sync(GFULL, g, d);
-      if (lane + d < 32 && og == g) v += ov;
-    }
-    const ull pg = __shfl_up_sync(GFULL, g, 1);
-    if ((lane == 0 || pg != g) && v && valid) {
-      const uint32_t c0 = (uint32_t)(v & 63);
-      if (c0) atomicAdd(&sc[g], c0);
+        for (int j = 0; j < 4; ++j)
+          if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
+        atomicAdd(&cg[4], cs);
+      } else {
+        const ull g = s0 + gl;
+        atomicAdd(&sc[g], cs);
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const uint32_t cb = (uint32_t)((v >> (6 * (b + 1))) & 63);
-        if (cb) atomicAdd(&wc[8 * g + b], cb);
+        for (int b = 0; b < 8; ++b)
+          if (cb[b]) atomicAdd(&wc[8 * g + b], cb[b]);
       }
     }
   }
-  for (int d = 16; d; d >>= 1) distinct += __shfl_xor_sync(GFULL, distinct, d);
-  if (lane == 0 && distinct) atomicAdd(&ctr->distinct_pairs, distinct);
+  if (threadIdx.x == 0 && nent) atomicAdd(&ctr->distinct_pairs, (ull)nent);
+  __syncthreads();
+  if (local) {  // the chunk owns its sectors: plain stores of the nonzero rows
+    for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
+      const uint32_t* cg = cnt + j * 5;
+      if (cg[4] == 0) continue;
+      const ull g = s0 + j;
+      sc[g] = cg[4];
+      uint4 lo, hi;
+      lo.x = cg[0] & 0xFFFFu; lo.y = cg[0] >> 16; lo.z = cg[1] & 0xFFFFu; lo.w = cg[1] >> 16;
+      hi.x = cg[2] & 0xFFFFu; hi.y = cg[2] >> 16; hi.z = cg[3] & 0xFFFFu; hi.w = cg[3] >> 16;
+      reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
+      reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
+    }
+  }
   if (!pc_hist) return;
-  __syncthreads();  // this chunk's dense counts are final (it owns its sectors)
-  // ---- (b) distinct (g, pcid) with OR-ed masks: per-pc level histograms (G11) ----
-  // a shared-memory hash set on the 32-bit (g - s0, pcid) key in the free buffer
-  // (runs of one (g, pcid) hold every warp touching the sector: too long to scan)
-  uint32_t* hk = reinterpret_cast<uint32_t*>(src == buf0 ? buf1 : buf0);  // [kSegBuf] keys
-  uint32_t* hm = hk + kSegBuf;                                            // [kSegBuf] masks
-  uint32_t* tbin = reinterpret_cast<uint32_t*>(whist);                    // [kPcBins] bin ids
-  uint32_t* tcnt = tbin + kPcBins;                                        // [kPcBins] counts
-  for (uint32_t i = threadIdx.x; i < kSegBuf; i += kSegThreads) { hk[i] = 0xFFFFFFFFu; hm[i] = 0; }
+  // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
+  for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
   for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
   __syncthreads();
   const ull pmask = (1ull << kl.P) - 1;
-  for (uint32_t i = threadIdx.x; i < npad; i += kSegThreads) {
-    const ull k = src[i];
-    if (k == ~0ull) continue;
-    const uint32_t hkey = (uint32_t)(((k >> (LWP + 8)) << kl.P) | ((k >> 8) & pmask));
-    const uint32_t m = (uint32_t)(k & 0xFF);
-    uint32_t h = (hkey * 0x9E3779B1u) & (kSegBuf - 1);
-    for (int probe = 0; probe < kSegBuf; ++probe) {
-      uint32_t cur = hk[h];
-      if (cur == 0xFFFFFFFFu) {
-        cur = atomicCAS(&hk[h], 0xFFFFFFFFu, hkey);
-        if (cur == 0xFFFFFFFFu) cur = hkey;
-      }
-      if (cur == hkey) {
-        if ((hm[h] & m) != m) atomicOr(&hm[h], m);
-        break;
-      }
-      h = (h + 1) & (kSegBuf - 1);
-    }
+  for (uint32_t i = threadIdx.x; i < nk; i += kSegThreads) {
+    const ull k = seg[k0 + i];
+    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
+    hset_or(tab, list, &s_n[1], ((key_g(k, kl) - s0) << kl.P) | ((k >> 8) & pmask), (uint32_t)k & 0xFFu);
   }
   __syncthreads();
-  ull dpc = 0;
-  for (uint32_t base = 0; base < kSegBuf; base += kSegThreads) {
-    const uint32_t i = base + threadIdx.x;
-    const uint32_t hkey = hk[i];
-    const bool head = hkey != 0xFFFFFFFFu;
-    const uint32_t m = hm[i];
-    dpc += head ? 1 : 0;
-    if (!__any_sync(GFULL, head)) continue;
-    const ull g = s0 + (hkey >> kl.P);
-    const uint32_t pcid = (uint32_t)(hkey & pmask);
+  const uint32_t npc = s_n[1];
+  for (uint32_t base = threadIdx.x & ~31u; base < npc; base += kSegThreads) {
+    const uint32_t i = base + lane;
+    const bool head = i < npc;
+    const ull v = head ? tab[list[i]] : kHEmpty;
+    const uint32_t gl = (uint32_t)(v >> (8 + kl.P));
+    const uint32_t pcid = (uint32_t)((v >> 8) & pmask);
+    const uint32_t m = (uint32_t)v & 0xFFu;
+    const uint32_t* cg = cnt + gl * 5;
+    const ull g = s0 + gl;
     {
-      const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(sc[g]) : 0xFFFFFFFFu;
+      const uint32_t scv = head ? (local ? cg[4] : __ldcg(&sc[g])) : 0u;
+      const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(scv) : 0xFFFFFFFFu;
       const unsigned mm = __match_any_sync(GFULL, bin);
       if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
     }
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const bool hb = head && ((m >> b) & 1u);
-      const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wc[8 * g + b]) : 0xFFFFFFFFu;
+      uint32_t wv = 0;
+      if (hb) wv = local ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : __ldcg(&wc[8 * g + b]);
+      const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wv) : 0xFFFFFFFFu;
       const unsigned mm = __match_any_sync(GFULL, bin);
       if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
     }
   }
-  for (int d = 16; d; d >>= 1) dpc += __shfl_xor_sync(GFULL, dpc, d);
-  if (lane == 0 && dpc) atomicAdd(&ctr->distinct_pc, dpc);
+  if (threadIdx.x == 0 && npc) atomicAdd(&ctr->distinct_pc, (ull)npc);
   __syncthreads();
   for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
     if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
   (void)site_of;
+  (void)nsec;
 }
 
-static size_t segment_chunk_smem() { return (size_t)2 * kSegBuf * sizeof(ull) + kSegWarps * 256 * sizeof(uint32_t); }
+static size_t segment_chunk_smem() {
+  return (size_t)kHSlots * sizeof(ull) + ((size_t)kHWin * 5 + 2 * kPcBins) * sizeof(uint32_t) +
+         2 * kSegCap * sizeof(uint16_t);
+}
 ull segment_chunk_cap() { return kSegCap; }
 
 // phases 1-2; syncs once so the caller can read the largest per-sector count
