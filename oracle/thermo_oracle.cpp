@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <array>
 #include <map>
 #include <set>
 #include <unordered_map>
@@ -92,6 +93,8 @@ struct Oracle {
   // restriction (sampled mode): only these (object index, local sector) pairs
   bool restricted = false;
   std::set<std::pair<uint32_t, uint64_t>> allow;
+  // restricted build: the allowed sectors' rows only (8 word counts, sector count)
+  std::map<std::pair<uint32_t, uint64_t>, std::array<uint32_t, 9>> sampled;
 
   // Wset[(o, w)] = set of (launch<<32 | warp)  (written as a set)
   std::unordered_map<uint64_t, std::set<uint64_t>> wset;
@@ -188,9 +191,35 @@ struct Oracle {
     return c;
   }
 
+  // one sector's row, straight from the sets (G6)
+  std::array<uint32_t, 9> sector_row(uint32_t o, uint64_t s) const {
+    std::array<uint32_t, 9> row{};
+    std::set<uint64_t> u;
+    for (uint64_t b = 0; b < 8; ++b) {
+      auto it = wset.find(wkey(o, 8 * s + b));
+      if (it == wset.end()) continue;
+      row[b] = uint32_t(filtered_size(it->second));
+      for (uint64_t lw : it->second) if (pass(lw)) u.insert(lw);
+    }
+    row[8] = uint32_t(u.size());
+    return row;
+  }
+
   void build(uint32_t f) {
     filter = f;
     size_t no = objs.size();
+    if (restricted) {  // sampled mode: only the allowed sectors' rows (no dense arrays;
+      // dense queries, histograms and indicators then read empty / zero)
+      word_count.assign(no, {});
+      sector_count.assign(no, {});
+      hist_word.assign(no, std::vector<uint64_t>(33, 0));
+      hist_sector.assign(no, std::vector<uint64_t>(33, 0));
+      pcrows.clear();
+      sampled.clear();
+      for (auto& os : allow) sampled[os] = sector_row(os.first, os.second);
+      built = true;
+      return;
+    }
     word_count.assign(no, {});
     sector_count.assign(no, {});
     hist_word.assign(no, std::vector<uint64_t>(33, 0));
@@ -389,6 +418,11 @@ void orc_sample(void* h, const uint32_t* obj_idx, const uint64_t* sectors, size_
   for (size_t i = 0; i < n; ++i) {
     uint32_t o = obj_idx[i];
     uint64_t s = sectors[i];
+    if (p->restricted) {
+      auto it = p->sampled.find({o, s});
+      for (int b = 0; b < 9; ++b) out[9 * i + b] = it == p->sampled.end() ? 0u : it->second[b];
+      continue;
+    }
     for (int b = 0; b < 8; ++b) {
       uint64_t w = 8 * s + b;
       out[9 * i + b] = w < p->word_count[o].size() ? p->word_count[o][w] : 0;

@@ -73,8 +73,6 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
   const uint32_t LW = a.kl.L + a.kl.W, P = a.kl.P;
 
   Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0, a.seg_cnt, 8 + a.kl.P + a.kl.L + a.kl.W};
-  InstrCache icache;
-  icache.init();
   ull n_invalid = 0, n_oor = 0, n_mapped = 0, n_unmapped = 0;
   uint32_t cur_launch = 0xFFFFFFFFu;
 
@@ -222,12 +220,11 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
         const int o = __shfl_sync(FULL, i_obj, h);
         const uint32_t la = __shfl_sync(FULL, i_launch, h);
         const bool mh = __shfl_sync(FULL, mis, h);
-        icache.add(la * nobj + (uint32_t)o + 1u, mh, sm.ikey, sm.ival, a.instr_ctr, lane);
+        instr_add(sm, la * nobj + (uint32_t)o + 1u, mh, a.instr_ctr, lane);
       }
     }
   }
   st.flush(a.keys, &a.ctr->n_keys, lane);
-  icache.drain(sm.ikey, sm.ival, a.instr_ctr, lane);
   flush_launch_ctr(a.launch_ctr, cur_launch, n_unmapped, n_mapped);
   for (int d = 16; d; d >>= 1) {
     n_invalid += __shfl_xor_sync(FULL, n_invalid, d);

@@ -199,35 +199,6 @@ static __device__ __noinline__ void instr_flush(uint32_t* s_ikey, ull* s_ival, u
   if (nm) atomicAdd(&g_ctr[2 * (key - 1) + 1], (ull)nm);
 }
 
-// per-warp register cache of the (launch, object) misalignment counters;
-// warp-uniform values, lane 0 flushes evictions into the block's table
-struct InstrCache {
-  uint32_t k0, k1, i0, m0, i1, m1;
-  __device__ __forceinline__ void init() { k0 = k1 = 0; i0 = m0 = i1 = m1 = 0; }
-  __device__ __forceinline__ void add(uint32_t key, bool mis, uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
-    bool h0 = key == k0;
-    const bool h1 = key == k1;
-    if (!(h0 | h1)) {  // (warp-uniform) evict entry 1
-      if (k1 && lane == 0) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
-      k1 = k0; i1 = i0; m1 = m0;
-      k0 = key; i0 = 0; m0 = 0;
-      h0 = true;
-    }
-    i0 += h0;
-    m0 += h0 & mis;
-    i1 += h1;
-    m1 += h1 & mis;
-  }
-  __device__ __forceinline__ void drain(uint32_t* s_ikey, ull* s_ival, ull* g, int lane) {
-    if (lane == 0) {
-      if (k0) instr_flush(s_ikey, s_ival, g, k0, i0, m0);
-      if (k1) instr_flush(s_ikey, s_ival, g, k1, i1, m1);
-    }
-    init();
-  }
-};
-
-
 // shared-memory layout common to both decode kernels: object table, one
 // per-warp key staging buffer, the block's (launch, object) counter table and
 // (site -> pc id) cache
@@ -241,10 +212,12 @@ constexpr size_t kOffIval = 0;                                         // [kInst
 constexpr size_t kOffPc = kOffIval + 2 * kInstrSlots * sizeof(ull);    // [kPcSlots] u64
 constexpr size_t kOffIkey = kOffPc + kPcSlots * sizeof(ull);           // [kInstrSlots] u32
 constexpr size_t kOffWarp = (kOffIkey + kInstrSlots * sizeof(uint32_t) + 15) & ~(size_t)15;  // [kDecWarps]
-constexpr size_t kOffObj = kOffWarp + (size_t)kDecWarps * kWarpRegion;  // lo, hi, soff [n] u64 each
+constexpr int kInstrDirect = 1024;      // (launch, object) counters addressed directly (launch * n_obj + obj)
+constexpr size_t kOffIdir = kOffWarp + (size_t)kDecWarps * kWarpRegion;  // [kInstrDirect] u64: instrs | mis << 32
+constexpr size_t kOffObj = kOffIdir + kInstrDirect * sizeof(ull);       // lo, hi, soff [n] u64 each
 static_assert(kOffWarp % 16 == 0 && kWarpRegion % 16 == 0, "128-bit ring loads need 16-byte alignment");
 struct Smem {
-  ull *lo, *hi, *soff, *ival, *pc;
+  ull *lo, *hi, *soff, *ival, *pc, *idir;
   unsigned char* warp;  // [kDecWarps][kWarpRegion]
   uint32_t* ikey;
 };
@@ -255,6 +228,7 @@ __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs
   m.pc = reinterpret_cast<ull*>(smem + kOffPc);
   m.ikey = reinterpret_cast<uint32_t*>(smem + kOffIkey);
   m.warp = smem + kOffWarp;
+  m.idir = reinterpret_cast<ull*>(smem + kOffIdir);
   m.lo = reinterpret_cast<ull*>(smem + kOffObj);
   m.hi = m.lo + nobj;
   m.soff = m.hi + nobj;
@@ -269,12 +243,30 @@ __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs
     m.ival[2 * i + 1] = 0;
   }
   for (int i = threadIdx.x; i < kPcSlots; i += blockDim.x) m.pc[i] = ((ull)0xFFFFFFFFu << 32) | kPcNone;
+  for (int i = threadIdx.x; i < kInstrDirect; i += blockDim.x) m.idir[i] = 0;
   __syncthreads();
   return m;
 }
 
+// one warp instruction of (launch, object) key1 - 1 = launch * n_obj + obj
+// (warp-uniform arguments): lane 0 adds 1 | mis << 32 to the block's direct
+// table (one shared atomic; a block counts < 2^32 instructions per ingest
+// call), or, for ids past the table, to the hashed one
+__device__ __forceinline__ void instr_add(const Smem& m, uint32_t key1, bool mis, ull* g, int lane) {
+  if (lane != 0) return;
+  if (key1 - 1u < (uint32_t)kInstrDirect) atomicAdd(&m.idir[key1 - 1u], 1ull | ((ull)mis << 32));
+  else instr_flush(m.ikey, m.ival, g, key1, 1u, mis ? 1u : 0u);
+}
+
 __device__ __forceinline__ void smem_flush_instr(const Smem& m, ull* g) {
   __syncthreads();
+  for (int i = threadIdx.x; i < kInstrDirect; i += blockDim.x) {
+    const ull v = m.idir[i];
+    if (v) {
+      atomicAdd(&g[2 * i], v & 0xFFFFFFFFull);
+      if (v >> 32) atomicAdd(&g[2 * i + 1], v >> 32);
+    }
+  }
   for (int i = threadIdx.x; i < kInstrSlots; i += blockDim.x) {
     const uint32_t k = m.ikey[i];
     if (k) {

@@ -61,8 +61,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
   const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(ring + lane);
 
-  InstrCache icache;
-  icache.init();
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
   WinEnt e0, e1;
@@ -244,8 +242,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
           const uint32_t mx = __reduce_max_sync(FULL, act ? x : 0u);
           span = (ull)(mx - mn) + size;
         }
-        icache.add(launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, sm.ikey, sm.ival,
-                   a.instr_ctr, lane);
+        instr_add(sm, launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, a.instr_ctr, lane);
       }
       off = offn;
     }
@@ -255,7 +252,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
   STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
   st.flush(gkeys, gnk, lane);
-  icache.drain(sm.ikey, sm.ival, a.instr_ctr, lane);
   if (cur_launch != 0xFFFFFFFFu) {
     const uint32_t um = __reduce_add_sync(FULL, lane_unmapped), mm = __reduce_add_sync(FULL, lane_mapped);
     if (lane == 0 && (um | mm)) {

@@ -45,8 +45,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
   ull* const gnk = &a.ctr->n_keys;
   Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0, a.seg_cnt, 8 + a.kl.P + a.kl.L + a.kl.W};
 
-  InstrCache icache;
-  icache.init();
   uint32_t lane_mapped = 0, lane_unmapped = 0;
   uint32_t cur_launch = 0xFFFFFFFFu;
   WinEnt e0, e1;
@@ -200,15 +198,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
       const uint32_t mn = __reduce_min_sync(FULL, act ? x : 0xFFFFFFFFu);
       const uint32_t mx = __reduce_max_sync(FULL, act ? x : 0u);
       const ull span = (ull)(mx - mn) + size;
-      icache.add(launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, sm.ikey, sm.ival, a.instr_ctr,
-                 lane);
+      instr_add(sm, launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, a.instr_ctr, lane);
     }
   }
   }
   STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
   STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
   st.flush(gkeys, gnk, lane);
-  icache.drain(sm.ikey, sm.ival, a.instr_ctr, lane);
   if (cur_launch != 0xFFFFFFFFu) {
     const uint32_t um = __reduce_add_sync(FULL, lane_unmapped), mm = __reduce_add_sync(FULL, lane_mapped);
     if (lane == 0 && (um | mm)) {

@@ -428,3 +428,85 @@ def test_many_objects(dedup):
     orc.ingest_warp(recs)
     orc.build()
     compare(orc, th, tw)
+
+
+@pytest.mark.parametrize("dedup", [1, 2, 3])
+def test_synthetic_medium_all_outputs(dedup):
+    """BJ configs[4]'s generator (64 objects, 8 launches, the 8 motifs) at a size
+    the oracle finishes in seconds: every heat-map row, histogram, per-pc row,
+    indicator and stat, bit-exact, in every dedup mode."""
+    from paper_2507_18729_b200 import Thermo
+    t = tg.synthetic(n_objects=64, n_launches=8, warps_per_launch=256, records_per_warp=256, size_shift=14)
+    orc = oracle.run([o[:4] for o in t.objects], t.calls())
+    th = Thermo(max_launches=8, max_warps_per_launch=256, max_pcs=64, dedup=dedup)
+    th.register_objects(t.objects)
+    th.ingest(t.records.cuda())
+    th.build(BOTH)
+    compare(orc, th, t)
+    th.build(BOTH, 5)  # one launch (the paper's per-kernel map, G2)
+    o5 = oracle.run([o[:4] for o in t.objects], t.calls(), 5)
+    compare(o5, th, t)
+
+
+def _touched(objects, recs, sectors_per_obj, rng):
+    """Pick sectors the trace touches (and a few it may not), per object."""
+    r = recs.view(torch.int32)
+    addr = (r[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((r[:, 1].to(torch.int64) & 0xFFFF) << 32)
+    sec = torch.unique(addr[:: max(1, recs.shape[0] // (1 << 22))] >> 5).cpu().numpy()
+    oi, se = [], []
+    for k, ob in enumerate(objects):
+        lo, ns = ob[0] // 32, (ob[1] + 31) // 32
+        mine = sec[(sec >= lo) & (sec < lo + ns)] - lo
+        pick = list(rng.choice(mine, min(len(mine), sectors_per_obj), replace=False)) if len(mine) else []
+        pick += [0, ns - 1, int(rng.integers(ns))]
+        pick = sorted(set(int(p) for p in pick))
+        oi += [k] * len(pick)
+        se += pick
+    return np.array(oi), np.array(se, dtype=np.uint64)
+
+
+def test_synthetic_full_size_sampled():
+    """BJ configs[4] at bench size on one GPU (one rank's slice of the 8-GPU job:
+    2^15 warps x 8 launches x 2048 records = 2^29 records over 64 objects of
+    4-512 MB): the oracle on sampled sectors of every object -- only the
+    records touching a sampled sector decide its row, so they are selected on
+    the device and the oracle ingests just those -- plus the histogram
+    invariants (level sums = n_words / n_sectors) on every object."""
+    t = tg.synthetic(warps_per_launch=1 << 15, warp_range=(0, 1 << 15), device="cuda")
+    assert t.n == 1 << 29
+    from paper_2507_18729_b200 import Thermo
+    th = Thermo(max_launches=8, max_warps_per_launch=1 << 15, max_pcs=64)
+    th.register_objects(t.objects)
+    th.ingest(t.records)
+    th.build(BOTH)
+    st = th.stats()
+    assert st["records"] == 1 << 29 and st["invalid"] == 0
+    rng = np.random.default_rng(9)
+    oi, se = _touched(t.objects, t.records, 6, rng)
+    # the records touching a sampled sector (first or last byte in it)
+    abs_sec = torch.tensor([t.objects[o][0] // 32 + int(s) for o, s in zip(oi, se)], device="cuda")
+    keep = []
+    r = t.records
+    for a in range(0, r.shape[0], 1 << 26):
+        c = r[a:a + (1 << 26)]
+        addr = (c[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((c[:, 1].to(torch.int64) & 0xFFFF) << 32)
+        size = torch.ones_like(addr) << ((c[:, 1].to(torch.int64) >> 16) & 7)
+        m = torch.isin(addr >> 5, abs_sec) | torch.isin((addr + size - 1) >> 5, abs_sec)
+        keep.append(c[m].cpu())
+    sub = torch.cat(keep)
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.restrict(oi, se)
+    orc.ingest(sub)
+    orc.build()
+    ref = orc.sample(oi, se)
+    for k, ob in enumerate(t.objects):
+        oid = ob[3]
+        assert th.histogram(oid, WORD).sum() == (ob[1] + 3) // 4
+        assert th.histogram(oid, SECTOR).sum() == (ob[1] + 31) // 32
+        rows = [i for i in range(len(oi)) if oi[i] == k]
+        if not rows:
+            continue
+        both = th.heatmap(oid, BOTH).reshape(-1, 9)
+        for i in rows:
+            assert np.array_equal(both[int(se[i])], ref[i]), (k, int(se[i]), both[int(se[i])], ref[i])
+    assert sum(int((ref[:, 8] > 0).sum()) for _ in [0]) > 64  # the sample hits touched sectors

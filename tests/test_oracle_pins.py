@@ -508,3 +508,35 @@ def test_runs_closed_forms_and_round_trip():
             assert np.array_equal(rows, dense)
             assert (st == np.concatenate([[0], np.cumsum(ct)[:-1]])).all()
             assert all((tp[i] != tp[i + 1]).any() for i in range(len(tp) - 1))  # maximal
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_restricted_sample_equals_brute_force(seed):
+    """Sampled mode (the full-size parity tests): the oracle restricted to a
+    set of sectors builds only their rows; each equals the brute-force count
+    (a sector's row depends only on the records touching it), with and
+    without a launch filter, and unsampled sectors read 0."""
+    t = tg.random_trace(n=8000, seed=seed, n_warps=200, n_launches=3)
+    rng = np.random.default_rng(seed)
+    oi, se = [], []
+    for k, ob in enumerate(t.objects):
+        ns = (ob[1] + 31) // 32
+        pick = rng.choice(ns, min(ns, 12), replace=False)
+        oi += [k] * len(pick)
+        se += list(pick)
+    oi, se = np.array(oi), np.array(se, dtype=np.uint64)
+    for lf in (None, 2):
+        o = oracle.Oracle(objs(t))
+        o.restrict(oi, se)
+        o.ingest(t.records)
+        o.build(oracle.ALL_LAUNCHES if lf is None else lf)
+        rows = o.sample(oi, se)
+        wc, sc = R.brute_counts(objs(t), t.records, lf)
+        for row, k, s in zip(rows, oi, se):
+            s = int(s)
+            nw = len(wc[k])
+            exp = [int(wc[k][8 * s + b]) if 8 * s + b < nw else 0 for b in range(8)] + [int(sc[k][s])]
+            assert list(row) == exp, (k, s)
+        other = o.sample(np.array([0]), np.array([int(s) for s in range(100) if (0, s) not in set(zip(oi, se))][:1],
+                                                 dtype=np.uint64))
+        assert (other == 0).all()

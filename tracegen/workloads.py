@@ -510,12 +510,16 @@ def random_warp_trace(n_instr=3000, seed=1, n_objects=5, n_warps=60, n_launches=
 # synthetic multi-kernel trace over 64 objects
 # --------------------------------------------------------------------------
 def synthetic(n_objects=64, n_launches=8, warps_per_launch=1 << 18, records_per_warp=2048,
-              seed=0x5EED0005, device="cpu", size_shift=22, launch_lo=0, launch_hi=None) -> Trace:
+              seed=0x5EED0005, device="cpu", size_shift=22, launch_lo=0, launch_hi=None,
+              warp_range=None) -> Trace:
     """Each launch touches 8 objects with one motif each (coalesced 4 B, float4,
     broadcast-hot, column-strided, stencil-halo, Zipf-like gather, +16 B
     misaligned stream, random atomics); object sizes 2^(size_shift + h mod 8) B.
     Warps issue records_per_warp/32 instructions cycling over the 8 motifs.
-    Randomness: splitmix64 keyed by (seed, launch, warp, instruction, lane)."""
+    Randomness: splitmix64 keyed by (seed, launch, warp, instruction, lane).
+    warp_range=(lo, hi): only warps [lo, hi) of every launch (a rank's slice
+    of the job, or a bounded sample); records are written into one
+    preallocated tensor, so the peak is the trace plus one 2^24-record chunk."""
     dev = torch.device(device)
     sizes, bases, objects = [], [], []
     base = 0x600000000000
@@ -531,12 +535,14 @@ def synthetic(n_objects=64, n_launches=8, warps_per_launch=1 << 18, records_per_
     ipw = records_per_warp // 32
     lane = _lanes(dev)
     launch_hi = n_launches if launch_hi is None else launch_hi
-    parts = []
+    wlo, whi = (0, warps_per_launch) if warp_range is None else warp_range
+    out = torch.empty(((launch_hi - launch_lo) * (whi - wlo) * records_per_warp, 4), dtype=torch.int32, device=dev)
+    pos = 0
     wchunk = max(1, (1 << 24) // records_per_warp)
     for L in range(launch_lo, launch_hi):
         objs_L = torch.tensor([(L * 8 + m * 9) % n_objects for m in range(8)], dtype=torch.int64, device=dev)
-        for w0 in range(0, warps_per_launch, wchunk):
-            w = torch.arange(w0, min(warps_per_launch, w0 + wchunk), dtype=torch.int64, device=dev)
+        for w0 in range(wlo, whi, wchunk):
+            w = torch.arange(w0, min(whi, w0 + wchunk), dtype=torch.int64, device=dev)
             W = w.shape[0]
             t = torch.arange(ipw, dtype=torch.int64, device=dev)
             motif = (t % 8)[None, :, None].expand(W, ipw, 32)
@@ -567,9 +573,11 @@ def synthetic(n_objects=64, n_launches=8, warps_per_launch=1 << 18, records_per_
             first[:, :, 0] = 1
             rec = pack_records(addr.reshape(-1), l2s.reshape(-1), kind.reshape(-1), SPACE_GLOBAL,
                                first.reshape(-1), gw.expand(W, ipw, 32).reshape(-1), pc.reshape(-1), L)
-            parts.append(rec)
-    return Trace(f"synthetic-{n_objects}x{n_launches}", objects, _concat(parts, dev),
-                 meta=dict(launches=n_launches, warps=warps_per_launch))
+            out[pos:pos + rec.shape[0]] = rec
+            pos += rec.shape[0]
+            del rec, addr, off, rnd, r31
+    return Trace(f"synthetic-{n_objects}x{n_launches}", objects, out,
+                 meta=dict(launches=n_launches, warps=warps_per_launch, pcs=8 * n_launches))
 
 
 WORKLOADS = {
