@@ -117,8 +117,8 @@ typedef enum {
  *   HASH     open-addressing hash set in HBM
  *   SEGMENT  counting sort by sector + per-chunk shared-memory dedup; the
  *            keys of sectors holding >= 2048 keys take a hash-set side path
- *   AUTO     SEGMENT up to 2^25 registered sectors, HASH beyond (chosen by
- *            measurement) */
+ *   AUTO     SEGMENT up to 2^30 registered sectors (its workspace is 28 B per
+ *            sector), HASH beyond (chosen by measurement) */
 typedef enum {
   THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2, THERMO_DEDUP_SEGMENT = 3
 } thermo_dedup;

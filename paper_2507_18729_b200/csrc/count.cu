@@ -194,6 +194,9 @@ __device__ __forceinline__ void agg_add(uint32_t* s_hist, ull* g_hist, bool use_
   }
 }
 
+// a6 per-object histograms over the dense rows, one sector per lane (the 8
+// word counts as two 16-byte loads, a warp reads 1 KB contiguous); the
+// object is looked up once per warp while its 32 sectors stay inside it.
 __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __restrict__ wc,
                                                           const uint32_t* __restrict__ sc, const ull* __restrict__ soff,
                                                           const ull* __restrict__ nwords, uint32_t nobj,
@@ -205,19 +208,38 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
     for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
   }
-  const ull stride = (ull)gridDim.x * blockDim.x;
-  const ull nthreads = (total + 255) / 256 * 256;
-  for (ull g = (ull)blockIdx.x * blockDim.x + threadIdx.x; g < nthreads; g += stride) {
+  const uint32_t lane = threadIdx.x & 31;
+  const ull wstride = (ull)gridDim.x * blockDim.x;
+  uint32_t o0 = 0;
+  ull olo = 1, ohi = 0;  // sectors [olo, ohi) of object o0 (the last one looked up)
+  for (ull g0 = ((ull)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); g0 < total; g0 += wstride) {
+    const ull g = g0 + lane;
     const bool in = g < total && shard_owner(g, nranks) == rank;
-    uint32_t o = in ? obj_of_sector(soff, nobj, g) : 0;
+    const ull glast = (g0 + 31 < total ? g0 + 31 : total - 1);
+    // warp-uniform object when the first and last sector of the 32 agree
+    if (g0 < olo || g0 >= ohi) {  // (uniform) search only when leaving the object
+      o0 = obj_of_sector(soff, nobj, g0);
+      olo = soff[o0];
+      ohi = soff[o0 + 1];
+    }
+    const bool uni = glast < ohi;
+    const uint32_t o = uni ? o0 : (g < total ? obj_of_sector(soff, nobj, g) : 0u);
+    uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
+    uint32_t c = 0;
+    if (in) {
+      lo = reinterpret_cast<const uint4*>(wc + 8 * g)[0];
+      hi = reinterpret_cast<const uint4*>(wc + 8 * g)[1];
+      c = sc[g];
+    }
+    const ull nwo = nwords[o];
     const ull wl0 = in ? (g - soff[o]) * 8 : 0;
-    const ull nwo = in ? nwords[o] : 0;
-    // sector bin
-    agg_add(s_hist, hist, use_smem, (o * 2 + 1) * kLevels + (in ? level_of(sc[g]) : 0), in);
+    const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    // bins aggregated over the warp's lanes (match_any), one atomic per distinct bin
+    agg_add(s_hist, hist, use_smem, (o * 2 + 1) * kLevels + (in ? level_of(c) : 0), in);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const bool hw = in && wl0 + b < nwo;
-      agg_add(s_hist, hist, use_smem, (o * 2) * kLevels + (hw ? level_of(wc[8 * g + b]) : 0), hw);
+      agg_add(s_hist, hist, use_smem, (o * 2) * kLevels + (hw ? level_of(x[b]) : 0), hw);
     }
   }
   if (use_smem) {

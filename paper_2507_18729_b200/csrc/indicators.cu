@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   const ull nw = a.obj_nwords[o];
   const thermo_params& P = a.prm;
   const ull cand = mode ? a.ind[(ull)o * kIndFields + F_CAND] : 0;
+  // no surviving vote: no gap holds a majority, the verify count is not needed
+  if (mode == 1 && a.ind[(ull)o * kIndFields + F_CANDCNT] == 0) return;
 
   ull T = 0, TW = 0, hot = 0, fs = 0, sumx = 0, le1 = 0, maxsec = 0, verify = 0;
   u128 sumx2 = 0;
@@ -109,12 +111,17 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     const ull g = gs + i;
     if (g >= g1) break;
     const uint32_t c = a.sector_cnt[g];
+    // the sector's 8 word counts: two 16-byte loads (rows are 32-byte aligned)
+    const uint4 lo = reinterpret_cast<const uint4*>(a.word_cnt + 8 * g)[0];
+    const uint4 hi = reinterpret_cast<const uint4*>(a.word_cnt + 8 * g)[1];
+    const uint32_t xs[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     ull mw = 0;
     const ull wl0 = (g - soff) * 8;
+#pragma unroll
     for (int b = 0; b < 8; ++b) {
       const ull wl = wl0 + b;
       if (wl >= nw) break;
-      const uint32_t x = a.word_cnt[8 * g + b];
+      const uint32_t x = xs[b];
       mw = x > mw ? x : mw;
       if (x == 0) continue;
       ++TW;

@@ -98,18 +98,22 @@ __global__ void seg_scan_blocks(ull* bsum, ull nb, ull* total) {
   if (threadIdx.x == 0) *total = carry;
 }
 
-// off[j] = exclusive prefix of cnt; cur[j] = off[j] (scatter cursors)
+// off[j] = exclusive prefix of cnt; dst[j] = the chunk sector j's keys go to
+// (the one its segment starts in; ~0 for a big sector)
 __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum,
-                               ull* __restrict__ off) {
+                               ull* __restrict__ off, uint32_t* __restrict__ dst) {
   __shared__ ull ws[kSegWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
   uint32_t v[8];
+  bool bg[8];
   ull t = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
-    v[k] = j < n ? seg_len(in[j]) : 0u;
+    const uint32_t c = j < n ? in[j] : 0u;
+    v[k] = seg_len(c);
+    bg[k] = c >= (uint32_t)kSegCap;
     t += v[k];
   }
   ull incl = t;
@@ -125,7 +129,10 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
-    if (j < n) off[j] = pre;
+    if (j < n) {
+      off[j] = pre;
+      dst[j] = bg[k] ? 0xFFFFFFFFu : (uint32_t)(pre / (ull)kSegCap);
+    }
     pre += v[k];
   }
 }
@@ -135,37 +142,37 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 // atomics' latency (contended cursors of hot sectors), not bandwidth, bounds it
 constexpr int kScatterPer = 8;
 __global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
-                                                          const ull* __restrict__ off, ull* __restrict__ cur,
-                                                          ull* __restrict__ out, const uint32_t* __restrict__ cnt,
-                                                          ull* __restrict__ big, ull* __restrict__ nbig_ctr) {
+                                                          const uint32_t* __restrict__ dst, ull* __restrict__ cur,
+                                                          ull* __restrict__ out, ull* __restrict__ big,
+                                                          ull* __restrict__ nbig_ctr) {
   const int lane = threadIdx.x & 31;
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const ull tile = (ull)blockDim.x * kScatterPer;
   for (ull t0 = (ull)blockIdx.x * tile; t0 < n; t0 += (ull)gridDim.x * tile) {
     ull k[kScatterPer], pos[kScatterPer];
+    uint32_t d[kScatterPer];
     const ull i0 = t0 + threadIdx.x;
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) k[u] = i0 + (ull)u * blockDim.x < n ? keys[i0 + (ull)u * blockDim.x] : 0;
-    bool isbig[kScatterPer];
+    // one 4-byte read per key: the key's chunk (chunk cursors stay
+    // cache-resident however many sectors there are) or ~0 for a big sector
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) d[u] = i0 + (ull)u * blockDim.x < n ? dst[key_g(k[u], kl)] : 0xFFFFFFFEu;
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u)
+      if (d[u] < 0xFFFFFFFEu) pos[u] = atomicAdd(&cur[d[u]], 1ull);
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
-      const bool in = i0 + (ull)u * blockDim.x < n;
-      isbig[u] = in && cnt[key_g(k[u], kl)] >= (uint32_t)kSegCap;
-      // the key's chunk = where its sector's segment starts; chunk cursors stay
-      // cache-resident however many sectors there are
-      if (in && !isbig[u]) pos[u] = atomicAdd(&cur[off[key_g(k[u], kl)] / (ull)kSegCap], 1ull);
-    }
-#pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) {
-      const unsigned bb = __ballot_sync(GFULL, isbig[u]);  // big keys: one append per warp
+      const bool isbig = d[u] == 0xFFFFFFFFu;
+      const unsigned bb = __ballot_sync(GFULL, isbig);  // big keys: one append per warp
       if (bb) {
         ull b0 = 0;
         if (lane == __ffs(bb) - 1) b0 = atomicAdd(nbig_ctr, (ull)__popc(bb));
         b0 = __shfl_sync(GFULL, b0, __ffs(bb) - 1);
-        if (isbig[u]) big[b0 + __popc(bb & lt)] = k[u];
+        if (isbig) big[b0 + __popc(bb & lt)] = k[u];
       }
-      if (i0 + (ull)u * blockDim.x < n && !isbig[u]) out[pos[u]] = k[u];
+      if (d[u] < 0xFFFFFFFEu) out[pos[u]] = k[u];
     }
   }
 }
@@ -384,13 +391,15 @@ ull segment_chunk_cap() { return kSegCap; }
 cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
   cudaError_t e;
   if (ws.cap_sec < nsec + 1) {
-    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum); cudaFree(ws.cs0);
+    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum); cudaFree(ws.cs0); cudaFree(ws.dst);
     ws.cnt = nullptr; ws.off = ws.cur = ws.bsum = ws.cs0 = nullptr;
+    ws.dst = nullptr;
     ws.cap_sec = 0;
     if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
     if ((e = cudaMalloc(&ws.off, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cs0, (nsec + 2) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.dst, (nsec + 1) * sizeof(uint32_t)))) return e;
     if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
     ws.cap_sec = nsec + 1;
   }
@@ -415,7 +424,7 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
   seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc,
                                                        reinterpret_cast<ull*>(ws.maxc) + 1);
   seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
-  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off);
+  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.dst);
   ws.launches += 3;
   ull hv[2];
   if ((e = cudaMemcpyAsync(hv, ws.maxc, 2 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
@@ -433,7 +442,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
     const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
     seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
-    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.off, ws.cur, out, ws.cnt, big,
+    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.dst, ws.cur, out, big,
                                             reinterpret_cast<ull*>(ws.maxc) + 2);
   }
   const size_t smem = segment_chunk_smem();

@@ -506,7 +506,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
                   ctx->d_table, ctx->d_pctable, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
-                  ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->d_stage[0],
+                  ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
                   ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr, ctx->d_wstage[0], ctx->d_wstage[1]};
   for (void* b : bufs) dfree(b);
@@ -651,7 +651,10 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
   ctx->records = 0;
   ctx->state = 1;
   ctx->hist_valid = false;
-  ctx->seg_counted = !ctx->comm && ctx->S_tot <= (1ull << 25) &&
+  // the decoder counts keys per sector as it flushes them (one RED per key,
+  // hidden in the issue-bound decode; measured cheaper than a histogram pass
+  // over the keys at every sector count: synthetic 2^28 sectors 55.9 -> 52.7 ms)
+  ctx->seg_counted = !ctx->comm && ctx->S_tot <= (1ull << 30) &&
                      (ctx->cfg.dedup == THERMO_DEDUP_AUTO || ctx->cfg.dedup == THERMO_DEDUP_SEGMENT);
   if (ctx->seg_counted) CK(cudaMemsetAsync(ctx->seg.cnt, 0, (ctx->S_tot + 1) * sizeof(uint32_t), ctx->stream));
   if (ctx->d_acc) CK(cudaMemsetAsync(ctx->d_acc, 0, 8 * ctx->S_tot * sizeof(uint32_t), ctx->stream));
@@ -869,13 +872,13 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
-  // AUTO, chosen by measurement: the SEGMENT counting sort keeps
-  // its per-sector cursors cache-resident up to ~2^25 sectors (SGEMM 5.3 ms vs
-  // HASH 6.3 ms; stencil 2^24 sectors 48 vs 62 ms); beyond, its scatter
-  // degenerates into random HBM atomics and the hash set wins (SpMV s=24,
-  // 2^26 sectors: 170 vs 228 ms)
+  // AUTO, chosen by measurement: SEGMENT (counting sort by
+  // sector + shared-memory hash set per chunk) beats the HBM hash set on every
+  // BJ config (SGEMM 4.9 vs 6.3 ms; stencil 2^24 sectors 26 vs 62 ms; SpMV
+  // 2^26 sectors 127 vs 170 ms; synthetic 2^28 sectors 60 vs 82 ms); its
+  // per-sector workspace (28 B/sector) decides the limit
   uint32_t mode = ctx->cfg.dedup;
-  if (mode == THERMO_DEDUP_AUTO) mode = ctx->S_tot <= (1ull << 25) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
+  if (mode == THERMO_DEDUP_AUTO) mode = ctx->S_tot <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
   bool pc_done = false;

@@ -128,6 +128,7 @@ struct SegWorkspace {
   ull* off = nullptr;        // [S_tot + 1] exclusive prefix (off[S_tot] = total)
   ull* cur = nullptr;        // [S_tot + 1] scatter cursors (one per chunk)
   ull* cs0 = nullptr;        // [S_tot + 2] first sector of each chunk (+ end)
+  uint32_t* dst = nullptr;   // [S_tot + 1] chunk of each sector's keys (~0: a big sector's, hash path)
   ull* bsum = nullptr;       // scan block sums
   uint32_t* maxc = nullptr;  // [4 u64]: max keys in one sector, big-sector keys, big cursor
   ull cap_sec = 0;
