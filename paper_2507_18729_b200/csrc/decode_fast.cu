@@ -60,19 +60,21 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   Stage st{reinterpret_cast<ull*>(sm.warp + wib * kWarpRegion), 0, a.seg_cnt, 8 + a.kl.P + a.kl.L + a.kl.W};
   uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
   const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(ring + lane);
+  // warp-uniform caches kept in shared memory (registers are the kernel's
+  // occupancy limit): window entries e = 0, 1 as {H, blo, bn, sbase},
+  // {tail_s, tail_m, oid, -} at wc[2e], wc[2e + 1]; site -> pc id cache
+  // {site0, id0, site1, id1} at wc[4]
+  uint4* const wc = ring + kRingChunks * 32;
+  if (lane == 0) {
+    wc[0] = wc[2] = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+    wc[1] = wc[3] = make_uint4(1, 0xFFu, 0xFFFFFFFFu, 0);
+    wc[4] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
+  }
+  __syncwarp();
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
-  WinEnt e0, e1;
-  e0.H = e1.H = 0xFFFFFFFFu;
-  e0.blo = e1.blo = 0;
-  e0.bn = e1.bn = 0;
-  e0.sbase = e1.sbase = 0;
-  e0.tail_s = e1.tail_s = 1;
-  e0.tail_m = e1.tail_m = 0xFFu;
-  e0.oid = e1.oid = -1;
   bool last1 = false;
-  uint32_t ps0 = 0xFFFFFFFFu, pi0 = 0, ps1 = 0xFFFFFFFFu, pi1 = 0;  // site -> pc id cache
   // this lane's two most recent dedup entries: (pc id << 32 | g) -> mask
   ull c0 = 0, c1 = 0;
   uint32_t m0 = 0, m1 = 0;
@@ -144,19 +146,27 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       const uint32_t H = ((y0 >> 5) & 0x30000u) | (y0 & 0xFFFFu);  // space << 16 | addr[32,48)
       const uint32_t xs = x & ~31u;
       const uint32_t xs0 = __shfl_sync(FULL, xs, 0);
-      const bool h0 = win_has(e0, H, xs0), h1 = win_has(e1, H, xs0);
+      const uint4 A0 = wc[0], A1 = wc[2];
+      const bool h0 = (A0.x == H) & (xs0 - A0.y < A0.z), h1 = (A1.x == H) & (xs0 - A1.y < A1.z);
+      uint32_t blo, bn, sbase, tail_s, tail_m;
+      int oid0;
       if (!(h0 | h1)) {  // uniform miss: replace the entry not used last
         const WinEnt ne = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs0);
-        if (last1) { e0 = ne; last1 = false; } else { e1 = ne; last1 = true; }
+        const int e = last1 ? 0 : 1;
+        if (lane == 0) {
+          wc[2 * e] = make_uint4(ne.H, ne.blo, ne.bn, ne.sbase);
+          wc[2 * e + 1] = make_uint4(ne.tail_s, ne.tail_m, (uint32_t)ne.oid, 0);
+        }
+        last1 = e == 1;
+        blo = ne.blo; bn = ne.bn; sbase = ne.sbase; tail_s = ne.tail_s; tail_m = ne.tail_m; oid0 = ne.oid;
       } else {
         last1 = !h0;
+        const uint4 A = last1 ? A1 : A0;
+        const uint4 B = wc[last1 ? 3 : 1];
+        blo = A.y; bn = A.z; sbase = A.w; tail_s = B.x; tail_m = B.y; oid0 = (int)B.z;
       }
-      uint32_t blo = last1 ? e1.blo : e0.blo;
-      uint32_t sbase = last1 ? e1.sbase : e0.sbase;
-      uint32_t tail_s = last1 ? e1.tail_s : e0.tail_s, tail_m = last1 ? e1.tail_m : e0.tail_m;
-      const int oid0 = last1 ? e1.oid : e0.oid;
       int oid = oid0;
-      const bool inw = xs - blo < (last1 ? e1.bn : e0.bn);
+      const bool inw = xs - blo < bn;
       if (__ballot_sync(FULL, act & !inw)) {  // lanes outside lane 0's interval (rare)
         if (act & !inw) {
           const WinEnt le = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs);
@@ -199,17 +209,20 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         }
         uint32_t pcid = 0;
         if (a.track_pc) {
-          if (w0 == ps0) {
-            pcid = pi0;
-          } else if (w0 == ps1) {
-            pcid = pi1; ps1 = ps0; pi1 = pi0; ps0 = w0; pi0 = pcid;
+          const uint4 pcc = wc[4];  // two most recent sites (uniform)
+          if (w0 == pcc.x) {
+            pcid = pcc.y;
+          } else if (w0 == pcc.z) {
+            pcid = pcc.w;
           } else {
             uint32_t id = 0;
-            if (lane == 0) id = pc_lookup(sm.pc, a.pcmap, w0, a.ctr);
+            if (lane == 0) {
+              id = pc_lookup(sm.pc, a.pcmap, w0, a.ctr);
+              id = id < a.pcmap.max_pcs ? id : 0u;  // overflow is reported at build (ERANGE)
+              wc[4] = make_uint4(w0, id, pcc.x, pcc.y);
+            }
             pcid = __shfl_sync(FULL, id, 0);
-            ps1 = ps0; pi1 = pi0; ps0 = w0; pi0 = pcid;
           }
-          pcid = pcid < a.pcmap.max_pcs ? pcid : 0u;  // overflow is reported at build (ERANGE)
         }
         // two-entry LRU of (pc id, sector) -> mask; entry 0 is the most recent
         const ull ck = ((ull)pcid << 32) | g;
@@ -284,7 +297,11 @@ void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
   const int feat = (a.acc ? 1 : 0) | (a.block_warps ? 2 : 0);
   static const int minb = getenv("THERMO_DEC_MINB") ? atoi(getenv("THERMO_DEC_MINB")) : 3;
   switch (feat) {
-    case 0: if (minb == 4) launch_decode_t<4, 0>(a, num_sms, s, smem); else launch_decode_t<3, 0>(a, num_sms, s, smem); break;
+    case 0:
+      if (minb == 4) launch_decode_t<4, 0>(a, num_sms, s, smem);
+      else if (minb == 2) launch_decode_t<2, 0>(a, num_sms, s, smem);
+      else launch_decode_t<3, 0>(a, num_sms, s, smem);
+      break;
     case 1: launch_decode_t<3, 1>(a, num_sms, s, smem); break;
     case 2: launch_decode_t<3, 2>(a, num_sms, s, smem); break;
     default: launch_decode_t<3, 3>(a, num_sms, s, smem); break;
