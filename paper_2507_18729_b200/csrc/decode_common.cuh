@@ -136,9 +136,11 @@ struct Stage {
   do {                                                                    \
     const bool has_ = (HAS);                                              \
     const unsigned b_ = __ballot_sync(FULL, has_);                        \
-    if (has_) (st).s[(st).cnt + __popc(b_ & lane_lt)] = (KEY);            \
-    (st).cnt += __popc(b_);                                               \
-    if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane);   \
+    if (b_) {                                                             \
+      if (has_) (st).s[(st).cnt + __popc(b_ & lane_lt)] = (KEY);          \
+      (st).cnt += __popc(b_);                                             \
+      if ((st).cnt > (uint32_t)kFlushAt) (st).flush((gbuf), (gcnt), lane); \
+    }                                                                     \
   } while (0)
 
 // (launch, pc) -> dense pc id; inserts on first sight (G11)
@@ -258,6 +260,27 @@ __device__ __forceinline__ void instr_add(const Smem& m, uint32_t key1, bool mis
   if (key1 - 1u < (uint32_t)kInstrDirect) atomicAdd(&m.idir[key1 - 1u], 1ull | ((ull)mis << 32));
   else instr_flush(m.ikey, m.ival, g, key1, 1u, mis ? 1u : 0u);
 }
+
+// (launch, object) ids k < 32 counted in registers, lane k holding id k: one
+// predicated add per instruction instead of instr_add's 64-bit shared atomic
+// (a CAS loop on sm_100a); flushed with global atomics when the warp ends (a
+// warp counts < 2^32 instructions per ingest call)
+struct InstrRegs {
+  uint32_t n = 0, m = 0;
+  __device__ __forceinline__ void add(const Smem& sm, uint32_t k, bool mis, ull* g, int lane) {
+    if (k < 32u) {
+      const bool me = (uint32_t)lane == k;
+      n += me;
+      m += me & mis;
+    } else {
+      instr_add(sm, k + 1u, mis, g, lane);
+    }
+  }
+  __device__ __forceinline__ void flush(ull* g, int lane) {
+    if (n) atomicAdd(&g[2 * lane], (ull)n);
+    if (m) atomicAdd(&g[2 * lane + 1], (ull)m);
+  }
+};
 
 __device__ __forceinline__ void smem_flush_instr(const Smem& m, ull* g) {
   __syncthreads();

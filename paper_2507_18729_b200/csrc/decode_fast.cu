@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
+  InstrRegs ir;  // (launch, object) instruction counters for ids < 32
   bool last1 = false;
   // this lane's two most recent dedup entries: (pc id << 32 | g) -> mask
   ull c0 = 0, c1 = 0;
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
           const uint32_t mx = __reduce_max_sync(FULL, act ? x : 0u);
           span = (ull)(mx - mn) + size;
         }
-        instr_add(sm, launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, a.instr_ctr, lane);
+        ir.add(sm, launch0 * nobj + (uint32_t)oid0, distinct > (span + 31) / 32, a.instr_ctr, lane);
       }
       off = offn;
     }
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       atomicAdd(&a.launch_ctr[2 * cur_launch + 1], (ull)mm);
     }
   }
+  ir.flush(a.instr_ctr, lane);
   smem_flush_instr(sm, a.instr_ctr);
 }
 

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;
   uint32_t cur_launch = 0xFFFFFFFFu;
+  InstrRegs ir;  // (launch, object) instruction counters for ids < 32
   WinEnt e0, e1;
   e0.H = e1.H = 0xFFFFFFFFu;
   e0.blo = e1.blo = 0;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
       const uint32_t mn = __reduce_min_sync(FULL, act ? x : 0xFFFFFFFFu);
       const uint32_t mx = __reduce_max_sync(FULL, act ? x : 0u);
       const ull span = (ull)(mx - mn) + size;
-      instr_add(sm, launch0 * nobj + (uint32_t)oid0 + 1u, distinct > (span + 31) / 32, a.instr_ctr, lane);
+      ir.add(sm, launch0 * nobj + (uint32_t)oid0, distinct > (span + 31) / 32, a.instr_ctr, lane);
     }
   }
   }
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     }
   }
   if (lane == 0 && lanes_seen) atomicAdd(&wa.spill_ctr[1], lanes_seen);
+  ir.flush(a.instr_ctr, lane);
   smem_flush_instr(sm, a.instr_ctr);
 }
 
