@@ -214,14 +214,15 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
       }
       const bool mis = svalid && i_obj >= 0 && distinct > (mx - mn + 1 + 31) / 32;
       const bool counted = svalid && i_obj >= 0;
-      // one counter update per instruction, in order (warp-uniform loop over the heads)
-      for (unsigned m = hb & __ballot_sync(FULL, counted && lane == s0); m; m &= m - 1) {
-        const int h = __ffs(m) - 1;
-        const int o = __shfl_sync(FULL, i_obj, h);
-        const uint32_t la = __shfl_sync(FULL, i_launch, h);
-        const bool mh = __shfl_sync(FULL, mis, h);
-        instr_add(sm, la * nobj + (uint32_t)o + 1u, mh, a.instr_ctr, lane);
-      }
+      // counter updates aggregated over the view's instructions (lane s0 of
+      // each holds its (launch, object) and misalignment): one update per
+      // distinct (launch, object), by its lowest head lane
+      const bool head = counted && lane == s0;
+      const uint32_t key1 = head ? i_launch * nobj + (uint32_t)i_obj + 1u : 0u;
+      const unsigned peers = __match_any_sync(FULL, key1);
+      const unsigned misb = __ballot_sync(FULL, head && mis);
+      if (head && lane == __ffs(peers) - 1)
+        instr_add_n(sm, key1, (uint32_t)__popc(peers), (uint32_t)__popc(peers & misb), a.instr_ctr);
     }
   }
   st.flush(a.keys, &a.ctr->n_keys, lane);

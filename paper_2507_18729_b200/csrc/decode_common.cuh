@@ -216,11 +216,12 @@ constexpr size_t kOffPc = kOffIval + 2 * kInstrSlots * sizeof(ull);    // [kPcSl
 constexpr size_t kOffIkey = kOffPc + kPcSlots * sizeof(ull);           // [kInstrSlots] u32
 constexpr size_t kOffWarp = (kOffIkey + kInstrSlots * sizeof(uint32_t) + 15) & ~(size_t)15;  // [kDecWarps]
 constexpr int kInstrDirect = 1024;      // (launch, object) counters addressed directly (launch * n_obj + obj)
-constexpr size_t kOffIdir = kOffWarp + (size_t)kDecWarps * kWarpRegion;  // [kInstrDirect] u64: instrs | mis << 32
+constexpr size_t kOffIdir = kOffWarp + (size_t)kDecWarps * kWarpRegion;  // [kInstrDirect][2] u32: instrs, misaligned
 constexpr size_t kOffObj = kOffIdir + kInstrDirect * sizeof(ull);       // lo, hi, soff [n] u64 each
 static_assert(kOffWarp % 16 == 0 && kWarpRegion % 16 == 0, "128-bit ring loads need 16-byte alignment");
 struct Smem {
-  ull *lo, *hi, *soff, *ival, *pc, *idir;
+  ull *lo, *hi, *soff, *ival, *pc;
+  uint32_t* idir;  // [kInstrDirect][2]: instructions, misaligned ones
   unsigned char* warp;  // [kDecWarps][kWarpRegion]
   uint32_t* ikey;
 };
@@ -231,7 +232,7 @@ __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs
   m.pc = reinterpret_cast<ull*>(smem + kOffPc);
   m.ikey = reinterpret_cast<uint32_t*>(smem + kOffIkey);
   m.warp = smem + kOffWarp;
-  m.idir = reinterpret_cast<ull*>(smem + kOffIdir);
+  m.idir = reinterpret_cast<uint32_t*>(smem + kOffIdir);
   m.lo = reinterpret_cast<ull*>(smem + kOffObj);
   m.hi = m.lo + nobj;
   m.soff = m.hi + nobj;
@@ -246,25 +247,33 @@ __device__ __forceinline__ Smem smem_setup(unsigned char* smem, const DecodeArgs
     m.ival[2 * i + 1] = 0;
   }
   for (int i = threadIdx.x; i < kPcSlots; i += blockDim.x) m.pc[i] = ((ull)0xFFFFFFFFu << 32) | kPcNone;
-  for (int i = threadIdx.x; i < kInstrDirect; i += blockDim.x) m.idir[i] = 0;
+  for (int i = threadIdx.x; i < 2 * kInstrDirect; i += blockDim.x) m.idir[i] = 0;
   __syncthreads();
   return m;
 }
 
-// one warp instruction of (launch, object) key1 - 1 = launch * n_obj + obj
-// (warp-uniform arguments): lane 0 adds 1 | mis << 32 to the block's direct
-// table (one shared atomic; a block counts < 2^32 instructions per ingest
-// call), or, for ids past the table, to the hashed one
+// n warp instructions of (launch, object) key1 - 1 = launch * n_obj + obj, nm
+// of them misaligned, from the calling lane: two 32-bit shared atomics in the
+// block's direct table (native; a 64-bit shared atomicAdd is a CAS loop on
+// sm_100a; a block counts < 2^32 instructions per ingest call), or, for ids
+// past the table, the hashed one
+__device__ __forceinline__ void instr_add_n(const Smem& m, uint32_t key1, uint32_t n, uint32_t nm, ull* g) {
+  if (key1 - 1u < (uint32_t)kInstrDirect) {
+    atomicAdd(&m.idir[2 * (key1 - 1u)], n);
+    if (nm) atomicAdd(&m.idir[2 * (key1 - 1u) + 1], nm);
+  } else {
+    instr_flush(m.ikey, m.ival, g, key1, n, nm);
+  }
+}
+// one warp instruction (warp-uniform arguments), counted by lane 0
 __device__ __forceinline__ void instr_add(const Smem& m, uint32_t key1, bool mis, ull* g, int lane) {
-  if (lane != 0) return;
-  if (key1 - 1u < (uint32_t)kInstrDirect) atomicAdd(&m.idir[key1 - 1u], 1ull | ((ull)mis << 32));
-  else instr_flush(m.ikey, m.ival, g, key1, 1u, mis ? 1u : 0u);
+  if (lane == 0) instr_add_n(m, key1, 1u, mis ? 1u : 0u, g);
 }
 
 // (launch, object) ids k < 32 counted in registers, lane k holding id k: one
-// predicated add per instruction instead of instr_add's 64-bit shared atomic
-// (a CAS loop on sm_100a); flushed with global atomics when the warp ends (a
-// warp counts < 2^32 instructions per ingest call)
+// predicated add per instruction instead of a shared atomic; flushed with
+// global atomics when the warp ends (a warp counts < 2^32 instructions per
+// ingest call)
 struct InstrRegs {
   uint32_t n = 0, m = 0;
   __device__ __forceinline__ void add(const Smem& sm, uint32_t k, bool mis, ull* g, int lane) {
@@ -285,11 +294,9 @@ struct InstrRegs {
 __device__ __forceinline__ void smem_flush_instr(const Smem& m, ull* g) {
   __syncthreads();
   for (int i = threadIdx.x; i < kInstrDirect; i += blockDim.x) {
-    const ull v = m.idir[i];
-    if (v) {
-      atomicAdd(&g[2 * i], v & 0xFFFFFFFFull);
-      if (v >> 32) atomicAdd(&g[2 * i + 1], v >> 32);
-    }
+    const uint32_t n = m.idir[2 * i], nm = m.idir[2 * i + 1];
+    if (n) atomicAdd(&g[2 * i], (ull)n);
+    if (nm) atomicAdd(&g[2 * i + 1], (ull)nm);
   }
   for (int i = threadIdx.x; i < kInstrSlots; i += blockDim.x) {
     const uint32_t k = m.ikey[i];
