@@ -159,9 +159,19 @@ __global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict_
     // cache-resident however many sectors there are) or ~0 for a big sector
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) d[u] = i0 + (ull)u * blockDim.x < n ? dst[key_g(k[u], kl)] : 0xFFFFFFFEu;
+    // warp-aggregated cursor atomics: lanes holding keys of the same chunk take
+    // consecutive positions from one atomic by their lowest lane
+    unsigned peers[kScatterPer];
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) peers[u] = __match_any_sync(GFULL, d[u]);
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) {
+      pos[u] = 0;
+      if (d[u] < 0xFFFFFFFEu && lane == __ffs(peers[u]) - 1) pos[u] = atomicAdd(&cur[d[u]], (ull)__popc(peers[u]));
+    }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u)
-      if (d[u] < 0xFFFFFFFEu) pos[u] = atomicAdd(&cur[d[u]], 1ull);
+      pos[u] = __shfl_sync(GFULL, pos[u], __ffs(peers[u]) - 1) + __popc(peers[u] & lt);
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
       const bool isbig = d[u] == 0xFFFFFFFFu;
@@ -227,8 +237,11 @@ __device__ __forceinline__ void bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, 
 constexpr int kHSlots = 5120;  // > 1.25 x the chunk's < 2 * kSegCap keys (typically ~2/3 of that)
 constexpr int kHWin = 1024;    // chunks spanning at most this many sectors count them in shared memory
 constexpr ull kHEmpty = ~0ull;
-// (a new entry appends its slot to `list`, so the scans visit occupied slots only)
-__device__ __forceinline__ void hset_or(ull* tab, uint16_t* list, uint32_t* nlist, ull id, uint32_t m) {
+// insert returns true when the id takes a new slot (*slot); the caller appends
+// new slots to the chunk's list (one atomic per warp), so the scans visit
+// occupied slots only.  The mask lives in the slot's low 32-bit word: the OR
+// is a native 32-bit shared atomic (a 64-bit atomicOr is a CAS loop)
+__device__ __forceinline__ bool hset_or(ull* tab, ull id, uint32_t m, uint32_t& slot) {
   const uint32_t hx = (uint32_t)((id * 0x9E3779B97F4A7C15ull) >> 32);
   uint32_t h = __umulhi(hx, (uint32_t)kHSlots);
   const ull v = (id << 8) | m;
@@ -237,15 +250,50 @@ __device__ __forceinline__ void hset_or(ull* tab, uint16_t* list, uint32_t* nlis
     if (cur == kHEmpty) {
       cur = atomicCAS(&tab[h], kHEmpty, v);
       if (cur == kHEmpty) {
-        list[atomicAdd(nlist, 1u)] = (uint16_t)h;
-        return;
+        slot = h;
+        return true;
       }
     }
     if ((cur >> 8) == id) {
-      if (((uint32_t)cur & m) != m) atomicOr(&tab[h], (ull)m);
-      return;
+      if (((uint32_t)cur & m) != m) atomicOr(reinterpret_cast<uint32_t*>(&tab[h]), m);
+      return false;
     }
     h = h + 1 == (uint32_t)kHSlots ? 0u : h + 1;
+  }
+}
+
+// one insert pass over the chunk's keys seg[k0, k0 + nk): id = (sector - s0) <<
+// A | (key >> B) & M, mask = the key's low 8 bits.  Each warp takes 32 x kIns
+// consecutive keys per iteration, all loads in flight before the inserts
+constexpr int kIns = 4;
+__device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint32_t* nlist, const ull* __restrict__ seg,
+                                                  ull k0, uint32_t nk, ull s0, const KeyLayout& kl, uint32_t filter,
+                                                  uint32_t A, uint32_t B, ull M) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  for (uint32_t wb = (threadIdx.x >> 5) * 32u * kIns; wb < nk; wb += (uint32_t)kSegThreads * kIns) {
+    ull kk[kIns];
+#pragma unroll
+    for (int u = 0; u < kIns; ++u) {
+      const uint32_t i = wb + u * 32u + lane;
+      kk[u] = i < nk ? seg[k0 + i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kIns; ++u) {
+      const ull k = kk[u];
+      bool ok = wb + u * 32u + lane < nk;
+      if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
+      uint32_t slot = 0;
+      const bool nw = ok && hset_or(tab, ((key_g(k, kl) - s0) << A) | ((k >> B) & M), (uint32_t)k & 0xFFu, slot);
+      const unsigned b = __ballot_sync(GFULL, nw);
+      if (b) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(nlist, (uint32_t)__popc(b));
+        base = __shfl_sync(GFULL, base, 0);
+        if (nw) list[base + __popc(b & lt)] = (uint16_t)slot;
+      }
+    }
   }
 }
 
@@ -286,11 +334,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
   __syncthreads();
   // ---- (a) distinct (sector, launch, warp) ----
-  for (uint32_t i = threadIdx.x; i < nk; i += kSegThreads) {
-    const ull k = seg[k0 + i];
-    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
-    hset_or(tab, list, &s_n[0], ((key_g(k, kl) - s0) << LW) | ((k >> RS) & lwmask), (uint32_t)k & 0xFFu);
-  }
+  chunk_insert_pass(tab, list, &s_n[0], seg, k0, nk, s0, kl, filter, LW, RS, lwmask);
   __syncthreads();
   const uint32_t nent = s_n[0];
   for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
@@ -341,11 +385,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
   __syncthreads();
   const ull pmask = (1ull << kl.P) - 1;
-  for (uint32_t i = threadIdx.x; i < nk; i += kSegThreads) {
-    const ull k = seg[k0 + i];
-    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
-    hset_or(tab, list, &s_n[1], ((key_g(k, kl) - s0) << kl.P) | ((k >> 8) & pmask), (uint32_t)k & 0xFFu);
-  }
+  chunk_insert_pass(tab, list, &s_n[1], seg, k0, nk, s0, kl, filter, kl.P, 8, pmask);
   __syncthreads();
   const uint32_t npc = s_n[1];
   for (uint32_t base = threadIdx.x & ~31u; base < npc; base += kSegThreads) {
