@@ -252,8 +252,15 @@ void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s) {
     cudaFuncSetAttribute(decode_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  ull grid = (a.n_ranges + kDecWarps - 1) / kDecWarps;  // the deferred count is read on the device
-  const ull cap = (ull)num_sms * 2;
+  // the deferred count is read on the device: a full persistent grid (the
+  // kernel waits on record loads, so every resident warp helps)
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_general_kernel, kDecWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  ull grid = (a.n_ranges + kDecWarps - 1) / kDecWarps;
+  const ull cap = (ull)num_sms * per_sm;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   decode_general_kernel<<<(unsigned)grid, kDecWarps * 32, smem, s>>>(a);

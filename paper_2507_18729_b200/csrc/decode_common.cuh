@@ -84,10 +84,10 @@ __device__ __forceinline__ void adjacent_merge(ull& prefix, uint32_t& mask, bool
 }
 
 // same on 32-bit sector ids (fast path: launch/warp are uniform)
+// (g < 2^31 where has: the previous lane's g is shuffled as kNoG when it has no key)
 __device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, bool& has, int lane) {
-  const uint32_t pg = __shfl_up_sync(FULL, g, 1);
-  const bool ph = __shfl_up_sync(FULL, has, 1);
-  const bool same = lane > 0 && has && ph && pg == g;
+  const uint32_t pg = __shfl_up_sync(FULL, has ? g : kNoG, 1);
+  const bool same = lane > 0 && has && pg == g;
   const unsigned sb = __ballot_sync(FULL, same);
   if (sb == 0) return;
   const unsigned hb = __ballot_sync(FULL, has);
@@ -208,7 +208,8 @@ constexpr int kRingChunks = 8;          // fast kernel: per-warp record ring of 
 constexpr int kAhead = 6;               // chunks in flight ahead of the current one (cp.async)
 constexpr uint32_t kShortView = 8;      // instructions shorter than this are packed for the general kernel
 constexpr size_t kWarpCache = 5 * 16;   // fast kernel: the two window-cache entries (2 x 2 uint4) + pc-id cache
-constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16 + kWarpCache;
+constexpr int kDeferBuf = 32;           // fast kernel: deferred-view descriptors staged per warp
+constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16 + kWarpCache + kDeferBuf * sizeof(ull);
 // fixed-size parts first, at compile-time offsets (addresses are immediates,
 // nothing to keep in registers); the object table (3 x n u64) last
 constexpr size_t kOffIval = 0;                                         // [kInstrSlots][2] u64
@@ -269,6 +270,28 @@ __device__ __forceinline__ void instr_add_n(const Smem& m, uint32_t key1, uint32
 __device__ __forceinline__ void instr_add(const Smem& m, uint32_t key1, bool mis, ull* g, int lane) {
   if (lane == 0) instr_add_n(m, key1, 1u, mis ? 1u : 0u, g);
 }
+
+// deferred views staged per warp in shared memory, appended to the global
+// list with one atomic per 32 (a per-view atomic on the one counter serialises
+// in L2 when most instructions are short, e.g. SpMV)
+struct DeferBuf {
+  ull* s;        // smem [kDeferBuf]
+  uint32_t n;    // warp-uniform
+  __device__ __forceinline__ void flush(ull* g, ull* gcount, int lane) {
+    __syncwarp();
+    if (n == 0) return;
+    ull base = 0;
+    if (lane == 0) base = atomicAdd(gcount, (ull)n);
+    base = __shfl_sync(FULL, base, 0);
+    if ((uint32_t)lane < n) g[base + lane] = s[lane];
+    __syncwarp();
+    n = 0;
+  }
+  __device__ __forceinline__ void push(ull e, ull* g, ull* gcount, int lane) {
+    if (lane == 0) s[n] = e;
+    if (++n == (uint32_t)kDeferBuf) flush(g, gcount, lane);
+  }
+};
 
 // (launch, object) ids k < 32 counted in registers, lane k holding id k: one
 // predicated add per instruction instead of a shared atomic; flushed with

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
     wc[1] = wc[3] = make_uint4(1, 0xFFu, 0xFFFFFFFFu, 0);
     wc[4] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
   }
+  DeferBuf dq{reinterpret_cast<ull*>(wc + 5), 0};
   __syncwarp();
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
@@ -109,10 +110,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         // instructions of the next 32 records into one general-path view
         const uint32_t span = rem <= 32 ? rem : (sb ? 31u - __clz(sb) : 0u);  // to the last head / range end
         if (span > len) {
-          if (lane == 0) {
-            const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);
-            a.deferred[slot] = ((p0 + off) << 7) | span;
-          }
+          dq.push(((p0 + off) << 7) | span, a.deferred, &a.ctr->n_deferred, lane);
           off += span;
           continue;
         }
@@ -136,17 +134,15 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         continue;
       }
       if (!ok0 || __ballot_sync(FULL, odd) != 0) {
-        if (lane == 0) {  // defer the view to the general kernel
-          const ull slot = atomicAdd(&a.ctr->n_deferred, 1ull);
-          a.deferred[slot] = ((p0 + off) << 7) | len;
-        }
+        dq.push(((p0 + off) << 7) | len, a.deferred, &a.ctr->n_deferred, lane);  // to the general kernel
         off = offn;
         continue;
       }
       // ---- interval of lane 0's sector (uniform cache), lanes test theirs ----
       const uint32_t H = ((y0 >> 5) & 0x30000u) | (y0 & 0xFFFFu);  // space << 16 | addr[32,48)
       const uint32_t xs = x & ~31u;
-      const uint32_t xs0 = __shfl_sync(FULL, xs, 0);
+      const uint32_t x0 = __shfl_sync(FULL, x, 0);
+      const uint32_t xs0 = x0 & ~31u;
       const uint4 A0 = wc[0], A1 = wc[2];
       const bool h0 = (A0.x == H) & (xs0 - A0.y < A0.z), h1 = (A1.x == H) & (xs0 - A1.y < A1.z);
       uint32_t blo, bn, sbase, tail_s, tail_m;
@@ -166,6 +162,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         const uint4 B = wc[last1 ? 3 : 1];
         blo = A.y; bn = A.z; sbase = A.w; tail_s = B.x; tail_m = B.y; oid0 = (int)B.z;
       }
+      // lane 0's first word is mapped (uniform, from lane 0's interval): its
+      // instruction is counted in the statistics below
+      const bool first_mapped = (oid0 >= 0) & ((xs0 != tail_s) | ((tail_m >> ((x0 >> 2) & 7u)) & 1u));
       int oid = oid0;
       const bool inw = xs - blo < bn;
       if (__ballot_sync(FULL, act & !inw)) {  // lanes outside lane 0's interval (rare)
@@ -238,9 +237,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         m0 = has ? (mprev | mk) : m0;
       }
       // ---- instruction statistics (G24) ----
-      const uint32_t fa0 = __shfl_sync(FULL, fa, 0);
-      const uint32_t x0 = __shfl_sync(FULL, x, 0);
-      if ((oid0 >= 0) & ((fa0 >> ((x0 >> 2) & 7u)) & 1u)) {  // lane 0's first word is mapped (uniform)
+      if (first_mapped) {
         const uint32_t px = __shfl_up_sync(FULL, x, 1);
         const bool down = act & (lane > 0) & (x < px);
         uint32_t distinct;
@@ -266,6 +263,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
   STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
   st.flush(gkeys, gnk, lane);
+  dq.flush(a.deferred, &a.ctr->n_deferred, lane);
   if (cur_launch != 0xFFFFFFFFu) {
     const uint32_t um = __reduce_add_sync(FULL, lane_unmapped), mm = __reduce_add_sync(FULL, lane_mapped);
     if (lane == 0 && (um | mm)) {
