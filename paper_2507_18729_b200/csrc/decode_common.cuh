@@ -405,6 +405,11 @@ __device__ __forceinline__ ull entry_key(ull c, uint32_t m, ull tag, uint32_t SH
   return ((((c & 0xFFFFFFFFull) << SH) | (tag << P) | (c >> 32)) << 8) | m;
 }
 
+// same with the (launch, warp) field pre-shifted: tag8 = tag << (P + 8), SH8 = SH + 8
+__device__ __forceinline__ ull entry_key8(ull c, uint32_t m, ull tag8, uint32_t SH8) {
+  return ((c & 0xFFFFFFFFull) << SH8) | tag8 | (((uint32_t)(c >> 32) << 8) | m);
+}
+
 size_t decode_smem(const DecodeArgs& a);
 
 }  // namespace thermo

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   int steps = 0;
   while ((1u << steps) < nobj) ++steps;
   const uint32_t P = a.kl.P, W = a.kl.W;
-  const uint32_t SH = a.kl.L + a.kl.W + P;
+  const uint32_t SH8 = a.kl.L + a.kl.W + P + 8;
   const uint32_t max_launches = a.max_launches, max_warps = a.max_warps;
   ull* const gkeys = a.keys;
   ull* const gnk = &a.ctr->n_keys;
@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   ull c0 = 0, c1 = 0;
   uint32_t m0 = 0, m1 = 0;
   ull tag = 0;  // (launch << W | warp) of the entries (uniform)
+  ull tag8 = 0;  // tag << (P + 8), its place in a key
 
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -202,10 +203,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       if (__any_sync(FULL, has)) {
         const ull lw = ((ull)launch0 << W) | z0;
         if (lw != tag) {  // new source warp: every entry leaves as a key
-          STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
-          STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
+          STAGE_PUSH(st, m0 != 0, entry_key8(c0, m0, tag8, SH8), gkeys, gnk);
+          STAGE_PUSH(st, m1 != 0, entry_key8(c1, m1, tag8, SH8), gkeys, gnk);
           m0 = m1 = 0;
           tag = lw;
+          tag8 = lw << (P + 8);
         }
         uint32_t pcid = 0;
         if (a.track_pc) {
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         const ull ck = ((ull)pcid << 32) | g;
         const bool hit0 = c0 == ck, hit1 = c1 == ck;
         // a replaced entry leaves as a key
-        STAGE_PUSH(st, has & !hit0 & !hit1 & (m1 != 0), entry_key(c1, m1, tag, SH, P), gkeys, gnk);
+        STAGE_PUSH(st, has & !hit0 & !hit1 & (m1 != 0), entry_key8(c1, m1, tag8, SH8), gkeys, gnk);
         const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : 0u);
         const bool shift = has & !hit0;  // entry 0 moves to slot 1 (selects, no branch)
         c1 = shift ? c0 : c1;
@@ -260,8 +262,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // no copy may land in the next range's slots
     __syncwarp();
   }
-  STAGE_PUSH(st, m0 != 0, entry_key(c0, m0, tag, SH, P), gkeys, gnk);
-  STAGE_PUSH(st, m1 != 0, entry_key(c1, m1, tag, SH, P), gkeys, gnk);
+  STAGE_PUSH(st, m0 != 0, entry_key8(c0, m0, tag8, SH8), gkeys, gnk);
+  STAGE_PUSH(st, m1 != 0, entry_key8(c1, m1, tag8, SH8), gkeys, gnk);
   st.flush(gkeys, gnk, lane);
   dq.flush(a.deferred, &a.ctr->n_deferred, lane);
   if (cur_launch != 0xFFFFFFFFu) {
