@@ -510,3 +510,68 @@ def test_synthetic_full_size_sampled():
         for i in rows:
             assert np.array_equal(both[int(se[i])], ref[i]), (k, int(se[i]), both[int(se[i])], ref[i])
     assert sum(int((ref[:, 8] > 0).sum()) for _ in [0]) > 64  # the sample hits touched sectors
+
+
+def _records_touching(recs, abs_sec, chunk=1 << 26):
+    """Records whose first or last byte lies in one of the sectors abs_sec
+    (sorted int64 tensor on the records' device), with per-sector counts."""
+    keep, cnt = [], torch.zeros(abs_sec.shape[0], dtype=torch.int64, device=abs_sec.device)
+    for a in range(0, recs.shape[0], chunk):
+        c = recs[a:a + chunk]
+        addr = (c[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((c[:, 1].to(torch.int64) & 0xFFFF) << 32)
+        size = torch.ones_like(addr) << ((c[:, 1].to(torch.int64) >> 16) & 7)
+        s0, s1 = addr >> 5, (addr + size - 1) >> 5
+        m = torch.isin(s0, abs_sec) | torch.isin(s1, abs_sec)
+        hit = torch.cat([s0[m], s1[m & (s1 != s0)]])
+        cnt += torch.bincount(torch.searchsorted(abs_sec, hit), minlength=abs_sec.shape[0])[:abs_sec.shape[0]]
+        keep.append(c[m].cpu())
+    return torch.cat(keep), cnt.cpu().numpy()
+
+
+def test_spmv_full_size_sampled():
+    """BJ configs[3] at bench size (CSR SpMV on an R-MAT scale-24 matrix, 840.6 M
+    records, the bench's launch configuration: AUTO dedup = SEGMENT with the
+    hot-sector hash side path): the oracle on sampled sectors of every object,
+    including sectors hot enough (>= 2048 keys) to take the side path -- a
+    sector's row depends only on the records touching it, so the oracle ingests
+    just those -- plus the histogram invariants on every object."""
+    t = tg.spmv(24, 16, device="cuda")
+    from paper_2507_18729_b200 import Thermo
+    th = Thermo(max_launches=max(1, int(t.meta.get("launches", 1))),  # bench.py's configuration
+                max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), max_pcs=int(t.meta.get("pcs", 256)))
+    th.register_objects(t.objects)
+    th.ingest(t.records)
+    th.build(BOTH)
+    assert th.stats()["invalid"] == 0
+    rng = np.random.default_rng(24)
+    oi, se = _touched(t.objects, t.records, 8, rng)
+    abs_sec = np.array([t.objects[o][0] // 32 + int(s) for o, s in zip(oi, se)], dtype=np.int64)
+    order = np.argsort(abs_sec)
+    oi, se, abs_sec = oi[order], se[order], abs_sec[order]
+    _, cnt = _records_touching(t.records, torch.tensor(abs_sec, device="cuda"))
+    # bound the oracle's work: drop the hottest sampled sectors beyond 4 M records
+    # each (the x vector's power-law columns), keeping every hot one below that
+    ok = cnt <= 4_000_000
+    print("sampled sectors:", len(cnt), "records per sampled sector (max kept):", int(cnt[ok].max()),
+          "dropped:", int((~ok).sum()))
+    assert (cnt[ok] >= 2048).any(), "the sample should include a hot (side-path) sector"
+    oi, se, abs_sec = oi[ok], se[ok], abs_sec[ok]
+    sub, _ = _records_touching(t.records, torch.tensor(abs_sec, device="cuda"))
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.restrict(oi, se)
+    orc.ingest(sub)
+    orc.build()
+    ref = orc.sample(oi, se)
+    for k, ob in enumerate(t.objects):
+        oid = ob[3]
+        assert th.histogram(oid, WORD).sum() == (ob[1] + 3) // 4
+        assert th.histogram(oid, SECTOR).sum() == (ob[1] + 31) // 32
+        rows = [i for i in range(len(oi)) if oi[i] == k]
+        if not rows:
+            continue
+        both = th.heatmap(oid, BOTH).reshape(-1, 9)
+        for i in rows:
+            assert np.array_equal(both[int(se[i])], ref[i]), (k, int(se[i]), both[int(se[i])], ref[i])
+    print("sector counts of the sample: max", int(ref[:, 8].max()), "sectors with >= 2048 warps:", int((ref[:, 8] >= 2048).sum()))
+    assert int((ref[:, 8] > 0).sum()) > 16
+    assert int(ref[:, 8].max()) >= 2048  # a hot sector (>= 2048 keys): the SEGMENT side path at full size
