@@ -144,6 +144,10 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       const uint32_t xs = x & ~31u;
       const uint32_t x0 = __shfl_sync(FULL, x, 0);
       const uint32_t xs0 = x0 & ~31u;
+      // broadcast instruction: every lane on lane 0's address (B[k][col] of
+      // Listing 1); its lanes are all in lane 0's interval, merge into lane 0
+      // and span one sector run (never misaligned), so those steps are skipped
+      const bool bcast = __ballot_sync(FULL, act & (x != x0)) == 0;
       const uint4 A0 = wc[0], A1 = wc[2];
       const bool h0 = (A0.x == H) & (xs0 - A0.y < A0.z), h1 = (A1.x == H) & (xs0 - A1.y < A1.z);
       uint32_t blo, bn, sbase, tail_s, tail_m;
@@ -168,7 +172,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       const bool first_mapped = (oid0 >= 0) & ((xs0 != tail_s) | ((tail_m >> ((x0 >> 2) & 7u)) & 1u));
       int oid = oid0;
       const bool inw = xs - blo < bn;
-      if (__ballot_sync(FULL, act & !inw)) {  // lanes outside lane 0's interval (rare)
+      if (!bcast && __ballot_sync(FULL, act & !inw)) {  // lanes outside lane 0's interval (rare)
         if (act & !inw) {
           const WinEnt le = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs);
           blo = le.blo; sbase = le.sbase; tail_s = le.tail_s; tail_m = le.tail_m; oid = le.oid;
@@ -199,7 +203,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       if (FEAT & 1) {  // access counts: every lane's every mapped word (before the merge)
         for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * g + (__ffs(m) - 1)], 1u);
       }
-      adjacent_merge32(g, mk, has, lane);
+      if (bcast) has = has & (lane == 0);  // the run of equal sectors is the whole view
+      else adjacent_merge32(g, mk, has, lane);
       if (__any_sync(FULL, has)) {
         const ull lw = ((ull)launch0 << W) | z0;
         if (lw != tag) {  // new source warp: every entry leaves as a key
@@ -239,7 +244,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         m0 = has ? (mprev | mk) : m0;
       }
       // ---- instruction statistics (G24) ----
-      if (first_mapped) {
+      if (first_mapped & bcast) {  // one address: distinct = 1 <= ceil(size / 32) sectors
+        ir.add(sm, launch0 * nobj + (uint32_t)oid0, false, a.instr_ctr, lane);
+      } else if (first_mapped) {
         const uint32_t px = __shfl_up_sync(FULL, x, 1);
         const bool down = act & (lane > 0) & (x < px);
         uint32_t distinct;

@@ -2,7 +2,7 @@
 set -x
 timeout 600 python -m pytest tests -x -q -m gpu -k "small_workloads or random_traces or hot_sector or warp_records or synthetic_medium" > gpurun_out/q_pytest.log 2>&1; echo rc=$?
 tail -2 gpurun_out/q_pytest.log
-for v in 2 4; do THERMO_GEN_PER_SM=$v timeout 300 python bench.py --workload spmv --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/q_spmv_$v.json 2> gpurun_out/q_spmv_$v.err; echo rc=$?; done
+for v in 1; do timeout 300 python bench.py --workload spmv --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/q_spmv_$v.json 2> gpurun_out/q_spmv_$v.err; echo rc=$?; done
 timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/q_bench.json 2> gpurun_out/q_bench.err; echo rc=$?
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:"thermo::" --csv --log-file gpurun_out/launches_spmv.csv python bench.py --workload spmv --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/launches_spmv.log 2>&1; echo rc=$?
 python - <<'PY'
