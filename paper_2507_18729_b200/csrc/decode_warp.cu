@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     const uint32_t xs = x & ~31u;
     const uint32_t x0 = __shfl_sync(FULL, x, f);
     const uint32_t xs0 = x0 & ~31u;
+    // broadcast instruction (every active lane on the first one's address): no
+    // interval check, the merge leaves the first lane's key, never misaligned
+    const bool bcast = __ballot_sync(FULL, act & (x != x0)) == 0;
     const bool h0 = win_has(e0, H, xs0), h1 = win_has(e1, H, xs0);
     if (!(h0 | h1)) {
       const WinEnt ne = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs0);
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     const int oid0 = last1 ? e1.oid : e0.oid;
     int oid = oid0;
     const bool inw = xs - blo < (last1 ? e1.bn : e0.bn);
-    if (__ballot_sync(FULL, act & !inw)) {
+    if (!bcast && __ballot_sync(FULL, act & !inw)) {
       if (act & !inw) {
         const WinEnt le = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs);
         blo = le.blo; sbase = le.sbase; tail_s = le.tail_s; tail_m = le.tail_m; oid = le.oid;
@@ -158,7 +161,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     if (a.acc) {
       for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * g + (__ffs(m) - 1)], 1u);
     }
-    adjacent_merge32(g, mk, has, lane);
+    if (bcast) has = has & (lane == f);
+    else adjacent_merge32(g, mk, has, lane);
     if (__any_sync(FULL, has)) {
       const ull lw = ((ull)launch0 << W) | z0;
       if (lw != tag) {
@@ -193,7 +197,17 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     }
     // ---- instruction statistics (G24): active lanes ----
     const uint32_t fa0 = __shfl_sync(FULL, fa, f);
-    if ((oid0 >= 0) & ((fa0 >> ((x0 >> 2) & 7u)) & 1u)) {  // the first record's first word is mapped
+    const bool first_mapped = (oid0 >= 0) & ((fa0 >> ((x0 >> 2) & 7u)) & 1u);  // the first record's first word
+    if (first_mapped & bcast) {
+      ir.add(sm, launch0 * nobj + (uint32_t)oid0, false, a.instr_ctr, lane);
+    } else if (first_mapped & (amask == FULL) &&
+               __ballot_sync(FULL, (lane > 0) & (x < __shfl_up_sync(FULL, x, 1))) == 0) {
+      // all lanes active, non-decreasing offsets: count sector changes; span = last - first + size
+      const uint32_t px = __shfl_up_sync(FULL, x, 1);
+      const uint32_t distinct = __popc(__ballot_sync(FULL, (lane == 0) | ((x >> 5) != (px >> 5))));
+      const ull span = (ull)(__shfl_sync(FULL, x, 31) - x0) + size;
+      ir.add(sm, launch0 * nobj + (uint32_t)oid0, distinct > (span + 31) / 32, a.instr_ctr, lane);
+    } else if (first_mapped) {
       const unsigned m = __match_any_sync(FULL, act ? (x >> 5) : (0xF8000000u | (uint32_t)lane));
       const uint32_t distinct = __popc(__ballot_sync(FULL, act & (__ffs(m) - 1 == lane)));
       const uint32_t mn = __reduce_min_sync(FULL, act ? x : 0xFFFFFFFFu);
