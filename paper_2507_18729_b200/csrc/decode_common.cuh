@@ -173,11 +173,13 @@ static __device__ uint32_t pc_lookup_global(const PcMap& pm, uint32_t site, DevC
 }
 
 static __device__ __noinline__ uint32_t pc_lookup(ull* s_pc, const PcMap& pm, uint32_t site, DevCounters* ctr) {
+  // the block's warps share the cache: atomic 64-bit read (a CAS that never
+  // changes the value) and exchange, so an entry is never seen torn
   const uint32_t h = hash32(site) & (kPcSlots - 1);
-  const ull e = *((volatile ull*)&s_pc[h]);
+  const ull e = atomicCAS(&s_pc[h], 0ull, 0ull);
   if ((uint32_t)(e >> 32) == site && (uint32_t)e != kPcNone) return (uint32_t)e;
   const uint32_t id = pc_lookup_global(pm, site, ctr);
-  s_pc[h] = ((ull)site << 32) | id;
+  atomicExch(&s_pc[h], ((ull)site << 32) | id);
   return id;
 }
 

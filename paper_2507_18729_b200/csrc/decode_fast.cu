@@ -155,10 +155,12 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       if (!(h0 | h1)) {  // uniform miss: replace the entry not used last
         const WinEnt ne = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs0);
         const int e = last1 ? 0 : 1;
+        __syncwarp();  // every lane has read the entries before lane 0 replaces one
         if (lane == 0) {
           wc[2 * e] = make_uint4(ne.H, ne.blo, ne.bn, ne.sbase);
           wc[2 * e + 1] = make_uint4(ne.tail_s, ne.tail_m, (uint32_t)ne.oid, 0);
         }
+        __syncwarp();  // and the warp sees it from the next view on
         last1 = e == 1;
         blo = ne.blo; bn = ne.bn; sbase = ne.sbase; tail_s = ne.tail_s; tail_m = ne.tail_m; oid0 = ne.oid;
       } else {
@@ -223,11 +225,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
             pcid = pcc.w;
           } else {
             uint32_t id = 0;
+            __syncwarp();  // (as for the window entries)
             if (lane == 0) {
               id = pc_lookup(sm.pc, a.pcmap, w0, a.ctr);
               id = id < a.pcmap.max_pcs ? id : 0u;  // overflow is reported at build (ERANGE)
               wc[4] = make_uint4(w0, id, pcc.x, pcc.y);
             }
+            __syncwarp();
             pcid = __shfl_sync(FULL, id, 0);
           }
         }
