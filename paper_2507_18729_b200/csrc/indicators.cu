@@ -107,13 +107,25 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   Vote vt{0, 0};
   ull first = kNone, last = kNone;
   const ull gs = g0 + (ull)threadIdx.x * kSecPerThread;
+  // software pipeline: the next sector's count and 8 word counts (two 16-byte
+  // loads; rows are 32-byte aligned) are in flight while this one is scanned
+  uint32_t c_n = 0;
+  uint4 lo_n = make_uint4(0, 0, 0, 0), hi_n = lo_n;
+  if (gs < g1) {
+    c_n = a.sector_cnt[gs];
+    lo_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * gs)[0];
+    hi_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * gs)[1];
+  }
   for (int i = 0; i < kSecPerThread; ++i) {
     const ull g = gs + i;
     if (g >= g1) break;
-    const uint32_t c = a.sector_cnt[g];
-    // the sector's 8 word counts: two 16-byte loads (rows are 32-byte aligned)
-    const uint4 lo = reinterpret_cast<const uint4*>(a.word_cnt + 8 * g)[0];
-    const uint4 hi = reinterpret_cast<const uint4*>(a.word_cnt + 8 * g)[1];
+    const uint32_t c = c_n;
+    const uint4 lo = lo_n, hi = hi_n;
+    if (i + 1 < kSecPerThread && g + 1 < g1) {
+      c_n = a.sector_cnt[g + 1];
+      lo_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * (g + 1))[0];
+      hi_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * (g + 1))[1];
+    }
     const uint32_t xs[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     ull mw = 0;
     const ull wl0 = (g - soff) * 8;
