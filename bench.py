@@ -50,33 +50,76 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed region:
+    NVML polled every 5 ms from a thread (nvidia-smi -lms 20 as the fallback).
+    __enter__ returns only once the first sample has arrived, so the timed
+    region that follows is covered; __exit__ keeps the samples taken up to the
+    end of the region plus the first one after it."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.stop = index, [], None, False
+        self.t_start, self.t_end = 0.0, None
 
-    def __enter__(self):
+    def _nvml(self):
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+        def poll():
+            try:
+                while not self.stop:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((time.perf_counter(), float(sm), float(mx), tuple(bool(r & b) for b in bits)))
+                    time.sleep(0.005)
+            finally:
+                pynvml.nvmlShutdown()
+        return poll
+
+    def _smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits", "-lms", "20"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+        def read():
+            for line in self.proc.stdout:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 6 and p[0].replace(".", "").isdigit():
+                    self.rows.append((time.perf_counter(), float(p[0]),
+                                      float(p[1]) if p[1].replace(".", "").isdigit() else float(p[0]),
+                                      tuple(x.lower() == "active" for x in p[2:6])))
+        return read
+
+    def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+            target = self._nvml()
+        except Exception:
+            try:
+                target = self._smi()
+            except FileNotFoundError:
+                return self
+        self.t = threading.Thread(target=target, daemon=True)
+        self.t.start()
+        t0 = time.perf_counter()
+        while not self.rows and time.perf_counter() - t0 < 10.0:
+            time.sleep(0.005)
+        self.t_start = time.perf_counter()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 6:
-                self.rows.append(parts)
-
     def __exit__(self, *a):
+        self.t_end = time.perf_counter()
+        t0 = time.perf_counter()
+        while not any(r[0] > self.t_end for r in self.rows) and time.perf_counter() - t0 < 2.0:
+            time.sleep(0.005)
+        self.stop = True
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(2)
@@ -84,14 +127,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        t0 = getattr(self, "t_start", 0.0)
+        t1 = self.t_end if self.t_end is not None else float("inf")
+        rows = [r for r in self.rows if t0 <= r[0] <= t1]
+        if not rows:  # a region shorter than the sampling period: the samples around it
+            rows = [r for r in self.rows if r[0] < t0][-1:] + [r for r in self.rows if r[0] > t1][:1]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[3][i]})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
 
 
 def make_trace(workload: str, device: str, rank: int = 0, ws: int = 1):
