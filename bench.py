@@ -278,7 +278,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="sgemm")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash", "segment"])
+    ap.add_argument("--dedup", default="auto", choices=["auto", "sort", "hash", "segment", "dense"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
@@ -309,7 +309,7 @@ def main():
     t = make_trace(args.workload, str(dev), rank, ws if sharded else 1)
     n = t.n
     stream = torch.cuda.current_stream(dev)
-    dedup = {"auto": 0, "sort": 1, "hash": 2, "segment": 3}[args.dedup]
+    dedup = {"auto": 0, "sort": 1, "hash": 2, "segment": 3, "dense": 4}[args.dedup]
     cfg = dict(max_launches=max(1, int(t.meta.get("launches", 1))),
                max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))),
                max_pcs=int(t.meta.get("pcs", 256)), dedup=dedup)
@@ -418,7 +418,7 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": args.workload, "records": n * ws, "format": args.format, "objects": len(t.objects),
-                       "dedup": {1: "sort", 2: "hash", 3: "segment"}.get(st["dedup_used"], "?"),
+                       "dedup": {1: "sort", 2: "hash", 3: "segment", 4: "dense"}.get(st["dedup_used"], "?"),
                        "l2": "inputs larger than L2 (16 B x records >> 126 MB), no flush",
                        "records_per_gpu": n, "parallelism": parallelism},
             "roofline": roof, "pipeline_roofline": pipe, "phase_ms": ph_mean, "dominant_phase": dominant,

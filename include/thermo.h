@@ -117,10 +117,19 @@ typedef enum {
  *   HASH     open-addressing hash set in HBM
  *   SEGMENT  counting sort by sector + per-chunk shared-memory dedup; the
  *            keys of sectors holding >= 2048 keys take a hash-set side path
- *   AUTO     SEGMENT up to 2^30 registered sectors (its workspace is 28 B per
- *            sector), HASH beyond (chosen by measurement) */
+ *   DENSE    sampled-block mode only (1 <= block_warps <= 64, SURVEY §8f item
+ *            1): the paper's per-word warp bitmask as one u64 per
+ *            (launch, word) in device memory (64 B per sector per launch),
+ *            OR-ed from the keys and popcounted; no sort, no hash
+ *   AUTO     DENSE in sampled-block mode with block_warps <= 64 when its masks
+ *            take <= 4 GiB; else SEGMENT up to 2^30 registered sectors (its
+ *            workspace is 28 B per sector), HASH beyond (chosen by
+ *            measurement)
+ * thermo_create returns THERMO_EINVAL for DENSE outside sampled-block mode or
+ * with block_warps > 64. */
 typedef enum {
-  THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2, THERMO_DEDUP_SEGMENT = 3
+  THERMO_DEDUP_AUTO = 0, THERMO_DEDUP_SORT = 1, THERMO_DEDUP_HASH = 2, THERMO_DEDUP_SEGMENT = 3,
+  THERMO_DEDUP_DENSE = 4
 } thermo_dedup;
 
 /*
@@ -206,7 +215,7 @@ typedef struct {
   uint64_t distinct_pairs;     /* distinct (sector, launch, warp) = sum of sector counts */
   uint64_t distinct_pc_pairs;  /* distinct (launch, pc, sector)                */
   uint64_t n_pcs;              /* distinct (launch, pc) pairs seen             */
-  uint32_t dedup_used;         /* THERMO_DEDUP_SORT, _HASH or _SEGMENT          */
+  uint32_t dedup_used;         /* THERMO_DEDUP_SORT, _HASH, _SEGMENT or _DENSE  */
   uint32_t reserved0;
   double ms_ingest, ms_build, ms_classify;  /* device time of the last calls   */
   /* device time (CUDA events on the context stream) of the phases of the last

@@ -6,8 +6,10 @@ object -> heat-level histograms per object and per PC -> pattern indicators.
 The compute lives in ``libthermo.so`` (sm_100a CUDA, C ABI in include/thermo.h);
 ``thermo`` is its ctypes binding.
 """
-from .thermo import (ALL_LAUNCHES, BOTH, DEDUP_AUTO, DEDUP_HASH, DEDUP_SORT, LABELS, LEVELS, SECTOR, WORD,  # noqa: F401
+from .thermo import (ALL_LAUNCHES, BOTH, DEDUP_AUTO, DEDUP_DENSE, DEDUP_HASH, DEDUP_SEGMENT, DEDUP_SORT,  # noqa: F401
+                     LABELS, LEVELS, SECTOR, WORD,
                      Thermo, ThermoError, default_params, label_names, load)
 
 __all__ = ["Thermo", "ThermoError", "load", "default_params", "label_names", "WORD", "SECTOR", "BOTH",
-           "ALL_LAUNCHES", "DEDUP_AUTO", "DEDUP_SORT", "DEDUP_HASH", "LEVELS", "LABELS"]
+           "ALL_LAUNCHES", "DEDUP_AUTO", "DEDUP_SORT", "DEDUP_HASH", "DEDUP_SEGMENT", "DEDUP_DENSE", "LEVELS",
+           "LABELS"]

@@ -88,6 +88,8 @@ struct thermo_ctx {
   size_t table_cap = 0;
   ull* d_pctable = nullptr;
   size_t pctable_cap = 0;
+  ull* d_dense = nullptr;  // DENSE dedup: [max_launches][S_tot][8] warp masks
+  size_t dense_cap = 0;
   SortWorkspace sw, swpc;
   SegWorkspace seg;
   // host staging
@@ -403,8 +405,9 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
   thermo_config c;
   if (cfg) c = *cfg; else thermo_default_config(&c);
   if (c.max_launches < 1 || c.max_launches > 4096 || c.max_warps_per_launch < 1 || c.max_pcs < 1 ||
-      c.max_pcs > 65536 || c.dedup > THERMO_DEDUP_SEGMENT)
+      c.max_pcs > 65536 || c.dedup > THERMO_DEDUP_DENSE)
     return THERMO_EINVAL;
+  if (c.dedup == THERMO_DEDUP_DENSE && (c.block_warps < 1 || c.block_warps > 64)) return THERMO_EINVAL;
   thermo_ctx* ctx = new thermo_ctx();
   ctx->device = device;
   ctx->cfg = c;
@@ -504,7 +507,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_keys, ctx->d_pckeys, ctx->d_ctr, ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of,
                   ctx->d_instr, ctx->d_launch_ctr, ctx->d_hist, ctx->d_pchist, ctx->d_ind, ctx->d_tile_obj,
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
-                  ctx->d_table, ctx->d_pctable, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
+                  ctx->d_table, ctx->d_pctable, ctx->d_dense, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
@@ -878,7 +881,13 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   // 2^26 sectors 127 vs 170 ms; synthetic 2^28 sectors 60 vs 82 ms); its
   // per-sector workspace (28 B/sector) decides the limit
   uint32_t mode = ctx->cfg.dedup;
-  if (mode == THERMO_DEDUP_AUTO) mode = ctx->S_tot <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
+  const ull dense_words = (ull)ctx->cfg.max_launches * ctx->S_tot * 8;  // DENSE masks (u64 each)
+  if (mode == THERMO_DEDUP_AUTO) {
+    if (ctx->cfg.block_warps >= 1 && ctx->cfg.block_warps <= 64 && dense_words * 8 <= (4ull << 30))
+      mode = THERMO_DEDUP_DENSE;
+    else
+      mode = ctx->S_tot <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
+  }
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
   bool pc_done = false;
@@ -954,6 +963,23 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     }
     launch_count_sorted(ctx->d_keys, ctx->n_keys, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
     ctx->launches += 1;
+  } else if (mode == THERMO_DEDUP_DENSE) {
+    // sampled-block mode: the paper's per-word warp bitmask per
+    // (launch, word), OR-ed from the keys, then popcounted
+    if (ctx->dense_cap < dense_words) {
+      dfree(ctx->d_dense);
+      ctx->dense_cap = 0;
+      CK(dalloc(&ctx->d_dense, dense_words));
+      ctx->dense_cap = dense_words;
+    }
+    CK(cudaEventRecord(ctx->evp[0], s));
+    CK(cudaMemsetAsync(ctx->d_dense, 0, dense_words * 8, s));
+    launch_dense_or(ctx->d_keys, ctx->n_keys, kl, ctx->cfg.block_id * ctx->cfg.block_warps, ctx->S_tot,
+                    ctx->d_dense, ctx->num_sms, s);
+    CK(cudaEventRecord(ctx->evp[1], s));
+    launch_dense_count(ctx->d_dense, ctx->cfg.max_launches, ctx->S_tot, launch_filter, ctx->d_wc, ctx->d_sc,
+                       ctx->d_ctr, ctx->num_sms, s);
+    ctx->launches += 2;
   } else if (mode == THERMO_DEDUP_HASH) {
     ull cap = next_pow2(std::max<ull>(1024, 2 * ctx->n_keys));
     if (ctx->table_cap < cap) {

@@ -160,6 +160,13 @@ void launch_count_sorted(const ull* keys, ull n, KeyLayout kl, uint32_t launch_f
 void launch_count_hash(const ull* table, ull cap, KeyLayout kl, uint32_t launch_filter, uint32_t* word_cnt,
                        uint32_t* sector_cnt, DevCounters* ctr, int num_sms, cudaStream_t s);
 
+// DENSE dedup (sampled-block mode, <= 64 warps in scope): keys OR-ed into one
+// u64 warp mask per (launch, word) [L][S_tot][8], then popcounts -> dense arrays
+void launch_dense_or(const ull* keys, ull n, KeyLayout kl, uint32_t warp0, ull S_tot, ull* dm, int num_sms,
+                     cudaStream_t s);
+void launch_dense_count(const ull* dm, uint32_t L, ull S_tot, uint32_t filter, uint32_t* wc, uint32_t* sc,
+                        DevCounters* ctr, int num_sms, cudaStream_t s);
+
 // a6 histograms over dense arrays, per object
 // (sharded mode: only the sectors rank owns; nranks = 1: all)
 void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj,

@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libthermo.so")
 
 WORD, SECTOR, BOTH = 1, 2, 3
-DEDUP_AUTO, DEDUP_SORT, DEDUP_HASH, DEDUP_SEGMENT = 0, 1, 2, 3
+DEDUP_AUTO, DEDUP_SORT, DEDUP_HASH, DEDUP_SEGMENT, DEDUP_DENSE = 0, 1, 2, 3, 4
 ALL_LAUNCHES = 0xFFFFFFFF
 LEVELS = 33
 STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ERANGE", -4: "ESTATE", -5: "ECUDA", -6: "ENCCL"}

@@ -81,3 +81,20 @@ def test_product_does_not_touch_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt and "/root/reference" not in txt, f
+
+
+def test_dense_dedup_needs_sampled_block_mode(lib):
+    """THERMO_DEDUP_DENSE is rejected before any device call
+    unless 1 <= block_warps <= 64 (the paper's warp bitmask holds <= 64 warps)."""
+    from paper_2507_18729_b200 import thermo
+    EINVAL = -1
+    for bw in (0, 65, 1024):
+        cfg = thermo.thermo_config()
+        lib.thermo_default_config(ctypes.byref(cfg))
+        cfg.dedup, cfg.block_warps = thermo.DEDUP_DENSE, bw
+        h = ctypes.c_void_p()
+        assert lib.thermo_create(ctypes.byref(h), 0, None, ctypes.byref(cfg)) == EINVAL
+    cfg = thermo.thermo_config()
+    lib.thermo_default_config(ctypes.byref(cfg))
+    cfg.dedup = 5  # past the last mode
+    assert lib.thermo_create(ctypes.byref(ctypes.c_void_p()), 0, None, ctypes.byref(cfg)) == EINVAL

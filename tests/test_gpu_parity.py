@@ -278,15 +278,17 @@ def test_access_counts(case):
         assert np.array_equal(th.heatmap(obj[3], WORD), orc2.word_counts(k))
 
 
+@pytest.mark.parametrize("dedup", [0, 3, 4])  # AUTO (= DENSE here), SEGMENT, DENSE
 @pytest.mark.parametrize("block", [0, 5])
-def test_sampled_block_mode(block):
+def test_sampled_block_mode(block, dedup):
     """Sampled-block mode: only one thread
     block's warps are reduced; everything against the oracle's block scope,
-    on a fuzz trace (mixed/invalid records, general path) and on SGEMM."""
+    on a fuzz trace (mixed/invalid records, general path) and on SGEMM, with
+    the DENSE warp-bitmask path and with SEGMENT."""
     from paper_2507_18729_b200 import Thermo
     for t, bw in ((tg.gemm(128, 96, 40, "v00"), 32),
                   (tg.random_trace(n=30000, seed=13, n_warps=400, n_launches=1), 16)):
-        th = Thermo(max_launches=1, max_warps_per_launch=1 << 22, block_warps=bw, block_id=block)
+        th = Thermo(max_launches=1, max_warps_per_launch=1 << 22, block_warps=bw, block_id=block, dedup=dedup)
         th.register_objects(t.objects)
         th.ingest(t.records.cuda().contiguous())
         th.build(BOTH)
@@ -295,6 +297,29 @@ def test_sampled_block_mode(block):
         orc.ingest(t.records)
         orc.build()
         compare(orc, th, t)
+        assert th.stats()["dedup_used"] == (4 if dedup in (0, 4) else dedup)
+
+
+@pytest.mark.parametrize("bw,block", [(64, 2), (8, 31)])
+def test_dense_multi_launch(bw, block):
+    """DENSE on the synthetic generator's 8 launches x 256
+    warps: one block of 64 (or 8) warps per launch; every output against the
+    oracle's block scope, for all launches and for one launch (G2)."""
+    from paper_2507_18729_b200 import Thermo
+    t = tg.synthetic(n_objects=16, n_launches=8, warps_per_launch=256, records_per_warp=256, size_shift=14)
+    th = Thermo(max_launches=8, max_warps_per_launch=256, max_pcs=64, block_warps=bw, block_id=block,
+                dedup=4)
+    th.register_objects(t.objects)
+    th.ingest(t.records.cuda())
+    for lf in (None, 5):
+        th.build(BOTH) if lf is None else th.build(BOTH, lf)
+        orc = oracle.Oracle([o[:4] for o in t.objects])
+        orc.block_scope(bw, block)
+        for c in t.calls():
+            orc.ingest(c)
+        orc.build() if lf is None else orc.build(lf)
+        compare(orc, th, t)
+        assert th.stats()["dedup_used"] == 4
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
