@@ -79,6 +79,7 @@ def _load():
         L.orc_restrict.argtypes = [vp, vp, vp, sz]
         L.orc_ingest.argtypes = [vp, vp, sz]
         L.orc_block_scope.argtypes = [vp, u32, u32]
+        L.orc_launch_whitelist.argtypes = [vp, vp, ctypes.c_size_t]
         L.orc_ingest_warp.argtypes = [vp, vp, sz]
         L.orc_build.argtypes = [vp, u32]
         L.orc_word_counts.argtypes = [vp, u32, vp]
@@ -139,6 +140,12 @@ class Oracle:
     def block_scope(self, warps_per_block: int, block: int):
         """Keep only the records of one sampled block; call before ingest."""
         _load().orc_block_scope(self._h, warps_per_block, block)
+
+    def launch_whitelist(self, launches):
+        """Kernel sampling by whitelist: only these launches are traced
+        (empty: all); call before ingest."""
+        a = np.ascontiguousarray(np.asarray(list(launches), dtype=np.uint32))
+        _load().orc_launch_whitelist(self._h, _ptr(a) if len(a) else None, len(a))
 
     def ingest(self, records):
         """records: anything exposing 16-byte records (numpy/torch int32 [n,4])."""

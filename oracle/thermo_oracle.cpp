@@ -90,6 +90,9 @@ struct Oracle {
   // only the records of global block `block_id` (warp / block_warps); the others
   // were never traced
   uint32_t block_warps = 0, block_id = 0;
+  // kernel sampling by whitelist: when non-empty, only the records of
+  // launches l with launch_ok[l] are traced; the others are as never traced
+  std::vector<bool> launch_ok;
   // restriction (sampled mode): only these (object index, local sector) pairs
   bool restricted = false;
   std::set<std::pair<uint32_t, uint64_t>> allow;
@@ -153,6 +156,7 @@ struct Oracle {
       if (k == 0 || r.instr_start || pos == 32) { close_instr(); in_instr = true; pos = 0; }
       ++pos;
       if (block_warps && r.warp / block_warps != block_id) continue;  // outside the sampled block
+      if (!launch_ok.empty() && (r.launch >= launch_ok.size() || !launch_ok[r.launch])) continue;  // not whitelisted
       if (!r.valid) { ++n_invalid; continue; }
       // ---- instruction extent (Fig.6) ----
       uint64_t lo = (uint64_t(r.space) << 48) | r.addr;
@@ -352,6 +356,16 @@ void orc_block_scope(void* h, uint32_t warps_per_block, uint32_t block) {
   Oracle* o = static_cast<Oracle*>(h);
   o->block_warps = warps_per_block;
   o->block_id = block;
+}
+
+// kernel whitelist: only launches listed are traced; n = 0 traces all
+void orc_launch_whitelist(void* h, const uint32_t* launches, size_t n) {
+  Oracle* o = static_cast<Oracle*>(h);
+  o->launch_ok.clear();
+  for (size_t i = 0; i < n; ++i) {
+    if (launches[i] >= o->launch_ok.size()) o->launch_ok.resize(launches[i] + 1, false);
+    o->launch_ok[launches[i]] = true;
+  }
 }
 
 void orc_ingest(void* h, const void* recs, size_t n) {

@@ -540,3 +540,35 @@ def test_restricted_sample_equals_brute_force(seed):
         other = o.sample(np.array([0]), np.array([int(s) for s in range(100) if (0, s) not in set(zip(oi, se))][:1],
                                                  dtype=np.uint64))
         assert (other == 0).all()
+
+
+def test_launch_whitelist():
+    """Kernel sampling by whitelist: the oracle with a
+    launch whitelist equals the oracle on the trace pre-filtered to those
+    launches' records, for every output; an empty whitelist traces all."""
+    t = tg.random_trace(n=20000, seed=21, n_warps=300, n_launches=6)
+    f = R.fields(t.records)
+    for wl in ([1, 4], [0], [5, 2, 3]):
+        o = oracle.Oracle(objs(t))
+        o.launch_whitelist(wl)
+        o.ingest(t.records)
+        o.build()
+        keep = np.isin(f["launch"], wl)
+        sub = t.records[torch.from_numpy(np.nonzero(keep)[0])]
+        assert 0 < sub.shape[0] < t.records.shape[0]
+        p = oracle.Oracle(objs(t))
+        p.ingest(sub)
+        p.build()
+        for k in range(len(t.objects)):
+            assert np.array_equal(o.word_counts(k), p.word_counts(k))
+            assert np.array_equal(o.sector_counts(k), p.sector_counts(k))
+            assert np.array_equal(o.hist(k, False), p.hist(k, False))
+        assert o.classify() == p.classify()
+        assert [(r[0], r[1]) for r in o.per_pc()] == [(r[0], r[1]) for r in p.per_pc()]
+    a = oracle.Oracle(objs(t))
+    a.launch_whitelist([])
+    a.ingest(t.records)
+    a.build()
+    b = oracle.run(objs(t), [t.records])
+    for k in range(len(t.objects)):
+        assert np.array_equal(a.word_counts(k), b.word_counts(k))
