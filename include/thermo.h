@@ -293,6 +293,17 @@ thermo_status thermo_destroy(thermo_ctx *ctx);
 thermo_status thermo_reset(thermo_ctx *ctx);
 
 /*
+ * Kernel sampling by whitelist ("kernel sampling is also supported by a
+ * whitelist method"): from the next ingest call on, only the
+ * records of the n launch ids in `launches` (host array, read during the call)
+ * are traced; the others are treated as never traced (counted in
+ * stats.records only), like the warps outside the sampled block.  n = 0 traces
+ * every launch again.  Combines with sampled-block mode.  Errors: EINVAL (a
+ * launch id >= max_launches, or launches == NULL with n > 0), ECUDA.
+ */
+thermo_status thermo_set_launch_whitelist(thermo_ctx *ctx, const uint32_t *launches, size_t n);
+
+/*
  * Register the data objects.  Called exactly once, before any
  * ingest.  objs is a HOST array of n objects (copied).  Errors: EINVAL
  * (len == 0, base not 32-aligned, base+len > 2^48, space > 2, overlap within a

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
     const uint32_t l2s = (cur.y >> 16) & 7u, kind = (cur.y >> 19) & 3u;
     const uint32_t space = (cur.y >> 21) & 3u, resv = cur.y >> 24;
     const ull size = 1ull << (l2s > 4 ? 0 : l2s);
-    const bool traced = act && (!a.block_warps || warp_id / a.block_warps == a.block_id);  // sampled block
+    const bool traced = act && !out_of_scope(a, warp_id, site >> 20);  // sampled block, launch whitelist
     bool valid = traced && l2s <= 4 && kind <= 2 && space <= 2 && resv == 0 && addr + size <= (1ull << 48);
     const uint32_t launch = site >> 20;
     const bool oor = valid && (launch >= a.max_launches || warp_id >= a.max_warps);

@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       // uniform instruction (upper address bits included), no sector straddle
       const bool odd = act & ((cur.z != z0) | (cur.w != w0) | (((cur.y ^ y0) & 0xFF7FFFFFu) != 0) |
                               ((x & 31u) + size > 32u));
-      if ((FEAT & 2) && z0 / a.block_warps != a.block_id && __ballot_sync(FULL, odd) == 0) {
-        off = offn;  // an instruction of a warp outside the sampled block: never traced
+      if ((FEAT & 2) && out_of_scope(a, z0, launch0) && __ballot_sync(FULL, odd) == 0) {
+        off = offn;  // an instruction outside the sampled block or the launch whitelist: never traced
         continue;
       }
       if (!ok0 || __ballot_sync(FULL, odd) != 0) {
@@ -307,7 +307,7 @@ static void launch_decode_t(const DecodeArgs& a, int num_sms, cudaStream_t s, si
 
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s) {
   const size_t smem = decode_smem(a);
-  const int feat = (a.acc ? 1 : 0) | (a.block_warps ? 2 : 0);
+  const int feat = (a.acc ? 1 : 0) | ((a.block_warps || a.wl) ? 2 : 0);
   static const int minb = getenv("THERMO_DEC_MINB") ? atoi(getenv("THERMO_DEC_MINB")) : 3;
   switch (feat) {
     case 0:

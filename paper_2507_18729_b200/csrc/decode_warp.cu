@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_warp_kernel(WarpD
     const uint32_t z0 = h.x, w0 = h.y, amask = h.z, flags = h.w;
     if (amask == 0) continue;  // no lane executed it: no records
     lanes_seen += __popc(amask);
-    if (a.block_warps && z0 / a.block_warps != a.block_id) continue;  // outside the sampled block (G28)
+    if (out_of_scope(a, z0, w0 >> 20)) continue;  // outside the sampled block (G28) or the launch whitelist
     const bool act = (amask >> lane) & 1u;
     const int f = __ffs(amask) - 1;  // the instruction's first record
     const uint32_t l2s = flags & 7u, kind = (flags >> 3) & 3u, space = (flags >> 5) & 3u;

@@ -90,6 +90,8 @@ struct thermo_ctx {
   size_t pctable_cap = 0;
   ull* d_dense = nullptr;  // DENSE dedup: [max_launches][S_tot][8] warp masks
   size_t dense_cap = 0;
+  uint32_t* d_wl = nullptr;  // launch whitelist bitmask [128]
+  bool wl_on = false;
   SortWorkspace sw, swpc;
   SegWorkspace seg;
   // host staging
@@ -252,6 +254,7 @@ DecodeArgs decode_args(thermo_ctx* ctx) {
   a.acc = ctx->d_acc;
   a.block_warps = ctx->cfg.block_warps;
   a.block_id = ctx->cfg.block_id;
+  a.wl = ctx->wl_on ? ctx->d_wl : nullptr;
   return a;
 }
 
@@ -507,7 +510,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_keys, ctx->d_pckeys, ctx->d_ctr, ctx->d_pc_keys_tab, ctx->d_pc_vals, ctx->d_site_of,
                   ctx->d_instr, ctx->d_launch_ctr, ctx->d_hist, ctx->d_pchist, ctx->d_ind, ctx->d_tile_obj,
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
-                  ctx->d_table, ctx->d_pctable, ctx->d_dense, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
+                  ctx->d_table, ctx->d_pctable, ctx->d_dense, ctx->d_wl, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
@@ -638,6 +641,22 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   }
   ctx->state = 1;
   return thermo_reset(ctx);
+}
+
+thermo_status thermo_set_launch_whitelist(thermo_ctx* ctx, const uint32_t* launches, size_t n) {
+  thermo_status st = pre(ctx);
+  if (st) return st;
+  if (n && !launches) return fail(ctx, THERMO_EINVAL, "launch whitelist: null array");
+  uint32_t bits[128] = {0};
+  for (size_t i = 0; i < n; ++i) {
+    if (launches[i] >= ctx->cfg.max_launches) return fail(ctx, THERMO_EINVAL, "launch whitelist: id >= max_launches");
+    bits[launches[i] >> 5] |= 1u << (launches[i] & 31u);
+  }
+  if (!ctx->d_wl) CK(dalloc(&ctx->d_wl, 128));
+  CK(cudaMemcpyAsync(ctx->d_wl, bits, sizeof bits, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // `bits` is on this stack frame
+  ctx->wl_on = n > 0;
+  return THERMO_OK;
 }
 
 thermo_status thermo_reset(thermo_ctx* ctx) {

@@ -96,7 +96,15 @@ struct DecodeArgs {
   uint32_t* seg_cnt;      // [S_tot] keys per sector (SEGMENT histogram), or null
   uint32_t* acc;          // [8 S_tot] lane accesses per word (track_access), or null
   uint32_t block_warps, block_id;  // sampled-block mode (0: whole grid)
+  const uint32_t* wl;               // launch whitelist bitmask [128], or null: every launch
 };
+
+// outside the traced scope: a warp outside the sampled block or a launch
+// outside the whitelist (launch < 4096 for any record: site >> 20)
+__device__ __forceinline__ bool out_of_scope(const DecodeArgs& a, uint32_t warp, uint32_t launch) {
+  return (a.block_warps && warp / a.block_warps != a.block_id) ||
+         (a.wl && !((a.wl[(launch >> 5) & 127u] >> (launch & 31u)) & 1u));
+}
 
 // ---- kernels (launch wrappers live in the .cu files) ----------------------
 void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_ranges, ull* heads,

@@ -80,7 +80,7 @@ EXPORTS = ("thermo_default_config", "thermo_default_params", "thermo_abi_version
            "thermo_register_objects", "thermo_ingest_trace", "thermo_build_heatmap", "thermo_query_heatmap",
            "thermo_query_histogram", "thermo_query_per_pc", "thermo_classify", "thermo_get_stats",
            "thermo_last_error", "thermo_create_local_shards", "thermo_sharding", "thermo_query_access",
-           "thermo_ingest_warp_trace", "thermo_query_runs")
+           "thermo_ingest_warp_trace", "thermo_query_runs", "thermo_set_launch_whitelist")
 
 _lib = None
 
@@ -106,6 +106,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.thermo_sharding.argtypes = [vp, P(ctypes.c_int), P(ctypes.c_int), P(u32)]
     L.thermo_destroy.argtypes = [vp]
     L.thermo_reset.argtypes = [vp]
+    L.thermo_set_launch_whitelist.argtypes = [vp, vp, sz]
     L.thermo_register_objects.argtypes = [vp, P(thermo_object), sz]
     L.thermo_ingest_trace.argtypes = [vp, vp, sz]
     L.thermo_ingest_warp_trace.argtypes = [vp, vp, sz]
@@ -241,6 +242,13 @@ class Thermo:
 
     def reset(self):
         self._ck(self.L.thermo_reset(self.h))
+
+    def set_launch_whitelist(self, launches=()):
+        """Kernel sampling by whitelist: only these launch ids are traced
+        from the next ingest on; () traces every launch."""
+        a = (ctypes.c_uint32 * max(1, len(launches)))(*[int(x) for x in launches])
+        self._ck(self.L.thermo_set_launch_whitelist(self.h, ctypes.cast(a, ctypes.c_void_p) if launches else None,
+                                                    len(launches)))
 
     def ingest(self, records):
         """records: torch int32 [n, 4] (device or host) or a numpy array."""

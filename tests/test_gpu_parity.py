@@ -600,3 +600,45 @@ def test_spmv_full_size_sampled():
     print("sector counts of the sample: max", int(ref[:, 8].max()), "sectors with >= 2048 warps:", int((ref[:, 8] >= 2048).sum()))
     assert int((ref[:, 8] > 0).sum()) > 16
     assert int(ref[:, 8].max()) >= 2048  # a hot sector (>= 2048 keys): the SEGMENT side path at full size
+
+
+@pytest.mark.parametrize("dedup", [3, 1])
+def test_launch_whitelist(dedup):
+    """Kernel sampling by whitelist on the 8-launch
+    synthetic trace, per-lane and warp-instruction records, alone and combined
+    with a sampled block (DENSE): every output against the oracle with the same
+    whitelist (pinned against the pre-filtered trace); clearing it traces all."""
+    from paper_2507_18729_b200 import Thermo
+    t = tg.synthetic(n_objects=16, n_launches=8, warps_per_launch=256, records_per_warp=256, size_shift=14)
+    for wl, bw, blk in (([1, 4, 7], 0, 0), ([2], 0, 0), ([0, 3, 5], 64, 1)):
+        kw = dict(block_warps=bw, block_id=blk) if bw else dict(dedup=dedup)
+        th = Thermo(max_launches=8, max_warps_per_launch=256, max_pcs=64, **kw)
+        th.register_objects(t.objects)
+        th.set_launch_whitelist(wl)
+        th.ingest(t.records.cuda())
+        th.build(BOTH)
+        orc = oracle.Oracle([o[:4] for o in t.objects])
+        if bw:
+            orc.block_scope(bw, blk)
+        orc.launch_whitelist(wl)
+        for c in t.calls():
+            orc.ingest(c)
+        orc.build()
+        compare(orc, th, t)
+        # the same through warp-instruction records
+        th.reset()
+        th.ingest_warp(tg.to_warp_records(t.records).cuda())
+        th.build(BOTH)
+        compare(orc, th, t)
+    th.set_launch_whitelist([])
+    th.reset()
+    th.ingest(t.records.cuda())
+    th.build(BOTH)
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.block_scope(64, 1)
+    for c in t.calls():
+        orc.ingest(c)
+    orc.build()
+    compare(orc, th, t)
+    with pytest.raises(Exception):
+        th.set_launch_whitelist([8])  # >= max_launches
