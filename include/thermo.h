@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define THERMO_ABI_VERSION 3u
+#define THERMO_ABI_VERSION 4u
 #define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
 #define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
 #define THERMO_MAX_OBJECTS 1024
