@@ -182,3 +182,38 @@ def test_shards_warp_records():
 
     run_ranks([job(r) for r in range(3)])
     compare(t, ref, shards)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_shards_dense_block_mode_and_whitelist(P):
+    """Row e with SURVEY §8f item 1: sampled-block mode (AUTO = DENSE warp
+    bitmasks) plus a launch whitelist, sharded over P in-process ranks, equals
+    one context on the same slices."""
+    from paper_2507_18729_b200 import Thermo
+    from paper_2507_18729_b200.dist import run_ranks
+    t = tg.synthetic(n_objects=16, n_launches=4, warps_per_launch=256, records_per_warp=256, size_shift=12)
+    cfg = dict(max_launches=4, max_warps_per_launch=1 << 22, block_warps=64, block_id=1)
+    sl = _slices(t, P)
+    ref = Thermo(**cfg)
+    ref.register_objects(t.objects)
+    ref.set_launch_whitelist([0, 2, 3])
+    for c in sl:
+        if c.shape[0]:
+            ref.ingest(c.cuda().contiguous())
+    ref.build(BOTH)
+    assert ref.stats()["dedup_used"] == 4
+    shards = Thermo.local_shards(P, **cfg)
+
+    def job(r):
+        def f():
+            th = shards[r]
+            th.register_objects(t.objects)
+            th.set_launch_whitelist([0, 2, 3])
+            if sl[r].shape[0]:
+                th.ingest(sl[r].cuda().contiguous())
+            th.build(BOTH)
+        return f
+
+    run_ranks([job(r) for r in range(P)])
+    assert all(s.stats()["dedup_used"] == 4 for s in shards)
+    compare(t, ref, shards)
