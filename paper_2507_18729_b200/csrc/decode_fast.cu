@@ -205,8 +205,18 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       if (FEAT & 1) {  // access counts: every lane's every mapped word (before the merge)
         for (uint32_t m = fa; m; m &= m - 1) atomicAdd(&a.acc[8ull * g + (__ffs(m) - 1)], 1u);
       }
+      // stride instruction: every active lane's sector strictly above the
+      // previous lane's (A[row][k] of Listing 1): no two lanes share a sector,
+      // so the merge has nothing to do and the distinct sectors are the lanes
+      uint32_t px = 0;
+      bool stride = false;
+      if (!bcast) {
+        px = __shfl_up_sync(FULL, x, 1);
+        const unsigned actm = len >= 32 ? FULL : ((1u << len) - 1u);
+        stride = __ballot_sync(FULL, act & (lane > 0) & ((x >> 5) > (px >> 5))) == (actm & ~1u);
+      }
       if (bcast) has = has & (lane == 0);  // the run of equal sectors is the whole view
-      else adjacent_merge32(g, mk, has, lane);
+      else if (!stride) adjacent_merge32(g, mk, has, lane);
       if (__any_sync(FULL, has)) {
         const ull lw = ((ull)launch0 << W) | z0;
         if (lw != tag) {  // new source warp: every entry leaves as a key
@@ -250,8 +260,11 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       // ---- instruction statistics (G24) ----
       if (first_mapped & bcast) {  // one address: distinct = 1 <= ceil(size / 32) sectors
         ir.add(sm, launch0 * nobj + (uint32_t)oid0, false, a.instr_ctr, lane);
+      } else if (first_mapped & stride) {  // len distinct sectors over [x0, x_last + size)
+        const uint32_t d = __shfl_sync(FULL, x, len - 1) - x0;
+        const uint32_t need = (d >> 5) + (((d & 31u) + size + 31u) >> 5);  // ceil((d + size) / 32)
+        ir.add(sm, launch0 * nobj + (uint32_t)oid0, len > need, a.instr_ctr, lane);
       } else if (first_mapped) {
-        const uint32_t px = __shfl_up_sync(FULL, x, 1);
         const bool down = act & (lane > 0) & (x < px);
         uint32_t distinct;
         ull span;
