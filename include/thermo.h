@@ -239,8 +239,10 @@ uint32_t thermo_abi_version(void);
 
 /*
  * Create a context on `device` using CUDA stream `stream` (a cudaStream_t
- * passed as void*, NULL = a new stream owned by the context).  cfg NULL =
- * defaults.  Ownership: the context owns every device buffer it allocates.
+ * passed as void*, NULL = a new blocking stream owned by the context, which is
+ * ordered after work queued on the legacy default stream).  Device-resident
+ * records written on any OTHER stream must be complete before ingest (pass
+ * that stream here, or synchronize).  cfg NULL = defaults.  Ownership: the context owns every device buffer it allocates.
  * Errors: EINVAL (bad cfg), ECUDA, ENOMEM.
  */
 thermo_status thermo_create(thermo_ctx **out, int device, void *stream, const thermo_config *cfg);

@@ -33,20 +33,27 @@ def _mtime(p):
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
     hdr_t = max(_mtime(os.path.join(CSRC, h)) for h in HEADERS)
-    objs, rebuilt = [], False
+    objs, todo = [], []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
         op = os.path.join(OBJDIR, src.replace(".cu", ".o"))
         objs.append(op)
         if force or _mtime(op) < max(_mtime(sp), hdr_t):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", sp, "-o", op]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                sys.stderr.write(r.stdout + r.stderr)
-                raise RuntimeError(f"nvcc failed on {src}")
-            if verbose:
-                sys.stderr.write(r.stderr)
-            rebuilt = True
+            todo.append((src, [NVCC, *ARCH, *FLAGS, "-c", sp, "-o", op]))
+
+    def compile_one(item):
+        return item[0], subprocess.run(item[1], capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, todo))
+    for src, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc failed on {src}")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    rebuilt = bool(todo)
     if force or rebuilt or not os.path.exists(LIB):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcuda", "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)

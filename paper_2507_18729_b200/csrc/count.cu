@@ -255,11 +255,7 @@ void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, Ob
   const uint32_t nb = obj.n * 2 * kLevels;
   const int use_smem = nb * sizeof(uint32_t) <= 96 * 1024;
   size_t smem = use_smem ? nb * sizeof(uint32_t) : 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(object_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)object_hist_kernel, 96 * 1024);
   unsigned grid = (unsigned)std::min<ull>((total_sectors + 255) / 256, (ull)num_sms * 8);
   if (grid < 1) grid = 1;
   object_hist_kernel<<<grid, 256, smem, s>>>(word_cnt, sector_cnt, obj.soff, obj_nwords, obj.n, hist,

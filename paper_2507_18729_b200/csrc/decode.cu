@@ -247,18 +247,12 @@ size_t decode_smem(const DecodeArgs& a) {
 
 void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s) {
   const size_t smem = decode_smem(a);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_general_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)decode_general_kernel, 200 * 1024);
   // the deferred count is read on the device: a full persistent grid (the
   // kernel waits on record loads, so every resident warp helps)
-  static int per_sm = 0;
-  if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_general_kernel, kDecWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_general_kernel, kDecWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
   ull grid = (a.n_ranges + kDecWarps - 1) / kDecWarps;
   const ull cap = (ull)num_sms * per_sm;
   if (grid > cap) grid = cap;

@@ -303,11 +303,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
 
 template <int MINB, int FEAT>
 static void launch_decode_t(const DecodeArgs& a, int num_sms, cudaStream_t s, size_t smem) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<MINB, FEAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)decode_kernel<MINB, FEAT>, 200 * 1024);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<MINB, FEAT>, kDecWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;

@@ -236,11 +236,7 @@ void launch_decode_warp(const DecodeArgs& a, const uint4* wrec, ull n_instr, uin
                         int num_sms, cudaStream_t s) {
   WarpDecodeArgs wa{a, wrec, n_instr, spill, spill_ctr};
   const size_t smem = decode_smem(a);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_optin((const void*)decode_warp_kernel<3>, 200 * 1024);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<3>, kDecWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;

@@ -486,11 +486,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
                                             reinterpret_cast<ull*>(ws.maxc) + 2);
   }
   const size_t smem = segment_chunk_smem();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(seg_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin((const void*)seg_chunk_kernel, (int)smem);
   const ull chunks = (n + kSegCap - 1) / kSegCap;
   if (chunks)
     seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,

@@ -22,9 +22,12 @@
 // used to test the sharded path on a single GPU).
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "shard.cuh"
 
@@ -140,6 +143,12 @@ cudaError_t shard_partition(const ull* keys, ull n, KeyLayout kl, uint32_t nrank
   return cudaStreamSynchronize(s);  // cur[] lives on the host stack
 }
 
+double comm_timeout_s() {
+  const char* e = getenv("THERMO_COMM_TIMEOUT_S");
+  const double v = e ? atof(e) : 0.0;
+  return v > 0 ? v : 600.0;
+}
+
 // ---------------------------------------------------------------------------
 // NCCL transport (one process per GPU)
 // ---------------------------------------------------------------------------
@@ -174,8 +183,38 @@ class NcclComm final : public Comm {
     if (scratch) cudaFree(scratch);
     if (comm) ncclCommDestroy(comm);
   }
+  void abort() override {
+    if (comm) ncclCommAbort(comm);
+    comm = nullptr;
+  }
+  // poll the stream and NCCL's asynchronous error state until the queued work
+  // completes, an error shows, or the deadline passes (then abort the comm)
+  int wait(cudaStream_t s) override {
+    if (!comm) { err = "communicator aborted"; return 2; }
+    const auto t0 = std::chrono::steady_clock::now();
+    const double lim = comm_timeout_s();
+    for (unsigned it = 0;; ++it) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) return 0;
+      if (q != cudaErrorNotReady) return cuda_fail(&err, "stream wait", q);
+      ncclResult_t ar = ncclSuccess;
+      const ncclResult_t r = ncclCommGetAsyncError(comm, &ar);
+      if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+        nccl_fail(&err, "ncclCommGetAsyncError", r != ncclSuccess ? r : ar);
+        abort();
+        return 2;
+      }
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > lim) {
+        err = "collective timed out (THERMO_COMM_TIMEOUT_S); communicator aborted";
+        abort();
+        return 2;
+      }
+      if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+  }
   int allreduce(ull* d, size_t n, bool op_max, cudaStream_t s) override {
     if (!n) return 0;
+    if (!comm) { err = "communicator aborted"; return 2; }
     NCK(ncclAllReduce(d, d, n, ncclUint64, op_max ? ncclMax : ncclSum, comm, s), "ncclAllReduce");
     return 0;
   }
@@ -189,14 +228,15 @@ class NcclComm final : public Comm {
       CCK(cudaMalloc(&scratch, need), "cudaMalloc (allgather scratch)");
       scratch_bytes = need;
     }
+    if (!comm) { err = "communicator aborted"; return 2; }
     CCK(cudaMemcpyAsync(scratch + (size_t)rank * bytes, mine, bytes, cudaMemcpyHostToDevice, s), "allgather H2D");
     NCK(ncclAllGather(scratch + (size_t)rank * bytes, scratch, bytes, ncclUint8, comm, s), "ncclAllGather");
     CCK(cudaMemcpyAsync(all, scratch, need, cudaMemcpyDeviceToHost, s), "allgather D2H");
-    CCK(cudaStreamSynchronize(s), "allgather sync");
-    return 0;
+    return wait(s);
   }
   int alltoallv(const ull* send, const ull* scnt, const ull* sdispl, ull* recv, const ull* rcnt, const ull* rdispl,
                 cudaStream_t s) override {
+    if (!comm) { err = "communicator aborted"; return 2; }
     NCK(ncclGroupStart(), "ncclGroupStart");
     for (int q = 0; q < nranks; ++q) {
       if (q == rank) {
@@ -223,19 +263,33 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0;
   unsigned long gen = 0;
+  bool poisoned = false;  // a rank failed inside a collective, or a barrier timed out
   std::vector<const void*> dptr, hptr;
   std::vector<const ull*> m1, m2;
   explicit LocalGroup(int p) : P(p), refs(p), dptr(p), hptr(p), m1(p), m2(p) {}
-  void barrier() {
+  // false once the group is poisoned (then every later barrier fails at once)
+  bool barrier() {
     std::unique_lock<std::mutex> l(m);
+    if (poisoned) return false;
     const unsigned long g = gen;
     if (++arrived == P) {
       arrived = 0;
       ++gen;
       cv.notify_all();
-    } else {
-      cv.wait(l, [&] { return gen != g; });
+      return true;
     }
+    const auto lim = std::chrono::duration<double>(comm_timeout_s());
+    if (!cv.wait_for(l, lim, [&] { return gen != g || poisoned; })) poisoned = true;
+    if (poisoned) {
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+  void poison() {
+    std::lock_guard<std::mutex> l(m);
+    poisoned = true;
+    cv.notify_all();
   }
 };
 
@@ -271,21 +325,21 @@ class LocalComm final : public Comm {
     CCK(cudaMemcpyAsync(snap, d, n * sizeof(ull), cudaMemcpyDeviceToDevice, s), "allreduce snapshot");
     CCK(cudaStreamSynchronize(s), "allreduce sync");
     g->dptr[rank] = snap;
-    g->barrier();
+    if (!g->barrier()) return peer_fail();
     for (int q = 0; q < nranks; ++q) {
       if (q == rank) continue;
       CCK(cudaMemcpyAsync(tmp, g->dptr[q], n * sizeof(ull), cudaMemcpyDeviceToDevice, s), "allreduce copy");
       launch_reduce_pair(d, tmp, n, op_max, s);
     }
     CCK(cudaStreamSynchronize(s), "allreduce sync");
-    g->barrier();  // peers done reading my snapshot
+    if (!g->barrier()) return peer_fail();  // peers done reading my snapshot
     return 0;
   }
   int allgather_host(const void* mine, size_t bytes, void* all, cudaStream_t) override {
     g->hptr[rank] = mine;
-    g->barrier();
+    if (!g->barrier()) return peer_fail();
     for (int q = 0; q < nranks; ++q) std::memcpy(static_cast<char*>(all) + (size_t)q * bytes, g->hptr[q], bytes);
-    g->barrier();
+    if (!g->barrier()) return peer_fail();
     return 0;
   }
   int alltoallv(const ull* send, const ull* scnt, const ull* sdispl, ull* recv, const ull* rcnt, const ull* rdispl,
@@ -294,13 +348,13 @@ class LocalComm final : public Comm {
     g->dptr[rank] = send;
     g->m1[rank] = scnt;
     g->m2[rank] = sdispl;
-    g->barrier();
+    if (!g->barrier()) return peer_fail();
     for (int q = 0; q < nranks; ++q) {
       const ull cnt = g->m1[q][rank];
       if (cnt != rcnt[q]) {
         err = "alltoallv: receive count mismatch";
-        g->barrier();
-        return 1;
+        g->poison();
+        return 2;
       }
       if (cnt)
         CCK(cudaMemcpyAsync(recv + rdispl[q], static_cast<const ull*>(g->dptr[q]) + g->m2[q][rank], cnt * sizeof(ull),
@@ -308,8 +362,17 @@ class LocalComm final : public Comm {
             "alltoallv copy");
     }
     CCK(cudaStreamSynchronize(s), "alltoallv sync");
-    g->barrier();
+    if (!g->barrier()) return peer_fail();
     return 0;
+  }
+  int wait(cudaStream_t s) override {
+    CCK(cudaStreamSynchronize(s), "stream wait");
+    return 0;
+  }
+  void abort() override { g->poison(); }
+  int peer_fail() {
+    err = "a peer rank failed inside the collective, or it timed out (THERMO_COMM_TIMEOUT_S)";
+    return 2;
   }
 };
 

@@ -24,7 +24,16 @@ class Comm {
   // recv[rdispl[q] .. + rcnt[q]).  Counts and displacements are host arrays.
   virtual int alltoallv(const ull* send, const ull* scnt, const ull* sdispl, ull* recv, const ull* rcnt,
                         const ull* rdispl, cudaStream_t s) = 0;
+  // wait for the stream (and the collectives queued on it) to complete; a
+  // hung or failed peer makes it return 2 after the timeout
+  // (THERMO_COMM_TIMEOUT_S, default 600 s) instead of blocking forever
+  virtual int wait(cudaStream_t s) = 0;
+  // a rank that fails inside a collective call aborts the group, so that its
+  // peers' pending and later collectives return an error instead of hanging
+  virtual void abort() = 0;
 };
+
+double comm_timeout_s();
 
 int nccl_unique_id(void* out128, std::string* msg);
 Comm* make_nccl_comm(const void* id128, int rank, int nranks, std::string* msg);

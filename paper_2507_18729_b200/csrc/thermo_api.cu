@@ -131,6 +131,7 @@ struct thermo_ctx {
   ull h_ctr_g[17] = {};                      // job-wide DevCounters + records (after build)
   bool have_glob = false;
   cudaEvent_t evx[2] = {nullptr, nullptr};  // around the key all-to-all
+  bool in_collective = false;               // inside build / classify of the sharded mode
   float ms_exchange = 0;
   ull exchange_bytes = 0;
 };
@@ -141,9 +142,29 @@ thermo_status fail(thermo_ctx* c, thermo_status st, const std::string& msg) {
   if (c) {
     c->err = msg;
     if (st == THERMO_ECUDA || st == THERMO_ENCCL) c->sticky = st;
+    // a rank failing alone inside a collective call aborts the communicator,
+    // so its peers get an error instead of waiting for it forever (sticky
+    // ENCCL on every rank from then on)
+    if (c->comm && c->in_collective) {
+      c->comm->abort();
+      c->in_collective = false;
+      c->sticky = THERMO_ENCCL;
+    }
   }
   return st;
 }
+// an error every rank of a sharded job detects at the same point (after a
+// collective made it job-wide): no abort, not sticky
+thermo_status fail_job(thermo_ctx* c, thermo_status st, const std::string& msg) {
+  if (c) c->err = msg;
+  return st;
+}
+// marks a sharded build / classify as a collective section
+struct CollectiveScope {
+  thermo_ctx* c;
+  explicit CollectiveScope(thermo_ctx* ctx) : c(ctx) { if (c->comm) c->in_collective = true; }
+  ~CollectiveScope() { c->in_collective = false; }
+};
 
 #define CK(call)                                                                                  \
   do {                                                                                            \
@@ -278,9 +299,9 @@ thermo_status dist_exchange(thermo_ctx* ctx, const DevCounters& hc) {
   CK(cudaMemcpyAsync(ctx->d_tmp, flags, sizeof flags, cudaMemcpyHostToDevice, s));
   DCK(c->allreduce(ctx->d_tmp, 2, false, s));
   CK(cudaMemcpyAsync(flags, ctx->d_tmp, sizeof flags, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  if (flags[0]) return fail(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths (job-wide)");
-  if (flags[1]) return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
+  DCK(c->wait(s));
+  if (flags[0]) return fail_job(ctx, THERMO_ERANGE, "records with launch/warp ids beyond the declared widths (job-wide)");
+  if (flags[1]) return fail_job(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
   // ---- job-wide pc ids: union of the new sites of every rank, appended in sorted order ----
   if (ctx->cfg.track_pc) {
     const uint32_t npc = (uint32_t)std::min<ull>(hc.pc_count, ctx->cfg.max_pcs);
@@ -305,7 +326,7 @@ thermo_status dist_exchange(thermo_ctx* ctx, const DevCounters& hc) {
         ctx->glob_sites.push_back(v);
       }
       if (ctx->glob_sites.size() > ctx->cfg.max_pcs)
-        return fail(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
+        return fail_job(ctx, THERMO_ERANGE, "more distinct (launch, pc) pairs than max_pcs (job-wide)");
       std::vector<uint32_t> map(mine.size());
       for (size_t i = 0; i < mine.size(); ++i) map[i] = ctx->glob_index[mine[i]];
       if (!map.empty())
@@ -344,7 +365,7 @@ thermo_status dist_exchange(thermo_ctx* ctx, const DevCounters& hc) {
   CK(cudaEventRecord(ctx->evx[0], s));
   DCK(c->alltoallv(ctx->sw.alt, scnt.data(), sdispl.data(), ctx->d_keys + ctx->n_exch, rcnt.data(), rdispl.data(), s));
   CK(cudaEventRecord(ctx->evx[1], s));
-  CK(cudaStreamSynchronize(s));
+  DCK(c->wait(s));
   cudaEventElapsedTime(&ctx->ms_exchange, ctx->evx[0], ctx->evx[1]);
   ctx->exchange_bytes = 0;
   for (uint32_t q = 0; q < P; ++q)
@@ -373,7 +394,7 @@ thermo_status dist_combine(thermo_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->d_tmp + 16, &ctx->records, sizeof(ull), cudaMemcpyHostToDevice, s));
   DCK(c->allreduce(ctx->d_tmp, 17, false, s));
   CK(cudaMemcpyAsync(ctx->h_ctr_g, ctx->d_tmp, 17 * sizeof(ull), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  DCK(c->wait(s));
   ctx->have_glob = true;
   return THERMO_OK;
 }
@@ -420,7 +441,10 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
   if (stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
   } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { delete ctx; return THERMO_ECUDA; }
+    // a BLOCKING stream: it waits for work already queued on the legacy default
+    // stream (where e.g. torch writes device-resident records by default), so a
+    // device trace produced there is complete before the first decode reads it
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault) != cudaSuccess) { delete ctx; return THERMO_ECUDA; }
     ctx->own_stream = true;
   }
   if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -798,10 +822,10 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
   // host records: chunks of kWarpChunk instructions copied on the copy stream
   // into two device staging buffers, each copy overlapped with the previous
   // chunk's decode (the device path is one chunk)
-  const ull C = on_device ? (ull)n : std::min<ull>(n, kWarpChunk);
+  // device records are decoded in the same chunks, so the spill space and the
+  // key-buffer growth are bounded by one chunk, not by the whole call
+  const ull C = std::min<ull>(n, kWarpChunk);
   const ull lanes_max = 32 * C;
-  st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * 32 * (ull)n + 64, ctx->n_keys);
-  if (st) return st;
   if (ctx->spill_cap < lanes_max) {  // worst case: every instruction of a chunk spills
     dfree(ctx->d_spill);
     ctx->d_spill = nullptr;
@@ -836,6 +860,10 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
       CK(cudaStreamWaitEvent(s, ctx->ev_copied[b], 0));
       drec = ctx->d_wstage[b];
     }
+    // worst case of this chunk: every lane record emits two keys
+    if ((st = sync_counts(ctx))) return st;
+    st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * 32 * cnt + 64, ctx->n_keys);
+    if (st) return st;
     CK(cudaMemsetAsync(ctx->d_wctr, 0, 2 * sizeof(ull), s));
     DecodeArgs a = decode_args(ctx);
     launch_decode_warp(a, drec, cnt, ctx->d_spill, ctx->d_wctr, ctx->num_sms, s);
@@ -872,6 +900,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   if (g < THERMO_WORD || g > THERMO_BOTH) return fail(ctx, THERMO_EINVAL, "bad granularity");
   if (launch_filter != THERMO_ALL_LAUNCHES && launch_filter >= ctx->cfg.max_launches)
     return fail(ctx, THERMO_EINVAL, "launch_filter beyond max_launches");
+  CollectiveScope coll(ctx);
   DevCounters hc;
   CK(cudaMemcpyAsync(&hc, ctx->d_ctr, sizeof hc, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1235,6 +1264,7 @@ thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, ther
   } else {
     // sharded: each rank scans its own tiles; sums, maxima, tile summaries and
     // verify counts are combined between the steps (collective)
+    CollectiveScope coll(ctx);
     Comm* c = ctx->comm;
     const size_t need = n * kIndSumFields + n + 1;
     if (ctx->red_cap < need) {
@@ -1259,6 +1289,7 @@ thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, ther
     launch_indicator_pack(ctx->d_ind, (uint32_t)n, nullptr, nullptr, sums, 1, s);
     launch_indicator_finalize(a, s);
     ctx->launches += ctx->n_tiles ? 8 : 6;
+    DCK(c->wait(s));
   }
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev1, s));

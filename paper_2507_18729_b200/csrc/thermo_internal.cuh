@@ -9,7 +9,10 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 #include <unordered_map>
 #include <vector>
 
@@ -22,6 +25,20 @@ typedef unsigned long long ull;
 constexpr int kLevels = THERMO_LEVELS;
 constexpr ull kEmptyKey = ~0ull;  // sentinel key (prefix all-ones is reserved)
 constexpr uint32_t kPcNone = 0xFFFFFFFFu;
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the CURRENT device.
+// cudaFuncSetAttribute applies per device (context), so the opt-in is cached per
+// (kernel, device) under a lock: contexts on several devices, or in-process
+// shards driven from several host threads, each get it exactly once.
+inline void smem_optin(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.insert(std::make_pair(func, dev)).second)
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 // ---- device-resident counters (one struct per context) -------------------
 struct DevCounters {

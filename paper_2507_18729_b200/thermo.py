@@ -164,6 +164,19 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def _default_stream(device: int) -> int:
+    """torch's current stream on `device` (records made by torch are ordered
+    before the ingest that reads them).  0 for the legacy default stream: the
+    library's own stream is then a blocking one, ordered after it as well."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return int(torch.cuda.current_stream(device).cuda_stream)
+    except Exception:
+        pass
+    return 0
+
+
 class Thermo:
     """One libthermo context (bound to a CUDA device and stream).
 
@@ -179,6 +192,7 @@ class Thermo:
             return
         cfg = _config(**cfg_kw)
         h = vp()
+        stream = _default_stream(device) if stream is None else stream
         st = self.L.thermo_create(ctypes.byref(h), device, vp(stream) if stream else None, ctypes.byref(cfg))
         if st:
             raise ThermoError(st, "thermo_create")
@@ -192,6 +206,7 @@ class Thermo:
         L = load()
         cfg = _config(**cfg_kw)
         h = vp()
+        stream = _default_stream(device) if stream is None else stream
         idb = ctypes.create_string_buffer(bytes(nccl_id), 128)
         st = L.thermo_create_dist(ctypes.byref(h), device, vp(stream) if stream else None, ctypes.byref(cfg), idb,
                                   rank, nranks)

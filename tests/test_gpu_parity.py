@@ -90,6 +90,36 @@ def test_random_traces(seed, dedup):
         compare(orc, th, t)
 
 
+@pytest.mark.parametrize("dist", ["bimodal", "uniform"])
+@pytest.mark.parametrize("dedup", [1, 2, 3])
+def test_random_hot(dist, dedup):
+    """RandomHot (Fig. 5(f)): 8192 sectors = 4 indicator
+    tiles, ~1.05 M records, word temps 3/29 (bimodal: CV 0.81 -> RandomHot) or
+    3..29 (uniform: CV 0.487 -> Hot) drawn per word.  Every output bit-exact
+    against the oracle, and the label itself asserted."""
+    T = tg.hot_temps(8192, dist)
+    t = tg.hot_spots(T)
+    assert t.n >= 10 ** 5
+    orc, th = run_both(t, dedup=dedup)
+    compare(orc, th, t)
+    want = "RandomHot" if dist == "bimodal" else "Hot"
+    assert oracle.label_names(th.classify()[0]["labels"]) == [want]
+    # shuffled instructions in 3 ingest calls: the same result
+    sh = tg.shuffle_instructions(t.records, 5)
+    calls = [sh[a:b] for a, b in tg.split_calls(t.n, sh, 3)]
+    orc2, th2 = run_both(t, calls=calls, dedup=dedup)
+    compare(orc2, th2, t)
+
+
+@pytest.mark.parametrize("lo,hi,want", [(16, 48, "Hot"), (16, 49, "RandomHot")])
+def test_random_hot_cv_boundary(lo, hi, want):
+    """Population CV exactly 1/2 (16/48) is not 'exceeds': Hot; 16/49: RandomHot."""
+    t = tg.hot_spots(torch.tensor([lo, hi] * (4 * 2048)))
+    orc, th = run_both(t)
+    compare(orc, th, t)
+    assert oracle.label_names(th.classify()[0]["labels"]) == [want]
+
+
 def test_launch_filter_rebuild_and_host_ingest():
     t = tg.random_trace(n=20000, seed=21, n_launches=4)
     t.meta["launches"] = 4

@@ -145,6 +145,57 @@ def test_hot_and_strided_examples():
     assert ind["dom_gap"] == 8 and "Strided" in oracle.label_names(ind["labels"])
 
 
+def _cv(temps):
+    """Population coefficient of variation of the nonzero word temperatures
+    (numpy's std / mean, ddof = 0) -- computed from the DESIGNED temperatures,
+    not from the oracle's output."""
+    x = np.asarray(temps, dtype=np.float64)
+    x = x[x > 0]
+    return float(x.std() / x.mean())
+
+
+@pytest.mark.parametrize("dist", ["bimodal", "uniform", "constant"])
+def test_random_hot_s363(dist):
+    """S:363 / P:404 Fig. 5(f): word temps varying 3..29 per sector, sectors hot.
+    Nested warp sets give word j exactly temps[j] warps and a sector the max of
+    its words (closed form).  The label is RandomHot iff the CV of the nonzero
+    word temps exceeds random_hot_cv = 1/2, else Hot.  Bimodal
+    3/29 draws (CV ~0.81) fire RandomHot; uniform 3..29 draws (CV ~0.487) stay
+    below the default threshold and read Hot (G13); a constant 29 is
+    the CV = 0 hot spot of P:404."""
+    g = PAPER["random_hot"]
+    T = tg.hot_temps(8192, dist, lo=g["word_temp_lo"], hi=g["word_temp_hi"]).numpy()
+    t = tg.hot_spots(T)
+    o = run(t)
+    assert (o.word_counts(0) == T).all()
+    assert (o.sector_counts(0) == T.reshape(-1, 8).max(1)).all()
+    cv = _cv(T)
+    ind = o.classify()[0]
+    # indicator sums against the designed temperatures
+    assert ind["touched_words"] == len(T) and ind["sum_x"] == int(T.sum())
+    assert (ind["sum_x2_hi"] << 64 | ind["sum_x2_lo"]) == int((T.astype(object) ** 2).sum())
+    smax = T.reshape(-1, 8).max(1)
+    assert ind["hot_sectors"] == int((smax >= 16).sum())     # theta_hot = 16, sector = max word
+    want = g["label"] if cv > g["random_hot_cv"] else "Hot"
+    assert labels_of(o, 0) == [want]
+    assert (dist == "bimodal") == (want == "RandomHot")
+
+
+@pytest.mark.parametrize("lo,hi,want", [(16, 48, "Hot"), (16, 49, "RandomHot"), (16, 47, "Hot")])
+def test_random_hot_cv_boundary(lo, hi, want):
+    """Equal numbers of words at lo and hi warps: population CV = (hi-lo)/(hi+lo),
+    exactly 1/2 at 16/48.  S:359 'exceeds' is strict, so CV = 1/2 reads Hot.
+    The sample-std reading (ddof = 1) would give 0.500015 and flip the 16/48
+    case; this pins the population reading of G13."""
+    T = np.tile(np.array([lo, hi], dtype=np.int64), 4 * 2048)
+    cv = _cv(T)
+    assert (cv > 0.5) == (want == "RandomHot")
+    o = run(tg.hot_spots(torch.from_numpy(T)))
+    assert labels_of(o, 0) == [want]
+    o2 = o.classify({"cv_num": 1, "cv_den": 3})   # a lower threshold flips 16/48 too
+    assert oracle.label_names(o2[0]["labels"]) == ["RandomHot"]
+
+
 # ---------------------------------------------------------------- closed forms
 def test_tiny_b_closed_form():
     g = CLOSED["tiny_b"]

@@ -186,7 +186,7 @@ def _lsr(z: torch.Tensor, k: int) -> torch.Tensor:
 
 from .workloads import (  # noqa: E402
     tiny, fig3, fig6, gemm, stencil, spmv, strided_gather, smem_thread_local,
-    smem_warp_broadcast, random_trace, synthetic, random_warp_trace, WORKLOADS,
+    smem_warp_broadcast, random_trace, synthetic, random_warp_trace, hot_temps, hot_spots, WORKLOADS,
 )
 
 __all__ = [
@@ -194,5 +194,5 @@ __all__ = [
     "pack_warp_records", "to_warp_records", "random_warp_trace",
     "instr_starts", "splitmix64", "tiny", "fig3", "fig6", "gemm", "stencil", "spmv",
     "strided_gather", "smem_thread_local", "smem_warp_broadcast", "random_trace",
-    "synthetic", "WORKLOADS",
+    "synthetic", "hot_temps", "hot_spots", "WORKLOADS",
 ]

@@ -400,6 +400,51 @@ def smem_warp_broadcast(blocks=4, device="cpu") -> Trace:
 
 
 # --------------------------------------------------------------------------
+# (random) hot spots: word temperatures drawn per word (Fig. 5(e)/(f);
+# S:363 "word temps varying 3..29 per sector, sectors hot -> RandomHot")
+# --------------------------------------------------------------------------
+def hot_temps(n_sectors=8192, dist="bimodal", seed=0x5EED0006, lo=3, hi=29, device="cpu") -> torch.Tensor:
+    """Designed word temperatures, int64 [8 n_sectors]: "bimodal" draws lo or hi
+    per word (probability 1/2 each), "uniform" draws uniformly from lo..hi,
+    "constant" is hi everywhere (the all-32-warps hot spot of P:404 when hi =
+    32).  Counter-based (splitmix64 keyed by seed and word index)."""
+    dev = torch.device(device)
+    w = torch.arange(8 * n_sectors, dtype=torch.int64, device=dev)
+    r = _lsr(splitmix64(w + _seed_off(seed)), 11)          # 53 random bits
+    if dist == "bimodal":
+        return torch.where((r & 1) == 1, hi, lo)
+    if dist == "uniform":
+        return lo + (r % (hi - lo + 1))
+    if dist == "constant":
+        return torch.full_like(w, hi)
+    raise ValueError(dist)
+
+
+def hot_spots(temps: torch.Tensor, base=0x7A0000000000, pc=0x700, device="cpu") -> Trace:
+    """One global object of len(temps) words; word j is read by the warps
+    0 .. temps[j]-1 (nested warp sets), so by construction word j's distinct-warp
+    count is temps[j] and a sector's is the largest of its 8 words' temps.
+    Warp w runs one 32-lane load per group of 32 consecutive words; lane l is
+    active iff temps[32 g + l] > w (instructions with no active lane are not
+    emitted).  Record order: warps ascending, groups ascending."""
+    dev = torch.device(device)
+    t = torch.as_tensor(temps, dtype=torch.int64, device=dev)
+    nw = t.shape[0]
+    G = (nw + 31) // 32
+    tp = torch.zeros(G * 32, dtype=torch.int64, device=dev)
+    tp[:nw] = t
+    W = int(tp.max())
+    wv = torch.arange(W, dtype=torch.int64, device=dev)[:, None, None]          # [W, 1, 1]
+    j = torch.arange(G * 32, dtype=torch.int64, device=dev).reshape(1, G, 32)    # [1, G, 32]
+    act = (tp.reshape(1, G, 32) > wv).reshape(W * G, 32)
+    A = (base + 4 * j).expand(W, G, 32).reshape(W * G, 32)
+    keep = act.any(1)
+    warp = wv.expand(W, G, 1).reshape(W * G)
+    rec = from_instructions(A[keep], act[keep], warp[keep], pc, KIND_LD, 2)
+    return Trace(f"hot_spots-{nw}", [(base, 4 * nw, SPACE_GLOBAL, 0, "x")], rec, meta=dict(warps=W))
+
+
+# --------------------------------------------------------------------------
 # random fuzz traces (brute-force pins, fuzz parity)
 # --------------------------------------------------------------------------
 def random_trace(n=20000, seed=1, n_objects=5, n_warps=50, n_launches=3, n_pcs=7,
