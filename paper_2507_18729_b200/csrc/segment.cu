@@ -33,157 +33,410 @@ __global__ void seg_hist_kernel(const ull* __restrict__ keys, ull n, KeyLayout k
   for (ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) atomicAdd(&cnt[key_g(keys[i], kl)], 1u);
 }
 
-// ---- 2. exclusive scan of the S_tot counts (3 phases) ----------------------------
-// a "big" sector (>= kSegCap keys) does not fit a chunk: its keys go to a
-// separate buffer (hash path) and its segment here is empty
+constexpr int kGroup = 64;               // sectors per coarse-bucket granule
+// ---- 2. exclusive scans of the S_tot counts (3 phases) ---------------------------
+// Per sector g with c = cnt[g] keys, three running sums:
+//   NL  normal keys  (c < kSegCap)   -> off[g], the sector's segment in the chunked layout
+//   BS  big sectors  (c >= kSegCap)  -> the sector's big index i (its keys go to `big`)
+//   BK  big keys                     -> boff[i], the sector's segment in `big`
+// and, at every coarse bucket boundary (g % 2^cs == 0), the bucket's first key
+// in the coarse layout (NL + BK) and its (NL, BS) starts.
 __device__ __forceinline__ uint32_t seg_len(uint32_t c) { return c >= (uint32_t)kSegCap ? 0u : c; }
 
-__global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __restrict__ bsum,
-                                uint32_t* __restrict__ maxc, ull* __restrict__ nbig) {
-  __shared__ ull s[kSegWarps];
+struct Sum3 {
+  ull nl, bs, bk;
+};
+__device__ __forceinline__ Sum3 sum3_of(uint32_t c) {
+  const bool big = c >= (uint32_t)kSegCap;
+  return Sum3{big ? 0ull : (ull)c, big ? 1ull : 0ull, big ? (ull)c : 0ull};
+}
+__device__ __forceinline__ Sum3 warp_incl_scan3(Sum3 v, int lane) {
+  for (int d = 1; d < 32; d <<= 1) {
+    const ull a = __shfl_up_sync(GFULL, v.nl, d), b = __shfl_up_sync(GFULL, v.bs, d),
+              c = __shfl_up_sync(GFULL, v.bk, d);
+    if (lane >= d) { v.nl += a; v.bs += b; v.bk += c; }
+  }
+  return v;
+}
+
+__global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __restrict__ bsum3,
+                                uint32_t* __restrict__ maxc) {
+  __shared__ ull s[3][kSegWarps];
   __shared__ uint32_t smax[kSegWarps];
   const ull base = (ull)blockIdx.x * kScanBlock;
-  ull t = 0, big = 0;
+  Sum3 t{0, 0, 0};
   uint32_t mx = 0;
   for (int i = threadIdx.x; i < kScanBlock; i += kSegThreads) {
     const ull j = base + i;
     const uint32_t v = j < n ? in[j] : 0u;
-    t += seg_len(v);
-    big += v - seg_len(v);
+    const Sum3 q = sum3_of(v);
+    t.nl += q.nl; t.bs += q.bs; t.bk += q.bk;
     mx = v > mx ? v : mx;
   }
-  for (int d = 16; d; d >>= 1) big += __shfl_xor_sync(GFULL, big, d);
-  if ((threadIdx.x & 31) == 0 && big) atomicAdd(nbig, big);
   for (int d = 16; d; d >>= 1) {
-    t += __shfl_xor_sync(GFULL, t, d);
+    t.nl += __shfl_xor_sync(GFULL, t.nl, d);
+    t.bs += __shfl_xor_sync(GFULL, t.bs, d);
+    t.bk += __shfl_xor_sync(GFULL, t.bk, d);
     const uint32_t o = __shfl_xor_sync(GFULL, mx, d);
     mx = o > mx ? o : mx;
   }
-  if ((threadIdx.x & 31) == 0) { s[threadIdx.x >> 5] = t; smax[threadIdx.x >> 5] = mx; }
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = t.nl; s[1][threadIdx.x >> 5] = t.bs; s[2][threadIdx.x >> 5] = t.bk;
+    smax[threadIdx.x >> 5] = mx;
+  }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 3) {
     ull a = 0;
+    for (int i = 0; i < kSegWarps; ++i) a += s[threadIdx.x][i];
+    bsum3[3 * blockIdx.x + threadIdx.x] = a;
+  }
+  if (threadIdx.x == 0) {
     uint32_t m = 0;
-    for (int i = 0; i < kSegWarps; ++i) { a += s[i]; m = smax[i] > m ? smax[i] : m; }
-    bsum[blockIdx.x] = a;
+    for (int i = 0; i < kSegWarps; ++i) m = smax[i] > m ? smax[i] : m;
     atomicMax(maxc, m);
   }
 }
 
-// one block: exclusive scan of the block sums; writes the grand total to *total
-__global__ void seg_scan_blocks(ull* bsum, ull nb, ull* total) {
-  __shared__ ull carry;
-  __shared__ ull ws[kSegWarps];
-  if (threadIdx.x == 0) carry = 0;
+// one block: exclusive scan of the block sums (three columns); totals -> tot[0..3)
+__global__ void seg_scan_blocks(ull* bsum3, ull nb, ull* tot) {
+  __shared__ ull carry[3];
+  __shared__ ull ws[3][kSegWarps];
+  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (ull b0 = 0; b0 < nb; b0 += kSegThreads) {
     const ull i = b0 + threadIdx.x;
-    const ull v = i < nb ? bsum[i] : 0;
+    const Sum3 v = i < nb ? Sum3{bsum3[3 * i], bsum3[3 * i + 1], bsum3[3 * i + 2]} : Sum3{0, 0, 0};
+    const Sum3 incl = warp_incl_scan3(v, lane);
+    if (lane == 31) { ws[0][w] = incl.nl; ws[1][w] = incl.bs; ws[2][w] = incl.bk; }
+    __syncthreads();
+    Sum3 pre{carry[0], carry[1], carry[2]};
+    for (int k = 0; k < w; ++k) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
+    if (i < nb) {
+      bsum3[3 * i] = pre.nl + incl.nl - v.nl;
+      bsum3[3 * i + 1] = pre.bs + incl.bs - v.bs;
+      bsum3[3 * i + 2] = pre.bk + incl.bk - v.bk;
+    }
+    __syncthreads();
+    if (threadIdx.x == kSegThreads - 1) {
+      carry[0] = pre.nl + incl.nl; carry[1] = pre.bs + incl.bs; carry[2] = pre.bk + incl.bk;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) tot[threadIdx.x] = carry[threadIdx.x];
+}
+
+// off[g] (normal-key prefix), dst[g] = chunk of g's normal keys, or 0x80000000
+// | big index for a big sector (then bg[i] = g, boff[i] = big-key prefix);
+// gpre[q] = (NL, BS, BK) at the first sector of group q (kGroup sectors)
+__global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum3,
+                               ull* __restrict__ off, uint32_t* __restrict__ dst, ull* __restrict__ bg,
+                               ull* __restrict__ boff, ull* __restrict__ gpre) {
+  __shared__ ull ws[3][kSegWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
+  uint32_t v[8];
+  Sum3 t{0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const ull j = base + k;
+    v[k] = j < n ? in[j] : 0u;
+    const Sum3 q = sum3_of(v[k]);
+    t.nl += q.nl; t.bs += q.bs; t.bk += q.bk;
+  }
+  const Sum3 incl = warp_incl_scan3(t, lane);
+  if (lane == 31) { ws[0][w] = incl.nl; ws[1][w] = incl.bs; ws[2][w] = incl.bk; }
+  __syncthreads();
+  Sum3 pre{bsum3[3 * blockIdx.x], bsum3[3 * blockIdx.x + 1], bsum3[3 * blockIdx.x + 2]};
+  for (int k = 0; k < w; ++k) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
+  pre.nl += incl.nl - t.nl; pre.bs += incl.bs - t.bs; pre.bk += incl.bk - t.bk;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const ull j = base + k;
+    if (j < n) {
+      off[j] = pre.nl;
+      const bool big = v[k] >= (uint32_t)kSegCap;
+      if (big) {
+        dst[j] = 0x80000000u | (uint32_t)pre.bs;
+        bg[pre.bs] = j;
+        boff[pre.bs] = pre.bk;
+      } else {
+        dst[j] = (uint32_t)(pre.nl / (ull)kSegCap);
+      }
+      if ((j & (kGroup - 1)) == 0) {
+        gpre[3 * (j / kGroup)] = pre.nl;
+        gpre[3 * (j / kGroup) + 1] = pre.bs;
+        gpre[3 * (j / kGroup) + 2] = pre.bk;
+      }
+    }
+    const Sum3 q = sum3_of(v[k]);
+    pre.nl += q.nl; pre.bs += q.bs; pre.bk += q.bk;
+  }
+}
+
+// coarse buckets balanced by key count: group q (kGroup sectors) goes to
+// bucket cb[q] = (keys before q) * ncoarse / n, non-decreasing in q; bucket b
+// starts at its first group's prefixes (cstart = all keys, cinfo = (NL, BS));
+// buckets no group maps to are empty (the next group's / the totals' start)
+__global__ void seg_groups_kernel(const ull* __restrict__ gpre, ull ngroups, const ull* __restrict__ tot,
+                                  uint32_t ncoarse, uint16_t* __restrict__ cb, ull* __restrict__ cstart,
+                                  ull* __restrict__ cinfo) {
+  const ull q = (ull)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q > ngroups) return;
+  const ull n = tot[0] + tot[2];
+  auto bucket = [&](ull qq) -> uint32_t {
+    if (qq >= ngroups) return ncoarse;
+    const ull p = gpre[3 * qq] + gpre[3 * qq + 2];
+    const ull b = n ? (ull)(((unsigned __int128)p * ncoarse) / n) : 0ull;
+    return (uint32_t)(b < ncoarse ? b : ncoarse - 1);
+  };
+  const uint32_t bq = bucket(q);
+  if (q < ngroups) cb[q] = (uint16_t)bq;
+  const uint32_t bp = q == 0 ? 0u : bucket(q - 1) + 1;  // buckets (bucket(q-1), bucket(q)] start here
+  const ull nl = q < ngroups ? gpre[3 * q] : tot[0], bs = q < ngroups ? gpre[3 * q + 1] : tot[1];
+  const ull all = q < ngroups ? gpre[3 * q] + gpre[3 * q + 2] : n;
+  for (uint32_t b = bp; b <= bq; ++b) {
+    cstart[b] = all;
+    cinfo[2 * b] = nl;
+    cinfo[2 * b + 1] = bs;
+  }
+}
+
+// ---- 3. two-pass partition of the keys into chunks and big sectors ----------------
+// A single scatter to ~n / 2048 chunk cursors writes 8-byte keys to random
+// places through a dependent key -> chunk -> cursor-atomic chain (ncu: 9 %
+// issue-active, long-scoreboard bound).  Instead, two onesweep-style passes
+// with <= 4096 destinations each: a tile of 4096 keys is ranked by destination
+// in shared memory, takes one cursor atomic per destination present, is staged
+// in destination order and written out in runs.
+//   pass 1: coarse bucket b = cb[g / kGroup] (<= kCoarse buckets balanced by
+//           key count, so each holds about n / kCoarse keys), into `tmp`;
+//   pass 2: per coarse bucket, the key's chunk or big sector, into `out` / `big`
+//           (a bucket's chunks and big sectors are consecutive ids, and the
+//           chunk-of-sector lookups stay within the bucket's sector range).
+constexpr int kCoarse = 1024;
+constexpr int kPT = 256;                 // partition threads
+constexpr int kPPer = 16;                // keys per thread
+constexpr int kPTile = kPT * kPPer;      // 4096 keys per tile
+constexpr int kFineBins = 4096;          // pass-2 destinations per bucket (more: direct scatter)
+
+// block-wide exclusive scan of cnt[0, nbins) into excl (nbins <= kFineBins), returns the total
+__device__ __forceinline__ uint32_t block_excl_scan(const uint32_t* cnt, uint32_t* excl, uint32_t nbins,
+                                                    uint32_t* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int per = kFineBins / kPT;  // 16 bins per thread
+  const uint32_t b0 = threadIdx.x * per;
+  uint32_t loc[per];
+  uint32_t t = 0;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    loc[k] = b0 + k < nbins ? cnt[b0 + k] : 0u;
+    t += loc[k];
+  }
+  uint32_t incl = t;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(GFULL, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  uint32_t pre = 0, tot = 0;
+  for (int k = 0; k < kPT / 32; ++k) {
+    pre += k < w ? wsum[k] : 0u;
+    tot += wsum[k];
+  }
+  pre += incl - t;
+#pragma unroll
+  for (int k = 0; k < per; ++k) {
+    if (b0 + k < nbins) excl[b0 + k] = pre;
+    pre += loc[k];
+  }
+  __syncthreads();
+  return tot;
+}
+
+struct PartSmem {
+  uint32_t cnt[kFineBins];
+  uint32_t excl[kFineBins];
+  ull base[kFineBins];
+  ull stage[kPTile];
+  uint16_t sd[kPTile];  // pass 2: the staged key's destination
+  uint32_t wsum[kPT / 32];
+};
+
+// pass 1: tiles of 4096 keys -> coarse buckets
+__global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
+                                                         const uint16_t* __restrict__ cb, uint32_t ncoarse,
+                                                         ull* __restrict__ ccur, ull* __restrict__ tmp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  for (ull t0 = (ull)blockIdx.x * kPTile; t0 < n; t0 += (ull)gridDim.x * kPTile) {
+    for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT) sm.cnt[i] = 0;
+    __syncthreads();
+    ull k[kPPer];
+    uint32_t b[kPPer], r[kPPer];
+#pragma unroll
+    for (int u = 0; u < kPPer; ++u) {
+      const ull i = t0 + (ull)u * kPT + threadIdx.x;
+      k[u] = i < n ? keys[i] : 0ull;
+      b[u] = i < n ? (uint32_t)cb[key_g(k[u], kl) / kGroup] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < kPPer; ++u) {
+      const unsigned peers = __match_any_sync(GFULL, b[u]);
+      const int ldr = __ffs(peers) - 1;
+      uint32_t r0 = 0;
+      if (b[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[b[u]], (uint32_t)__popc(peers));
+      r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT)
+      if (sm.cnt[i]) sm.base[i] = atomicAdd(&ccur[i], (ull)sm.cnt[i]);
+    const uint32_t tot = block_excl_scan(sm.cnt, sm.excl, ncoarse, sm.wsum);
+#pragma unroll
+    for (int u = 0; u < kPPer; ++u)
+      if (b[u] != 0xFFFFFFFFu) {
+        const uint32_t q = sm.excl[b[u]] + r[u];
+        sm.stage[q] = k[u];
+        sm.sd[q] = (uint16_t)b[u];
+      }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tot; i += kPT) {
+      const uint32_t bb = sm.sd[i];
+      tmp[sm.base[bb] + (i - sm.excl[bb])] = sm.stage[i];
+    }
+    __syncthreads();
+  }
+}
+
+// tiles of every coarse bucket (tpre[b] = first tile of bucket b) and the
+// sentinels of the bucket tables; one block
+__global__ void seg_tiles_kernel(const ull* __restrict__ tot, uint32_t ncoarse, ull* __restrict__ cstart,
+                                 ull* __restrict__ cinfo, ull* __restrict__ ccur, ull* __restrict__ tpre,
+                                 ull* __restrict__ off, ull nsec) {
+  __shared__ ull carry;
+  __shared__ ull wsum[kSegWarps];
+  if (threadIdx.x == 0) {
+    off[nsec] = tot[0];  // end of the last normal segment
+    carry = 0;
+  }
+  (void)cinfo;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t b0 = 0; b0 < ncoarse; b0 += kSegThreads) {
+    const uint32_t b = b0 + threadIdx.x;
+    ull v = 0;
+    if (b < ncoarse) {
+      v = (cstart[b + 1] - cstart[b] + kPTile - 1) / kPTile;
+      ccur[b] = cstart[b];
+    }
     ull incl = v;
     for (int d = 1; d < 32; d <<= 1) {
       const ull o = __shfl_up_sync(GFULL, incl, d);
       if (lane >= d) incl += o;
     }
-    if (lane == 31) ws[w] = incl;
+    if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    ull wpre = 0;
-    for (int k = 0; k < w; ++k) wpre += ws[k];
-    const ull c = carry;
-    if (i < nb) bsum[i] = c + wpre + incl - v;
+    ull pre = carry;
+    for (int k = 0; k < w; ++k) pre += wsum[k];
+    if (b < ncoarse) tpre[b] = pre + incl - v;
     __syncthreads();
-    if (threadIdx.x == kSegThreads - 1) carry = c + wpre + incl;
+    if (threadIdx.x == kSegThreads - 1) carry = pre + incl;
     __syncthreads();
   }
-  if (threadIdx.x == 0) *total = carry;
+  if (threadIdx.x == 0) tpre[ncoarse] = carry;
 }
 
-// off[j] = exclusive prefix of cnt; dst[j] = the chunk sector j's keys go to
-// (the one its segment starts in; ~0 for a big sector)
-__global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum,
-                               ull* __restrict__ off, uint32_t* __restrict__ dst) {
-  __shared__ ull ws[kSegWarps];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
-  uint32_t v[8];
-  bool bg[8];
-  ull t = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const ull j = base + k;
-    const uint32_t c = j < n ? in[j] : 0u;
-    v[k] = seg_len(c);
-    bg[k] = c >= (uint32_t)kSegCap;
-    t += v[k];
-  }
-  ull incl = t;
-  for (int d = 1; d < 32; d <<= 1) {
-    const ull o = __shfl_up_sync(GFULL, incl, d);
-    if (lane >= d) incl += o;
-  }
-  if (lane == 31) ws[w] = incl;
-  __syncthreads();
-  ull pre = bsum[blockIdx.x];
-  for (int k = 0; k < w; ++k) pre += ws[k];
-  pre += incl - t;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const ull j = base + k;
-    if (j < n) {
-      off[j] = pre;
-      dst[j] = bg[k] ? 0xFFFFFFFFu : (uint32_t)(pre / (ull)kSegCap);
-    }
-    pre += v[k];
-  }
-}
-
-// ---- 3. scatter keys into their sector's segment ------------------------------------
-// 8 keys per thread with their 8 cursor atomics in flight together: the
-// atomics' latency (contended cursors of hot sectors), not bandwidth, bounds it
-constexpr int kScatterPer = 8;
-__global__ void __launch_bounds__(256) seg_scatter_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
-                                                          const uint32_t* __restrict__ dst, ull* __restrict__ cur,
-                                                          ull* __restrict__ out, ull* __restrict__ big,
-                                                          ull* __restrict__ nbig_ctr) {
+// pass 2: tile t of coarse bucket b -> its chunks (out) and big sectors (big)
+__global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict__ tmp, KeyLayout kl,
+                                                       uint32_t ncoarse, const ull* __restrict__ cstart,
+                                                       const ull* __restrict__ cinfo, const ull* __restrict__ tpre,
+                                                       const uint32_t* __restrict__ dst, ull* __restrict__ cur,
+                                                       ull* __restrict__ bcur, ull* __restrict__ out,
+                                                       ull* __restrict__ big) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
   const int lane = threadIdx.x & 31;
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  const ull tile = (ull)blockDim.x * kScatterPer;
-  for (ull t0 = (ull)blockIdx.x * tile; t0 < n; t0 += (ull)gridDim.x * tile) {
-    ull k[kScatterPer], pos[kScatterPer];
-    uint32_t d[kScatterPer];
-    const ull i0 = t0 + threadIdx.x;
+  const ull t = blockIdx.x;
+  if (t >= tpre[ncoarse]) return;
+  uint32_t lo = 0, hi = ncoarse;  // bucket b: tpre[b] <= t < tpre[b + 1]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (tpre[mid] <= t) lo = mid; else hi = mid;
+  }
+  const uint32_t b = lo;
+  const ull k0 = cstart[b] + (t - tpre[b]) * kPTile;
+  const ull k1 = k0 + kPTile < cstart[b + 1] ? k0 + kPTile : cstart[b + 1];
+  const ull nl0 = cinfo[2 * b], nl1 = cinfo[2 * b + 2];
+  const ull bs0 = cinfo[2 * b + 1], bs1 = cinfo[2 * b + 3];
+  const ull c_lo = nl0 / kSegCap;
+  const uint32_t nbn = nl1 > nl0 ? (uint32_t)((nl1 - 1) / kSegCap - c_lo + 1) : 0u;  // chunk bins
+  const uint32_t nbins = nbn + (uint32_t)(bs1 - bs0);
+  ull k[kPPer];
+  uint32_t d[kPPer], r[kPPer];
 #pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) k[u] = i0 + (ull)u * blockDim.x < n ? keys[i0 + (ull)u * blockDim.x] : 0;
-    // one 4-byte read per key: the key's chunk (chunk cursors stay
-    // cache-resident however many sectors there are) or ~0 for a big sector
+  for (int u = 0; u < kPPer; ++u) {
+    const ull i = k0 + (ull)u * kPT + threadIdx.x;
+    k[u] = i < k1 ? tmp[i] : 0ull;
+  }
 #pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) d[u] = i0 + (ull)u * blockDim.x < n ? dst[key_g(k[u], kl)] : 0xFFFFFFFEu;
-    // warp-aggregated cursor atomics: lanes holding keys of the same chunk take
-    // consecutive positions from one atomic by their lowest lane
-    unsigned peers[kScatterPer];
-#pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) peers[u] = __match_any_sync(GFULL, d[u]);
-#pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) {
-      pos[u] = 0;
-      if (d[u] < 0xFFFFFFFEu && lane == __ffs(peers[u]) - 1) pos[u] = atomicAdd(&cur[d[u]], (ull)__popc(peers[u]));
+  for (int u = 0; u < kPPer; ++u) {
+    const ull i = k0 + (ull)u * kPT + threadIdx.x;
+    uint32_t dd = 0xFFFFFFFFu;
+    if (i < k1) {
+      const uint32_t x = dst[key_g(k[u], kl)];
+      dd = (x & 0x80000000u) ? nbn + ((x & 0x7FFFFFFFu) - (uint32_t)bs0) : x - (uint32_t)c_lo;
     }
+    d[u] = dd;
+  }
+  if (nbins > (uint32_t)kFineBins) {
+    // too many destinations for one tile's histogram: per-key cursor atomics
+    // (warp-aggregated), written directly
 #pragma unroll
-    for (int u = 0; u < kScatterPer; ++u)
-      pos[u] = __shfl_sync(GFULL, pos[u], __ffs(peers[u]) - 1) + __popc(peers[u] & lt);
-#pragma unroll
-    for (int u = 0; u < kScatterPer; ++u) {
-      const bool isbig = d[u] == 0xFFFFFFFFu;
-      const unsigned bb = __ballot_sync(GFULL, isbig);  // big keys: one append per warp
-      if (bb) {
-        ull b0 = 0;
-        if (lane == __ffs(bb) - 1) b0 = atomicAdd(nbig_ctr, (ull)__popc(bb));
-        b0 = __shfl_sync(GFULL, b0, __ffs(bb) - 1);
-        if (isbig) big[b0 + __popc(bb & lt)] = k[u];
+    for (int u = 0; u < kPPer; ++u) {
+      const unsigned peers = __match_any_sync(GFULL, d[u]);
+      const int ldr = __ffs(peers) - 1;
+      ull p0 = 0;
+      if (d[u] != 0xFFFFFFFFu && lane == ldr) {
+        ull* c = d[u] < nbn ? &cur[c_lo + d[u]] : &bcur[bs0 + d[u] - nbn];
+        p0 = atomicAdd(c, (ull)__popc(peers));
       }
-      if (d[u] < 0xFFFFFFFEu) out[pos[u]] = k[u];
+      const ull pos = __shfl_sync(GFULL, p0, ldr) + __popc(peers & lt);
+      if (d[u] != 0xFFFFFFFFu) (d[u] < nbn ? out : big)[pos] = k[u];
     }
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < nbins; i += kPT) sm.cnt[i] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kPPer; ++u) {
+    const unsigned peers = __match_any_sync(GFULL, d[u]);
+    const int ldr = __ffs(peers) - 1;
+    uint32_t r0 = 0;
+    if (d[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[d[u]], (uint32_t)__popc(peers));
+    r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(peers & lt);
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nbins; i += kPT)
+    if (sm.cnt[i]) sm.base[i] = atomicAdd(i < nbn ? &cur[c_lo + i] : &bcur[bs0 + i - nbn], (ull)sm.cnt[i]);
+  const uint32_t tot = block_excl_scan(sm.cnt, sm.excl, nbins, sm.wsum);
+  // stage in destination order (with each key's destination), then write runs
+#pragma unroll
+  for (int u = 0; u < kPPer; ++u)
+    if (d[u] != 0xFFFFFFFFu) {
+      const uint32_t q = sm.excl[d[u]] + r[u];
+      sm.stage[q] = k[u];
+      sm.sd[q] = (uint16_t)d[u];
+    }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < tot; i += kPT) {
+    const uint32_t dd = sm.sd[i];
+    (dd < nbn ? out : big)[sm.base[dd] + (i - sm.excl[dd])] = sm.stage[i];
   }
 }
 
@@ -421,6 +674,204 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   (void)nsec;
 }
 
+// ---- 5. big sectors (>= kSegCap keys: the hot x sectors of SpMV hold up to
+// 620 k keys of 138 k warps) ---------------------------------------------------
+// A big sector's keys big[boff[i], boff[i + 1]) are split into P_i = ceil(K_i /
+// kBigFill) passes by a hash of the (launch, warp) id, so that every distinct
+// warp lands in exactly one pass; one CTA per (sector, pass) collects its
+// warps' OR-ed masks in a shared-memory hash set and adds its entries to the
+// sector's counts (P:325 flush: sector count = distinct warps, word count =
+// those with the bit).  A second kernel, once the counts are final, collects
+// the sector's distinct pc ids (split the same way) and bins them at the
+// sector's and words' levels (G11).  All CTAs run in parallel: a CTA re-reads
+// its sector's keys (L2-resident) instead of one CTA looping over P passes.
+constexpr int kBigSlots = 8192;          // 64 KB table
+constexpr uint32_t kBigFill = 6144;      // keys per pass (load <= 3/4)
+__device__ __forceinline__ uint32_t big_pass_of(ull id, uint32_t P) {
+  return P <= 1 ? 0u : __umulhi((uint32_t)((id * 0xD6E8FEB86659FD93ull) >> 32), P);
+}
+// table of tb = log2(slots) bits, sized to the pass's keys (a CTA clears and
+// scans only what it uses)
+// returns false when the table is full (the pass drew far more distinct ids
+// than its share: reported as a hash overflow, never a wrong count)
+__device__ __forceinline__ bool big_or(ull* tab, uint32_t tb, ull id, uint32_t m) {
+  const uint32_t tmask = (1u << tb) - 1;
+  uint32_t h = (uint32_t)((id * 0x9E3779B97F4A7C15ull) >> (64 - tb));
+  const ull v = (id << 8) | m;
+  for (uint32_t probe = 0; probe <= tmask; ++probe) {
+    ull cur = tab[h];
+    if (cur == kHEmpty) {
+      cur = atomicCAS(&tab[h], kHEmpty, v);
+      if (cur == kHEmpty) return true;
+    }
+    if ((cur >> 8) == id) {
+      if (((uint32_t)cur & m) != m) atomicOr(reinterpret_cast<uint32_t*>(&tab[h]), m);
+      return true;
+    }
+    h = (h + 1) & tmask;
+  }
+  return false;
+}
+__device__ __forceinline__ uint32_t big_table_bits(uint32_t keys_per_pass) {
+  uint32_t tb = 8;
+  while ((1u << tb) * 3u < keys_per_pass * 4u && (1u << tb) < (uint32_t)kBigSlots) ++tb;
+  return tb;
+}
+
+// passes of every big sector: pre[i] = first CTA of sector i (pre[n] = total);
+// kind 0: main-key passes ceil(K / fill), kind 1: pc passes ceil(min(K, npc) / fill)
+__global__ void seg_big_plan_kernel(const ull* __restrict__ boff, const ull* __restrict__ tot, ull npc,
+                                    ull* __restrict__ pre_main, ull* __restrict__ pre_pc) {
+  __shared__ ull carry[2];
+  __shared__ ull wsum[2][kSegWarps];
+  const ull nbs = tot[1];
+  if (threadIdx.x < 2) carry[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (ull b0 = 0; b0 < nbs; b0 += kSegThreads) {
+    const ull i = b0 + threadIdx.x;
+    ull v0 = 0, v1 = 0;
+    if (i < nbs) {
+      const ull K = (i + 1 < nbs ? boff[i + 1] : tot[2]) - boff[i];
+      v0 = (K + kBigFill - 1) / kBigFill;
+      const ull kp = K < npc ? K : npc;
+      v1 = (kp + kBigFill - 1) / kBigFill;
+    }
+    ull i0 = v0, i1 = v1;
+    for (int d = 1; d < 32; d <<= 1) {
+      const ull a = __shfl_up_sync(GFULL, i0, d), b = __shfl_up_sync(GFULL, i1, d);
+      if (lane >= d) { i0 += a; i1 += b; }
+    }
+    if (lane == 31) { wsum[0][w] = i0; wsum[1][w] = i1; }
+    __syncthreads();
+    ull p0 = carry[0], p1 = carry[1];
+    for (int k = 0; k < w; ++k) { p0 += wsum[0][k]; p1 += wsum[1][k]; }
+    if (i < nbs) { pre_main[i] = p0 + i0 - v0; pre_pc[i] = p1 + i1 - v1; }
+    __syncthreads();
+    if (threadIdx.x == kSegThreads - 1) { carry[0] = p0 + i0; carry[1] = p1 + i1; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { pre_main[nbs] = carry[0]; pre_pc[nbs] = carry[1]; }
+}
+
+// CTA t -> (big sector i, pass p): pre[i] <= t < pre[i + 1]
+__device__ __forceinline__ bool big_cta(const ull* pre, ull nbs, ull t, ull& i, uint32_t& p, uint32_t& P) {
+  if (t >= pre[nbs]) return false;
+  ull lo = 0, hi = nbs;
+  while (hi - lo > 1) {
+    const ull mid = (lo + hi) >> 1;
+    if (pre[mid] <= t) lo = mid; else hi = mid;
+  }
+  i = lo;
+  p = (uint32_t)(t - pre[lo]);
+  P = (uint32_t)(pre[lo + 1] - pre[lo]);
+  return true;
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restrict__ big,
+                                                             const ull* __restrict__ boff,
+                                                             const ull* __restrict__ bg, const ull* __restrict__ tot,
+                                                             const ull* __restrict__ pre, KeyLayout kl,
+                                                             uint32_t filter, uint32_t* __restrict__ wc,
+                                                             uint32_t* __restrict__ sc, DevCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots]
+  __shared__ uint32_t s_cnt[9];
+  const ull nbs = tot[1];
+  ull i;
+  uint32_t p, P;
+  if (!big_cta(pre, nbs, blockIdx.x, i, p, P)) return;
+  const ull g = bg[i];
+  const ull b0 = boff[i], b1 = (i + 1 < nbs) ? boff[i + 1] : tot[2];
+  const uint32_t K = (uint32_t)(b1 - b0);
+  const uint32_t LW = kl.L + kl.W, RS = 8 + kl.P;
+  const ull lwmask = (1ull << LW) - 1;
+  if (threadIdx.x < 9) s_cnt[threadIdx.x] = 0;
+  const uint32_t tb = big_table_bits((K + P - 1) / P + 64);
+  const int T = 1 << tb;
+  for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
+    const ull k = big[b0 + j];
+    const ull id = (k >> RS) & lwmask;
+    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
+    if (big_pass_of(id, P) != p) continue;
+    if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+  }
+  __syncthreads();
+  uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs = 0;
+  for (int j = threadIdx.x; j < T; j += kSegThreads) {
+    const ull v = tab[j];
+    if (v == kHEmpty) continue;
+    ++cs;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cw[b] += ((uint32_t)v >> b) & 1u;
+  }
+  for (int d = 16; d; d >>= 1) {
+    cs += __shfl_xor_sync(GFULL, cs, d);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) cw[b] += __shfl_xor_sync(GFULL, cw[b], d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_cnt[8], cs);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) atomicAdd(&s_cnt[b], cw[b]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 9 && s_cnt[threadIdx.x]) {
+    // several passes of one sector add up (the dense arrays start at 0)
+    atomicAdd(threadIdx.x == 8 ? &sc[g] : &wc[8 * g + threadIdx.x], s_cnt[threadIdx.x]);
+    if (threadIdx.x == 8) atomicAdd(&ctr->distinct_pairs, (ull)s_cnt[8]);
+  }
+}
+
+__global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __restrict__ big,
+                                                                const ull* __restrict__ boff,
+                                                                const ull* __restrict__ bg,
+                                                                const ull* __restrict__ tot,
+                                                                const ull* __restrict__ pre, KeyLayout kl,
+                                                                uint32_t filter, const uint32_t* __restrict__ wc,
+                                                                const uint32_t* __restrict__ sc,
+                                                                const uint32_t* __restrict__ site_of,
+                                                                ull* __restrict__ pc_hist, DevCounters* ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots]
+  const ull nbs = tot[1];
+  ull i;
+  uint32_t p, P;
+  if (!big_cta(pre, nbs, blockIdx.x, i, p, P)) return;
+  const ull g = bg[i];
+  const ull b0 = boff[i], b1 = (i + 1 < nbs) ? boff[i + 1] : tot[2];
+  const uint32_t K = (uint32_t)(b1 - b0);
+  const ull pmask = (1ull << kl.P) - 1;
+  const uint32_t kp = K < (1u << kl.P) ? K : (1u << kl.P);
+  const uint32_t tb = big_table_bits((kp + P - 1) / P + 64);
+  const int T = 1 << tb;
+  for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
+    const ull k = big[b0 + j];
+    const ull id = (k >> 8) & pmask;
+    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) continue;
+    if (big_pass_of(id, P) != p) continue;
+    if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+  }
+  __syncthreads();
+  const uint32_t scnt = sc[g];
+  uint32_t npc = 0;
+  for (int j = threadIdx.x; j < T; j += kSegThreads) {
+    const ull v = tab[j];
+    if (v == kHEmpty) continue;
+    ++npc;
+    const uint32_t pcid = (uint32_t)(v >> 8);
+    atomicAdd(&pc_hist[(pcid * 2 + 1) * kLevels + level_of_g(scnt)], 1ull);
+    for (uint32_t m = (uint32_t)v & 0xFFu; m; m &= m - 1)
+      atomicAdd(&pc_hist[(pcid * 2) * kLevels + level_of_g(wc[8 * g + __ffs(m) - 1])], 1ull);
+  }
+  for (int d = 16; d; d >>= 1) npc += __shfl_xor_sync(GFULL, npc, d);
+  if ((threadIdx.x & 31) == 0 && npc) atomicAdd(&ctr->distinct_pc, (ull)npc);
+}
+
 static size_t segment_chunk_smem() {
   return (size_t)kHSlots * sizeof(ull) + ((size_t)kHWin * 5 + 2 * kPcBins) * sizeof(uint32_t) +
          2 * kSegCap * sizeof(uint16_t);
@@ -440,10 +891,20 @@ cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
     if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cs0, (nsec + 2) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.dst, (nsec + 1) * sizeof(uint32_t)))) return e;
-    if ((e = cudaMalloc(&ws.bsum, ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.bsum, 3 * ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
+    cudaFree(ws.gpre); cudaFree(ws.cb);
+    ws.gpre = nullptr; ws.cb = nullptr;
+    if ((e = cudaMalloc(&ws.gpre, 3 * ((nsec + kGroup - 1) / kGroup + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cb, ((nsec + kGroup - 1) / kGroup + 1) * sizeof(uint16_t)))) return e;
     ws.cap_sec = nsec + 1;
   }
-  if (!ws.maxc && (e = cudaMalloc(&ws.maxc, 4 * sizeof(ull)))) return e;  // maxc, big total, big cursor
+  if (!ws.maxc && (e = cudaMalloc(&ws.maxc, 8 * sizeof(ull)))) return e;  // maxc | totals NL, BS, BK
+  if (!ws.cstart) {
+    if ((e = cudaMalloc(&ws.cstart, (kCoarse + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cinfo, 2 * (kCoarse + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.ccur, kCoarse * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.tpre, (kCoarse + 1) * sizeof(ull)))) return e;
+  }
   return cudaSuccess;
 }
 
@@ -451,7 +912,7 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
                             cudaStream_t s, uint32_t* max_per_sector, ull* n_big, bool counted) {
   cudaError_t e;
   if ((e = segment_reserve(ws, nsec))) return e;
-  cudaMemsetAsync(ws.maxc, 0, 4 * sizeof(ull), s);  // maxc, big-key total, big-key cursor
+  cudaMemsetAsync(ws.maxc, 0, 8 * sizeof(ull), s);
   if (!counted) {
     cudaMemsetAsync(ws.cnt, 0, (nsec + 1) * sizeof(uint32_t), s);
     if (n) {
@@ -460,38 +921,95 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
       ws.launches += 1;
     }
   }
+  // big-sector tables: their number is known only after the scan; bound it by
+  // the sectors holding >= kSegCap of the n keys
+  const ull nbig_cap = std::min<ull>(nsec, n / kSegCap) + 2;
+  if (ws.big_cap < nbig_cap) {
+    cudaFree(ws.bg); cudaFree(ws.boff); cudaFree(ws.bcur); cudaFree(ws.bpre);
+    ws.bg = ws.boff = ws.bcur = ws.bpre = nullptr;
+    ws.big_cap = 0;
+    if ((e = cudaMalloc(&ws.bg, nbig_cap * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.boff, nbig_cap * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.bcur, nbig_cap * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.bpre, 2 * nbig_cap * sizeof(ull)))) return e;
+    ws.big_cap = nbig_cap;
+  }
+  const ull ngroups = (nsec + kGroup - 1) / kGroup;
+  ws.ncoarse = (uint32_t)std::min<ull>(kCoarse, ngroups);
+  ull* tot = reinterpret_cast<ull*>(ws.maxc) + 1;
   const ull nb = (nsec + kScanBlock - 1) / kScanBlock;
-  seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc,
-                                                       reinterpret_cast<ull*>(ws.maxc) + 1);
-  seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, ws.off + nsec);
-  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.dst);
-  ws.launches += 3;
-  ull hv[2];
-  if ((e = cudaMemcpyAsync(hv, ws.maxc, 2 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
+  seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
+  seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, tot);
+  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.dst, ws.bg, ws.boff,
+                                                      ws.gpre);
+  seg_groups_kernel<<<(unsigned)((ngroups + 256) / 256), 256, 0, s>>>(ws.gpre, ngroups, tot, ws.ncoarse, ws.cb,
+                                                                      ws.cstart, ws.cinfo);
+  seg_tiles_kernel<<<1, kSegThreads, 0, s>>>(tot, ws.ncoarse, ws.cstart, ws.cinfo, ws.ccur, ws.tpre, ws.off, nsec);
+  ws.launches += 5;
+  ull hv[4];
+  if ((e = cudaMemcpyAsync(hv, ws.maxc, 4 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
   if ((e = cudaStreamSynchronize(s))) return e;
   *max_per_sector = (uint32_t)hv[0];
-  *n_big = hv[1];
+  *n_big = hv[3];         // keys of big sectors
+  ws.n_bigsec = hv[2];
+  ws.n_big_keys = hv[3];
+  if (ws.n_bigsec)  // big-sector cursors start at their segments
+    if ((e = cudaMemcpyAsync(ws.bcur, ws.boff, ws.n_bigsec * sizeof(ull), cudaMemcpyDeviceToDevice, s))) return e;
   return cudaSuccess;
 }
 
-// phases 3-4: keys -> out (grouped by sector) -> dense counts (+ per-pc histograms)
+// phases 3-5: keys -> tmp (coarse buckets) -> out (chunks) / big (big sectors)
+// -> dense counts (+ per-pc histograms)
 cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout kl, ull nsec, uint32_t filter,
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
                           DevCounters* ctr, int num_sms, cudaStream_t s) {
+  cudaError_t e;
+  if (n && ws.tmp_cap < n) {
+    cudaFree(ws.tmp);
+    ws.tmp = nullptr;
+    ws.tmp_cap = 0;
+    if ((e = cudaMalloc(&ws.tmp, (n + n / 8 + 1024) * sizeof(ull)))) return e;
+    ws.tmp_cap = n + n / 8 + 1024;
+  }
+  const size_t psm = sizeof(PartSmem);
+  smem_optin((const void*)seg_coarse_kernel, (int)psm);
+  smem_optin((const void*)seg_fine_kernel, (int)psm);
   if (n) {
-    const unsigned grid = (unsigned)std::min<ull>((n + 256 * kScatterPer - 1) / (256 * kScatterPer), (ull)num_sms * 8);
     const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
     seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
-    seg_scatter_kernel<<<grid, 256, 0, s>>>(keys, n, kl, ws.dst, ws.cur, out, big,
-                                            reinterpret_cast<ull*>(ws.maxc) + 2);
+    const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
+    seg_coarse_kernel<<<g1, kPT, psm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
+    const ull g2 = (n + kPTile - 1) / kPTile + ws.ncoarse;  // >= the tiles of all buckets
+    seg_fine_kernel<<<(unsigned)g2, kPT, psm, s>>>(ws.tmp, kl, ws.ncoarse, ws.cstart, ws.cinfo, ws.tpre, ws.dst,
+                                                   ws.cur, ws.bcur, out, big);
+    ws.launches += 3;
   }
   const size_t smem = segment_chunk_smem();
   smem_optin((const void*)seg_chunk_kernel, (int)smem);
   const ull chunks = (n + kSegCap - 1) / kSegCap;
-  if (chunks)
+  if (chunks) {
     seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
                                                                   pc_hist, ctr, ws.cs0);
-  ws.launches += 2;
+    ws.launches += 1;
+  }
+  if (ws.n_bigsec) {
+    const ull* tot = reinterpret_cast<ull*>(ws.maxc) + 1;
+    const ull npc = pc_hist ? (1ull << kl.P) : 0ull;
+    seg_big_plan_kernel<<<1, kSegThreads, 0, s>>>(ws.boff, tot, npc, ws.bpre, ws.bpre + ws.big_cap);
+    // CTAs: at most one per kBigFill keys plus one per sector
+    const ull grid = ws.n_big_keys / kBigFill + ws.n_bigsec + 1;
+    const size_t bsm = kBigSlots * sizeof(ull);
+    smem_optin((const void*)seg_big_kernel, (int)bsm);
+    smem_optin((const void*)seg_big_pc_kernel, (int)bsm);
+    seg_big_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre, kl, filter, wc, sc,
+                                                             ctr);
+    ws.launches += 2;
+    if (pc_hist && kl.P) {
+      seg_big_pc_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre + ws.big_cap,
+                                                                  kl, filter, wc, sc, site_of, pc_hist, ctr);
+      ws.launches += 1;
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -536,7 +536,9 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
                   ctx->d_table, ctx->d_pctable, ctx->d_dense, ctx->d_wl, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
-                  ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->d_stage[0],
+                  ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->seg.gpre, ctx->seg.cb,
+                  ctx->seg.cstart, ctx->seg.cinfo, ctx->seg.ccur, ctx->seg.tpre, ctx->seg.tmp, ctx->seg.bg,
+                  ctx->seg.boff, ctx->seg.bcur, ctx->seg.bpre, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
                   ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr, ctx->d_wstage[0], ctx->d_wstage[1]};
   for (void* b : bufs) dfree(b);
@@ -941,9 +943,9 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   bool pc_done = false;
   // ---- a4 dedup + a5 count (+ a6 per-pc on the segment path) ----
   if (mode == THERMO_DEDUP_SEGMENT) {
-    // counting sort by sector + per-chunk shared-memory dedup; the keys of
-    // sectors too big for a chunk (hot sectors: >= 2048 warps x pcs) take the
-    // hash path below
+    // counting sort by sector (two partition passes) + per-chunk shared-memory
+    // dedup; the keys of sectors too big for a chunk (hot sectors: >= 2048
+    // keys) are reduced one CTA per sector
     CK(cudaEventRecord(ctx->evp[0], s));
     uint32_t maxc = 0;
     ull n_big = 0;
@@ -967,34 +969,6 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
     ctx->launches += ctx->seg.launches;
     ctx->seg.launches = 0;
-    if (n_big) {
-      // (sector, launch, warp) dedup of the big keys in an HBM hash set, counted
-      // into the same dense arrays (their sectors are disjoint from the chunks')
-      const ull cap = next_pow2(std::max<ull>(1024, 2 * n_big));
-      if (ctx->table_cap < cap) {
-        dfree(ctx->d_table);
-        ctx->table_cap = cap;
-        CK(dalloc(&ctx->d_table, cap));
-      }
-      CK(cudaMemsetAsync(ctx->d_table, 0xFF, cap * 8, s));
-      launch_hash_insert(ctx->d_pckeys, n_big, ctx->d_table, cap - 1, kl.P, ctx->d_ctr, ctx->num_sms, s);
-      launch_count_hash(ctx->d_table, cap, kl, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_ctr, ctx->num_sms, s);
-      ctx->launches += 2;
-      if (ctx->cfg.track_pc) {  // and their (pc, sector) facts, after the counts are final
-        launch_pc_extract(ctx->d_pckeys, n_big, kl, ctx->sw.alt, ctx->num_sms, s);  // (chunks are done with alt)
-        const ull pcap = next_pow2(std::max<ull>(1024, 2 * n_big));
-        if (ctx->pctable_cap < pcap) {
-          dfree(ctx->d_pctable);
-          ctx->pctable_cap = pcap;
-          CK(dalloc(&ctx->d_pctable, pcap));
-        }
-        CK(cudaMemsetAsync(ctx->d_pctable, 0xFF, pcap * 8, s));
-        launch_hash_insert(ctx->sw.alt, n_big, ctx->d_pctable, pcap - 1, 0, ctx->d_ctr, ctx->num_sms, s);
-        launch_pc_hist_hash(ctx->d_pctable, pcap, kl, site_tab, launch_filter, ctx->d_wc, ctx->d_sc, ctx->d_pchist,
-                            ctx->d_ctr, ctx->num_sms, s);
-        ctx->launches += 3;
-      }
-    }
     pc_done = true;
     (void)maxc;
   }

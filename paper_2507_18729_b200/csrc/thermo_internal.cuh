@@ -155,9 +155,24 @@ struct SegWorkspace {
   ull* cs0 = nullptr;        // [S_tot + 2] first sector of each chunk (+ end)
   uint32_t* dst = nullptr;   // [S_tot + 1] chunk of each sector's keys (~0: a big sector's, hash path)
   ull* bsum = nullptr;       // scan block sums
-  uint32_t* maxc = nullptr;  // [4 u64]: max keys in one sector, big-sector keys, big cursor
+  uint32_t* maxc = nullptr;  // [8 u64]: max keys in one sector | totals: normal keys, big sectors, big keys
   ull cap_sec = 0;
   ull launches = 0;
+  // two-pass partition (coarse buckets balanced by key count, then chunks / big sectors)
+  uint32_t ncoarse = 0;
+  ull* gpre = nullptr;       // [groups][3] (NL, BS, BK) at each 64-sector group
+  uint16_t* cb = nullptr;    // [groups] coarse bucket of each group
+  ull* cstart = nullptr;     // [ncoarse + 1] first key of each coarse bucket
+  ull* cinfo = nullptr;      // [ncoarse + 1][2] normal keys / big sectors before the bucket
+  ull* ccur = nullptr;       // [ncoarse] pass-1 cursors
+  ull* tpre = nullptr;       // [ncoarse + 1] first pass-2 tile of each bucket
+  ull* tmp = nullptr;        // pass-1 output
+  size_t tmp_cap = 0;
+  ull* bg = nullptr;         // [n big sectors] sector id of big sector i
+  ull* boff = nullptr;       // [n big sectors] its first key in `big`
+  ull* bcur = nullptr;       // [n big sectors] pass-2 cursors
+  ull* bpre = nullptr;       // [2][big_cap] first CTA of each big sector (main, pc passes)
+  ull big_cap = 0, n_bigsec = 0, n_big_keys = 0;
 };
 // counted: ws.cnt already holds the keys per sector (counted by the decoder)
 cudaError_t segment_reserve(SegWorkspace& ws, ull nsec);
