@@ -215,8 +215,8 @@ __global__ void seg_groups_kernel(const ull* __restrict__ gpre, ull ngroups, con
 //           (a bucket's chunks and big sectors are consecutive ids, and the
 //           chunk-of-sector lookups stay within the bucket's sector range).
 constexpr int kCoarse = 1024;
-constexpr int kPT = 256;                 // partition threads
-constexpr int kPPer = 16;                // keys per thread
+constexpr int kPT = 512;                 // partition threads (16 warps: two CTAs fill an SM's 32 warps)
+constexpr int kPPer = 8;                 // keys per thread
 constexpr int kPTile = kPT * kPPer;      // 4096 keys per tile
 constexpr int kFineBins = 4096;          // pass-2 destinations per bucket (more: direct scatter)
 
