@@ -175,9 +175,12 @@ def test_empty_and_degenerate():
         th4.build()
 
 
-def test_gemm_full_size_closed_form_and_sample():
+def test_gemm_full_size_all_outputs():
     """BJ configs[1] at full size (270,532,608 records) in the bench's launch
-    configuration: closed forms on every cell, oracle on sampled sectors."""
+    configuration: closed forms on every cell, then the UNRESTRICTED oracle over
+    all records compared on every output -- every dense word and sector row,
+    both histograms of every object, every per-PC row, every indicator field and
+    label, and the stats counters."""
     t = tg.gemm(1024, 1024, 128, "v00", device="cuda")
     th = gpu_ctx(t)
     th.ingest(t.records)
@@ -190,65 +193,64 @@ def test_gemm_full_size_closed_form_and_sample():
     assert labels == [["Hot"], ["FalseSharing"], ["FalseSharing"]]
     st = th.stats()
     assert st["records"] == 270532608 and st["distinct_pairs"] == 22020096
-    # oracle on a sample of sectors (restricted mode over the full trace)
-    rng = np.random.default_rng(5)
-    oi = np.repeat(np.arange(3), 20)
-    se = np.concatenate([rng.choice((o[1] + 31) // 32, 20, replace=False) for o in t.objects])
-    orc = oracle.Oracle([o[:4] for o in t.objects])
-    orc.restrict(oi, se)
     recs = t.records.cpu()
-    del t
+    t.records = recs
+    orc = oracle.Oracle([o[:4] for o in t.objects])
     for a in range(0, recs.shape[0], 1 << 25):
         orc.ingest(recs[a:a + (1 << 25)])
     orc.build()
-    ref = orc.sample(oi, se)
-    for row, o, s in zip(ref, oi, se):
-        b = th.heatmap(int(o), BOTH).reshape(-1, 9)[s]
-        assert np.array_equal(b, row), (o, s)
+    compare(orc, th, t)
 
 
-def test_stencil_full_size_closed_form_and_sample():
+def test_stencil_full_size_closed_form_all_cells():
     """BJ configs[2] at full size (8192^2 column-mapped 5-point stencil,
-    402,456,600 records): the closed forms on every deep-interior word/sector
-    of `in` and every interior cell of `out`, the oracle on sampled sectors
-    (boundaries included)."""
+    402,456,600 records): every word and sector of `in` and `out`, both
+    histograms of both objects, every per-PC row and the distinct-pair totals
+    against the reader enumeration of tests/closed_forms.py (pinned to the
+    oracle at N = 64, 96, 128 in test_oracle_pins.py).  Distinct (sector, warp)
+    pairs in closed form: `in` has sum over row blocks |R| (cols + cols with
+    j % 8 in {0, 7}) + 2 * 256 * 8190 = 8190 * 10236 + 4,193,280 = 88,026,120,
+    `out` 8190^2 = 67,076,100, total 155,102,220; distinct (pc, sector) pairs
+    50,319,360."""
+    from tests import closed_forms as C
     N = 8192
     t = tg.stencil(N, device="cuda")
     assert t.n == 6 * (N - 2) ** 2
     from paper_2507_18729_b200 import Thermo
-    # 2^24 sectors + 2^21 warps + 64 pc ids fit the 56-bit key prefix
     th = Thermo(max_launches=1, max_warps_per_launch=1 << 21, max_pcs=64)
     th.register_objects(t.objects)
     th.ingest(t.records)
     th.build()
-    w = th.heatmap(0, WORD).reshape(N, N).astype(np.int64)
-    s = th.heatmap(0, SECTOR).reshape(N, N // 8).astype(np.int64)
-    i = np.arange(N)[:, None]
-    edge = (i % 32 == 31).astype(np.int64) + (i % 32 == 0).astype(np.int64)
-    assert np.array_equal(w[2:N - 2, 2:N - 2], np.broadcast_to(3 + edge, (N, N))[2:N - 2, 2:N - 2])
-    # sectors whose 8 words are all deep interior: columns 8k..8k+7 with 2 <= 8k, 8k+7 <= N-3
-    assert np.array_equal(s[2:N - 2, 1:N // 8 - 1], np.broadcast_to(10 + 8 * edge, (N, N // 8))[2:N - 2, 1:N // 8 - 1])
-    wo = th.heatmap(1, WORD).reshape(N, N)
-    so = th.heatmap(1, SECTOR).reshape(N, N // 8)
-    assert (wo[1:N - 1, 1:N - 1] == 1).all() and (so[1:N - 1, 1:N // 8 - 1] == 8).all()
-    assert (wo[0] == 0).all() and (wo[N - 1] == 0).all()
-    # oracle on sampled sectors, boundaries included
-    rng = np.random.default_rng(7)
-    nsec = N * N // 8
-    picks = [np.concatenate([rng.choice(nsec, 24, replace=False), [0, N // 8 - 1, nsec - 1]]) for _ in range(2)]
-    oi = np.concatenate([np.full(len(p), k) for k, p in enumerate(picks)])
-    se = np.concatenate(picks)
-    orc = oracle.Oracle([o[:4] for o in t.objects])
-    orc.restrict(oi, se)
-    recs = t.records.cpu()
     del t
-    for a in range(0, recs.shape[0], 1 << 25):
-        orc.ingest(recs[a:a + (1 << 25)])
-    orc.build()
-    ref = orc.sample(oi, se)
-    for row, o, sct in zip(ref, oi, se):
-        b = th.heatmap(int(o), BOTH).reshape(-1, 9)[sct]
-        assert np.array_equal(b, row), (o, sct)
+    torch.cuda.empty_cache()
+    st = th.stats()
+    assert st["distinct_pairs"] == 8190 * 10236 + 4_193_280 + 8190 ** 2 == 155_102_220
+    assert st["distinct_pc_pairs"] == 50_319_360
+    assert st["records"] == 402_456_600 and st["invalid"] == 0 and st["unmapped_words"] == 0
+    w_in, s_in, w_out, s_out = C.stencil_counts(N, device="cuda")
+    exp = ((w_in, s_in), (w_out, s_out))
+    for k, (wc, sc) in enumerate(exp):
+        assert np.array_equal(th.heatmap(k, WORD), wc.cpu().numpy().reshape(-1).astype(np.uint32)), k
+        assert np.array_equal(th.heatmap(k, SECTOR), sc.cpu().numpy().reshape(-1).astype(np.uint32)), k
+        assert np.array_equal(th.histogram(k, WORD), C.level_hist(wc).cpu().numpy()), k
+        assert np.array_equal(th.histogram(k, SECTOR), C.level_hist(sc).cpu().numpy()), k
+    assert int(s_in.sum()) + int(s_out.sum()) == st["distinct_pairs"]
+    gw, gs = th.per_pc(WORD), th.per_pc(SECTOR)
+    assert [r[1] for r in gw] == list(C.STENCIL_PCS) == [r[1] for r in gs]
+    npc = 0
+    for k in range(6):
+        wm, sm = C.stencil_pc_cells(N, k, device="cuda")
+        wc, sc = exp[0] if k < 5 else exp[1]
+        assert np.array_equal(gw[k][2], C.level_hist(wc[wm]).cpu().numpy()), hex(C.STENCIL_PCS[k])
+        assert np.array_equal(gs[k][2], C.level_hist(sc[sm]).cpu().numpy()), hex(C.STENCIL_PCS[k])
+        npc += int(sm.sum())
+    assert npc == st["distinct_pc_pairs"]
+    ind = th.classify()
+    for k, (wc, sc) in enumerate(exp):
+        assert ind[k]["touched_sectors"] == int((sc > 0).sum()) and ind[k]["touched_words"] == int((wc > 0).sum())
+        assert ind[k]["sum_x"] == int(wc.to(torch.int64).sum()) and ind[k]["max_sector_count"] == int(sc.max())
+        assert ind[k]["sum_x2_lo"] + (ind[k]["sum_x2_hi"] << 64) == int((wc.to(torch.int64) ** 2).sum())
+    assert oracle.label_names(ind[1]["labels"]) == ["FalseSharing"]
 
 
 def _hot_sector_trace(n=40000, hot_warps=6000, seed=3):
@@ -503,30 +505,70 @@ def test_synthetic_medium_all_outputs(dedup):
     compare(o5, th, t)
 
 
-def _touched(objects, recs, sectors_per_obj, rng):
-    """Pick sectors the trace touches (and a few it may not), per object."""
-    r = recs.view(torch.int32)
+def _distinct_sector_warp(t):
+    """Distinct (global sector, warp) pairs of a single-launch trace of 4-byte
+    aligned accesses, by brute force (torch.unique on the device; no library
+    code): the sum of all sector counts."""
+    r = t.records
     addr = (r[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((r[:, 1].to(torch.int64) & 0xFFFF) << 32)
-    sec = torch.unique(addr[:: max(1, recs.shape[0] // (1 << 22))] >> 5).cpu().numpy()
-    oi, se = [], []
-    for k, ob in enumerate(objects):
-        lo, ns = ob[0] // 32, (ob[1] + 31) // 32
-        mine = sec[(sec >= lo) & (sec < lo + ns)] - lo
-        pick = list(rng.choice(mine, min(len(mine), sectors_per_obj), replace=False)) if len(mine) else []
-        pick += [0, ns - 1, int(rng.integers(ns))]
-        pick = sorted(set(int(p) for p in pick))
-        oi += [k] * len(pick)
-        se += pick
-    return np.array(oi), np.array(se, dtype=np.uint64)
+    bases = torch.tensor(sorted(o[0] for o in t.objects), device=r.device)
+    oi = torch.searchsorted(bases, addr, right=True) - 1
+    sec = (addr >> 5) - (bases[oi] >> 5) + oi * (1 << 36)  # object-qualified sector
+    return int(torch.unique(sec * (1 << 22) + r[:, 2].to(torch.int64)).shape[0])
 
 
-def test_synthetic_full_size_sampled():
+def _part_hash(x):
+    """Sector-hash partition id in [0, 64) of absolute sector indices (numpy
+    uint64/int64 or torch int64; the product stays below 2^63)."""
+    return ((x & 0x7FFFFFFF) * 2654435761 >> 26) & 63
+
+
+def _partition_exact(t, th, part=0):
+    """SURVEY.md:691-692: the oracle, exact, on the 1/64 sector-hash partition
+    `part` -- every (object, sector) whose absolute sector index hashes to it,
+    touched or not -- fed the records touching those sectors (a sector's row
+    depends only on them); every row of the partition compared with the GPU's.
+    Returns (rows compared, largest sector count in the partition)."""
+    oi_l, se_l, abs_l = [], [], []
+    for k, ob in enumerate(t.objects):
+        ns = (ob[1] + 31) // 32
+        a = np.arange(ns, dtype=np.int64) + ob[0] // 32
+        m = _part_hash(a) == part
+        oi_l.append(np.full(int(m.sum()), k, dtype=np.uint32))
+        se_l.append(np.nonzero(m)[0].astype(np.uint64))
+    oi, se = np.concatenate(oi_l), np.concatenate(se_l)
+    keep = []
+    r = t.records
+    for a in range(0, r.shape[0], 1 << 26):
+        c = r[a:a + (1 << 26)]
+        addr = (c[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((c[:, 1].to(torch.int64) & 0xFFFF) << 32)
+        size = torch.ones_like(addr) << ((c[:, 1].to(torch.int64) >> 16) & 7)
+        m = (_part_hash(addr >> 5) == part) | (_part_hash((addr + size - 1) >> 5) == part)
+        keep.append(c[m].cpu())
+    sub = torch.cat(keep)
+    orc = oracle.Oracle([o[:4] for o in t.objects])
+    orc.restrict(oi, se)
+    orc.ingest(sub)
+    orc.build()
+    ref = orc.sample(oi, se)
+    for k, ob in enumerate(t.objects):
+        rows = np.nonzero(oi == k)[0]
+        if not len(rows):
+            continue
+        both = th.heatmap(ob[3], BOTH).reshape(-1, 9)
+        got = both[se[rows].astype(np.int64)]
+        bad = np.nonzero((got != ref[rows]).any(1))[0]
+        assert len(bad) == 0, (ob[4], int(se[rows][bad[0]]), got[bad[0]], ref[rows][bad[0]])
+    print(f"partition {part}: {len(oi)} sectors, {sub.shape[0]} records, max sector count {int(ref[:, 8].max())}")
+    return len(oi), int(ref[:, 8].max())
+
+
+def test_synthetic_full_size_partition():
     """BJ configs[4] at bench size on one GPU (one rank's slice of the 8-GPU job:
     2^15 warps x 8 launches x 2048 records = 2^29 records over 64 objects of
-    4-512 MB): the oracle on sampled sectors of every object -- only the
-    records touching a sampled sector decide its row, so they are selected on
-    the device and the oracle ingests just those -- plus the histogram
-    invariants (level sums = n_words / n_sectors) on every object."""
+    4-512 MB): every row of the 1/64 sector-hash partition exactly against the
+    oracle, plus the histogram invariants (level sums = n_words / n_sectors) on
+    every object."""
     t = tg.synthetic(warps_per_launch=1 << 15, warp_range=(0, 1 << 15), device="cuda")
     assert t.n == 1 << 29
     from paper_2507_18729_b200 import Thermo
@@ -536,60 +578,19 @@ def test_synthetic_full_size_sampled():
     th.build(BOTH)
     st = th.stats()
     assert st["records"] == 1 << 29 and st["invalid"] == 0
-    rng = np.random.default_rng(9)
-    oi, se = _touched(t.objects, t.records, 6, rng)
-    # the records touching a sampled sector (first or last byte in it)
-    abs_sec = torch.tensor([t.objects[o][0] // 32 + int(s) for o, s in zip(oi, se)], device="cuda")
-    keep = []
-    r = t.records
-    for a in range(0, r.shape[0], 1 << 26):
-        c = r[a:a + (1 << 26)]
-        addr = (c[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((c[:, 1].to(torch.int64) & 0xFFFF) << 32)
-        size = torch.ones_like(addr) << ((c[:, 1].to(torch.int64) >> 16) & 7)
-        m = torch.isin(addr >> 5, abs_sec) | torch.isin((addr + size - 1) >> 5, abs_sec)
-        keep.append(c[m].cpu())
-    sub = torch.cat(keep)
-    orc = oracle.Oracle([o[:4] for o in t.objects])
-    orc.restrict(oi, se)
-    orc.ingest(sub)
-    orc.build()
-    ref = orc.sample(oi, se)
-    for k, ob in enumerate(t.objects):
-        oid = ob[3]
-        assert th.histogram(oid, WORD).sum() == (ob[1] + 3) // 4
-        assert th.histogram(oid, SECTOR).sum() == (ob[1] + 31) // 32
-        rows = [i for i in range(len(oi)) if oi[i] == k]
-        if not rows:
-            continue
-        both = th.heatmap(oid, BOTH).reshape(-1, 9)
-        for i in rows:
-            assert np.array_equal(both[int(se[i])], ref[i]), (k, int(se[i]), both[int(se[i])], ref[i])
-    assert sum(int((ref[:, 8] > 0).sum()) for _ in [0]) > 64  # the sample hits touched sectors
+    for ob in t.objects:
+        assert th.histogram(ob[3], WORD).sum() == (ob[1] + 3) // 4
+        assert th.histogram(ob[3], SECTOR).sum() == (ob[1] + 31) // 32
+    n, mx = _partition_exact(t, th, part=0)
+    assert n > 100_000 and mx > 1
 
 
-def _records_touching(recs, abs_sec, chunk=1 << 26):
-    """Records whose first or last byte lies in one of the sectors abs_sec
-    (sorted int64 tensor on the records' device), with per-sector counts."""
-    keep, cnt = [], torch.zeros(abs_sec.shape[0], dtype=torch.int64, device=abs_sec.device)
-    for a in range(0, recs.shape[0], chunk):
-        c = recs[a:a + chunk]
-        addr = (c[:, 0].to(torch.int64) & 0xFFFFFFFF) | ((c[:, 1].to(torch.int64) & 0xFFFF) << 32)
-        size = torch.ones_like(addr) << ((c[:, 1].to(torch.int64) >> 16) & 7)
-        s0, s1 = addr >> 5, (addr + size - 1) >> 5
-        m = torch.isin(s0, abs_sec) | torch.isin(s1, abs_sec)
-        hit = torch.cat([s0[m], s1[m & (s1 != s0)]])
-        cnt += torch.bincount(torch.searchsorted(abs_sec, hit), minlength=abs_sec.shape[0])[:abs_sec.shape[0]]
-        keep.append(c[m].cpu())
-    return torch.cat(keep), cnt.cpu().numpy()
-
-
-def test_spmv_full_size_sampled():
+def test_spmv_full_size_partition():
     """BJ configs[3] at bench size (CSR SpMV on an R-MAT scale-24 matrix, 840.6 M
-    records, the bench's launch configuration: AUTO dedup = SEGMENT with the
-    hot-sector hash side path): the oracle on sampled sectors of every object,
-    including sectors hot enough (>= 2048 keys) to take the side path -- a
-    sector's row depends only on the records touching it, so the oracle ingests
-    just those -- plus the histogram invariants on every object."""
+    records, the bench's launch configuration: AUTO = SEGMENT with its big-sector
+    kernels): every row of the 1/64 sector-hash partition (1.1 M sectors of all
+    five objects, hot x sectors included) exactly against the oracle, plus the
+    histogram invariants on every object."""
     t = tg.spmv(24, 16, device="cuda")
     from paper_2507_18729_b200 import Thermo
     th = Thermo(max_launches=max(1, int(t.meta.get("launches", 1))),  # bench.py's configuration
@@ -597,39 +598,14 @@ def test_spmv_full_size_sampled():
     th.register_objects(t.objects)
     th.ingest(t.records)
     th.build(BOTH)
-    assert th.stats()["invalid"] == 0
-    rng = np.random.default_rng(24)
-    oi, se = _touched(t.objects, t.records, 8, rng)
-    abs_sec = np.array([t.objects[o][0] // 32 + int(s) for o, s in zip(oi, se)], dtype=np.int64)
-    order = np.argsort(abs_sec)
-    oi, se, abs_sec = oi[order], se[order], abs_sec[order]
-    _, cnt = _records_touching(t.records, torch.tensor(abs_sec, device="cuda"))
-    # bound the oracle's work: drop the hottest sampled sectors beyond 4 M records
-    # each (the x vector's power-law columns), keeping every hot one below that
-    ok = cnt <= 4_000_000
-    print("sampled sectors:", len(cnt), "records per sampled sector (max kept):", int(cnt[ok].max()),
-          "dropped:", int((~ok).sum()))
-    assert (cnt[ok] >= 2048).any(), "the sample should include a hot (side-path) sector"
-    oi, se, abs_sec = oi[ok], se[ok], abs_sec[ok]
-    sub, _ = _records_touching(t.records, torch.tensor(abs_sec, device="cuda"))
-    orc = oracle.Oracle([o[:4] for o in t.objects])
-    orc.restrict(oi, se)
-    orc.ingest(sub)
-    orc.build()
-    ref = orc.sample(oi, se)
-    for k, ob in enumerate(t.objects):
-        oid = ob[3]
-        assert th.histogram(oid, WORD).sum() == (ob[1] + 3) // 4
-        assert th.histogram(oid, SECTOR).sum() == (ob[1] + 31) // 32
-        rows = [i for i in range(len(oi)) if oi[i] == k]
-        if not rows:
-            continue
-        both = th.heatmap(oid, BOTH).reshape(-1, 9)
-        for i in rows:
-            assert np.array_equal(both[int(se[i])], ref[i]), (k, int(se[i]), both[int(se[i])], ref[i])
-    print("sector counts of the sample: max", int(ref[:, 8].max()), "sectors with >= 2048 warps:", int((ref[:, 8] >= 2048).sum()))
-    assert int((ref[:, 8] > 0).sum()) > 16
-    assert int(ref[:, 8].max()) >= 2048  # a hot sector (>= 2048 keys): the SEGMENT side path at full size
+    st = th.stats()
+    assert st["invalid"] == 0 and st["distinct_pairs"] == _distinct_sector_warp(t)
+    for ob in t.objects:
+        assert th.histogram(ob[3], WORD).sum() == (ob[1] + 3) // 4
+        assert th.histogram(ob[3], SECTOR).sum() == (ob[1] + 31) // 32
+    n, mx = _partition_exact(t, th, part=0)
+    assert n > 1_000_000
+    assert mx >= 2048  # a big sector (>= 2048 keys): the big-sector kernels at full size
 
 
 @pytest.mark.parametrize("dedup", [3, 1])

@@ -196,6 +196,31 @@ def test_random_hot_cv_boundary(lo, hi, want):
     assert oracle.label_names(o2[0]["labels"]) == ["RandomHot"]
 
 
+@pytest.mark.parametrize("N", [64, 96, 128])
+def test_stencil_closed_form_enumeration(N):
+    """tests/closed_forms.py's reader enumeration of the column-mapped stencil
+    (every word of `in` and `out`, every sector, both histograms, every per-PC
+    row) equals the oracle exactly at small N; the GPU tests then use it on the
+    full 8192^2 trace (BJ configs[2])."""
+    from tests import closed_forms as C
+    t = tg.stencil(N)
+    o = run(t)
+    w_in, s_in, w_out, s_out = C.stencil_counts(N)
+    assert (o.word_counts(0) == w_in.numpy().reshape(-1)).all()
+    assert (o.sector_counts(0) == s_in.numpy().reshape(-1)).all()
+    assert (o.word_counts(1) == w_out.numpy().reshape(-1)).all()
+    assert (o.sector_counts(1) == s_out.numpy().reshape(-1)).all()
+    for k, (wc, sc) in enumerate(((w_in, s_in), (w_out, s_out))):
+        assert (o.hist(k, False) == C.level_hist(wc).numpy()).all()
+        assert (o.hist(k, True) == C.level_hist(sc).numpy()).all()
+    rows = o.per_pc()
+    assert [r[1] for r in rows] == list(C.STENCIL_PCS)
+    for k, (_, _, hw, hs) in enumerate(rows):
+        wm, sm = C.stencil_pc_cells(N, k)
+        wc, sc = (w_in, s_in) if k < 5 else (w_out, s_out)
+        assert (hw == C.level_hist(wc[wm]).numpy()).all() and (hs == C.level_hist(sc[sm]).numpy()).all()
+
+
 # ---------------------------------------------------------------- closed forms
 def test_tiny_b_closed_form():
     g = CLOSED["tiny_b"]
