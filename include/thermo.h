@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define THERMO_ABI_VERSION 4u
+#define THERMO_ABI_VERSION 5u
 #define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
 #define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
 #define THERMO_MAX_OBJECTS 1024
@@ -228,7 +228,22 @@ typedef struct {
    * and the bytes it sent to other ranks (NVLink roofline of row e) */
   double ms_exchange;
   uint64_t exchange_bytes;
+  /* per-kernel device time of the last ingest / build / classify (CUDA events
+   * on the context stream around each kernel or kernel group; 0 if it did not
+   * run): THERMO_K_* indices */
+  double ms_kernel[9];
 } thermo_stats;
+enum {
+  THERMO_K_DECODE = 0,         /* decode_kernel: fast per-instruction decode (a2+a3)        */
+  THERMO_K_DECODE_GENERAL = 1, /* decode_general_kernel: deferred / packed views (a2+a3)     */
+  THERMO_K_SEG_SCAN = 2,       /* SEGMENT: per-sector scans, coarse buckets, tiles (a4)      */
+  THERMO_K_SEG_COARSE = 3,     /* SEGMENT: partition pass 1, coarse buckets (a4)             */
+  THERMO_K_SEG_FINE = 4,       /* SEGMENT: partition pass 2, chunks / big sectors (a4)       */
+  THERMO_K_SEG_CHUNK = 5,      /* SEGMENT: per-chunk dedup + count + per-pc bins (a4-a6)     */
+  THERMO_K_SEG_BIG = 6,        /* SEGMENT: big-sector plan + count + per-pc bins (a4-a6)     */
+  THERMO_K_OBJECT_HIST = 7,    /* object_hist_kernel (a6)                                    */
+  THERMO_K_INDICATORS = 8      /* indicator kernels of classify (a7)                         */
+};
 
 typedef struct thermo_ctx thermo_ctx;
 

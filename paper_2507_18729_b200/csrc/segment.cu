@@ -974,24 +974,32 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   const size_t psm = sizeof(PartSmem);
   smem_optin((const void*)seg_coarse_kernel, (int)psm);
   smem_optin((const void*)seg_fine_kernel, (int)psm);
+  for (int k = 0; k < 4; ++k) ws.ran[k] = false;
+  if (ws.ev[0]) cudaEventRecord(ws.ev[0], s);
   if (n) {
     const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
     seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
     const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
     seg_coarse_kernel<<<g1, kPT, psm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
+    if (ws.ev[1]) cudaEventRecord(ws.ev[1], s);
     const ull g2 = (n + kPTile - 1) / kPTile + ws.ncoarse;  // >= the tiles of all buckets
     seg_fine_kernel<<<(unsigned)g2, kPT, psm, s>>>(ws.tmp, kl, ws.ncoarse, ws.cstart, ws.cinfo, ws.tpre, ws.dst,
                                                    ws.cur, ws.bcur, out, big);
+    if (ws.ev[2]) cudaEventRecord(ws.ev[2], s);
     ws.launches += 3;
+    ws.ran[0] = ws.ran[1] = true;
   }
   const size_t smem = segment_chunk_smem();
   smem_optin((const void*)seg_chunk_kernel, (int)smem);
   const ull chunks = (n + kSegCap - 1) / kSegCap;
   if (chunks) {
+    if (ws.ev[2] && !n) cudaEventRecord(ws.ev[2], s);
     seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
                                                                   pc_hist, ctr, ws.cs0);
     ws.launches += 1;
+    ws.ran[2] = true;
   }
+  if (ws.ev[3]) cudaEventRecord(ws.ev[3], s);
   if (ws.n_bigsec) {
     const ull* tot = reinterpret_cast<ull*>(ws.maxc) + 1;
     const ull npc = pc_hist ? (1ull << kl.P) : 0ull;
@@ -1009,7 +1017,9 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
                                                                   kl, filter, wc, sc, site_of, pc_hist, ctr);
       ws.launches += 1;
     }
+    ws.ran[3] = true;
   }
+  if (ws.ev[4]) cudaEventRecord(ws.ev[4], s);
   return cudaGetLastError();
 }
 

@@ -102,6 +102,8 @@ struct thermo_ctx {
   cudaEvent_t evp[8] = {};  // phase timers
   ull launches = 0;         // kernels launched
   float ms_phase[6] = {0, 0, 0, 0, 0, 0};  // decode, dedup, count, hist, pc, indicators
+  double ms_kernel[9] = {};                // THERMO_K_* (thermo.h)
+  cudaEvent_t evk[4] = {};                 // decode kernel timers
 
   uint32_t built_filter = THERMO_ALL_LAUNCHES;
   uint32_t built_gran = THERMO_BOTH;
@@ -228,7 +230,7 @@ thermo_status grow_keys(thermo_ctx* ctx, ull** buf, size_t* cap, ull need, ull k
 DecodeArgs decode_args(thermo_ctx* ctx);
 
 // decode one device-resident call (records[0] starts an instruction)
-thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
+thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n, bool timed = false) {
   if (n == 0) return THERMO_OK;
   const ull n_ranges = (n + kRangeLen - 1) / kRangeLen;
   if (ctx->heads_cap < n_ranges + 1) {
@@ -249,10 +251,22 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n) {
   a.n = n;
   a.heads = ctx->d_heads;
   a.n_ranges = (uint32_t)n_ranges;
+  CK(cudaEventRecord(ctx->evk[0], ctx->stream));
   launch_decode(a, ctx->num_sms, ctx->stream);
+  CK(cudaEventRecord(ctx->evk[1], ctx->stream));
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->evk[2], ctx->stream));
   CK(cudaEventRecord(ctx->evp[7], ctx->stream));
+  // per-kernel times of a device-resident call (the staged host path keeps its
+  // copy / decode overlap and is not timed per kernel)
+  if (!timed) return THERMO_OK;
+  CK(cudaEventSynchronize(ctx->evk[2]));
+  float t0 = 0, t1 = 0;
+  cudaEventElapsedTime(&t0, ctx->evk[0], ctx->evk[1]);
+  cudaEventElapsedTime(&t1, ctx->evk[1], ctx->evk[2]);
+  ctx->ms_kernel[THERMO_K_DECODE] += t0;
+  ctx->ms_kernel[THERMO_K_DECODE_GENERAL] += t1;
   ctx->launches += 3;
   return THERMO_OK;
 }
@@ -457,6 +471,16 @@ thermo_status thermo_create(thermo_ctx** out, int device, void* stream, const th
     delete ctx;
     return THERMO_ECUDA;
   }
+  for (int i = 0; i < 4; ++i)
+    if (cudaEventCreate(&ctx->evk[i]) != cudaSuccess) {
+      delete ctx;
+      return THERMO_ECUDA;
+    }
+  for (int i = 0; i < 5; ++i)
+    if (cudaEventCreate(&ctx->seg.ev[i]) != cudaSuccess) {
+      delete ctx;
+      return THERMO_ECUDA;
+    }
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&ctx->ev_copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->ev_used[i], cudaEventDisableTiming);
@@ -549,6 +573,10 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
   }
   for (int i = 0; i < 8; ++i)
     if (ctx->evp[i]) cudaEventDestroy(ctx->evp[i]);
+  for (int i = 0; i < 4; ++i)
+    if (ctx->evk[i]) cudaEventDestroy(ctx->evk[i]);
+  for (int i = 0; i < 5; ++i)
+    if (ctx->seg.ev[i]) cudaEventDestroy(ctx->seg.ev[i]);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   for (int i = 0; i < 2; ++i)
     if (ctx->evx[i]) cudaEventDestroy(ctx->evx[i]);
@@ -735,8 +763,9 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
   st = grow_keys(ctx, &ctx->d_keys, &ctx->keys_cap, ctx->n_keys + 2 * (ull)n + 64, ctx->n_keys);
   if (st) return st;
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  ctx->ms_kernel[THERMO_K_DECODE] = ctx->ms_kernel[THERMO_K_DECODE_GENERAL] = 0;
   if (on_device) {
-    st = decode_device(ctx, reinterpret_cast<const uint4*>(recs), n);
+    st = decode_device(ctx, reinterpret_cast<const uint4*>(recs), n, true);
     if (st) return st;
   } else {
     // staged host ingest: chunks split at explicit instruction heads, copy of
@@ -1065,6 +1094,15 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaEventSynchronize(ctx->ev1));
   cudaEventElapsedTime(&ctx->ms_build, ctx->ev0, ctx->ev1);
   for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&ctx->ms_phase[1 + i], ctx->evp[i], ctx->evp[i + 1]);
+  for (int k = THERMO_K_SEG_SCAN; k <= THERMO_K_OBJECT_HIST; ++k) ctx->ms_kernel[k] = 0;
+  ctx->ms_kernel[THERMO_K_SEG_SCAN] = ctx->dedup_used == THERMO_DEDUP_SEGMENT ? ctx->ms_phase[1] : 0.0;
+  if (ctx->dedup_used == THERMO_DEDUP_SEGMENT) {
+    float t = 0;
+    for (int k = 0; k < 4; ++k)
+      if (ctx->seg.ran[k] && cudaEventElapsedTime(&t, ctx->seg.ev[k], ctx->seg.ev[k + 1]) == cudaSuccess)
+        ctx->ms_kernel[THERMO_K_SEG_COARSE + k] = t;
+  }
+  ctx->ms_kernel[THERMO_K_OBJECT_HIST] = ctx->ms_phase[3];
   ctx->launches += ctx->sw.launches + ctx->swpc.launches;
   ctx->sw.launches = ctx->swpc.launches = 0;
   (void)l0;
@@ -1272,6 +1310,7 @@ thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, ther
   CK(cudaStreamSynchronize(s));
   cudaEventElapsedTime(&ctx->ms_classify, ctx->ev0, ctx->ev1);
   ctx->ms_phase[5] = ctx->ms_classify;
+  ctx->ms_kernel[THERMO_K_INDICATORS] = ctx->ms_classify;
   for (size_t r = 0; r < n; ++r) {
     const ull* v = ind.data() + ctx->reg_to_sorted[r] * kIndFields;
     thermo_indicators& o = out[r];
@@ -1332,6 +1371,7 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
   out->kernel_launches = ctx->launches;
   out->ms_exchange = ctx->ms_exchange;
   out->exchange_bytes = ctx->exchange_bytes;
+  for (int k = 0; k < 9; ++k) out->ms_kernel[k] = ctx->ms_kernel[k];
   return THERMO_OK;
 }
 

@@ -71,7 +71,7 @@ class thermo_stats(ctypes.Structure):
                 ("ms_classify", ctypes.c_double), ("ms_decode", ctypes.c_double), ("ms_dedup", ctypes.c_double),
                 ("ms_count", ctypes.c_double), ("ms_hist", ctypes.c_double), ("ms_pc", ctypes.c_double),
                 ("ms_indicators", ctypes.c_double), ("kernel_launches", u64),
-                ("ms_exchange", ctypes.c_double), ("exchange_bytes", u64)]
+                ("ms_exchange", ctypes.c_double), ("exchange_bytes", u64), ("ms_kernel", ctypes.c_double * 9)]
 
 
 # every symbol include/thermo.h declares
@@ -162,6 +162,11 @@ def nccl_unique_id() -> bytes:
     if st:
         raise ThermoError(st, "thermo_nccl_unique_id")
     return buf.raw
+
+
+# thermo_stats.ms_kernel entries (include/thermo.h THERMO_K_*)
+KERNELS = ("decode_kernel", "decode_general_kernel", "seg_scan", "seg_coarse_kernel", "seg_fine_kernel",
+           "seg_chunk_kernel", "seg_big_kernel", "object_hist_kernel", "indicator_kernels")
 
 
 def _default_stream(device: int) -> int:
@@ -346,4 +351,6 @@ class Thermo:
     def stats(self) -> dict:
         s = thermo_stats()
         self._ck(self.L.thermo_get_stats(self.h, ctypes.byref(s)))
-        return {f: getattr(s, f) for f, _ in thermo_stats._fields_ if not f.startswith("reserved")}
+        d = {f: getattr(s, f) for f, _ in thermo_stats._fields_ if not f.startswith("reserved") and f != "ms_kernel"}
+        d["ms_kernel"] = dict(zip(KERNELS, list(s.ms_kernel)))
+        return d

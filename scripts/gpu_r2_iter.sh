@@ -7,7 +7,7 @@ else
 fi
 tail -3 gpurun_out/it_pytest.log
 grep -E "Error|assert|FAILED" gpurun_out/it_pytest.log | head -20
-for w in ${WL:-sgemm stencil spmv}; do timeout 600 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/it_bench_$w.json 2> gpurun_out/it_bench_$w.err; echo rc=$?; tail -2 gpurun_out/it_bench_$w.err; done
+for w in ${WL:-sgemm stencil spmv}; do timeout 600 python bench.py --workload $w --only --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/it_bench_$w.json 2> gpurun_out/it_bench_$w.err; echo rc=$?; tail -2 gpurun_out/it_bench_$w.err; done
 python - <<'PY'
 import json
 for w in ["sgemm", "stencil", "spmv", "synthetic"]:

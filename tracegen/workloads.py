@@ -252,10 +252,14 @@ def rmat_csr(scale: int, edgefactor: int, seed: int = 0x5EED0004, device="cpu",
     return ro, cols
 
 
-def spmv(scale=15, edgefactor=16, seed=0x5EED0004, device="cpu", rows_per_chunk=1 << 20) -> Trace:
+def spmv(scale=15, edgefactor=16, seed=0x5EED0004, device="cpu", rows_per_chunk=1 << 20, row_range=None,
+         max_records=None) -> Trace:
     """One thread per row, block 256 (global warp = r // 32).  Per row: LD ro[r],
     LD ro[r+1]; per nnz i: LD col[i], LD val[i], LD x[col[i]] (lanes inactive
-    past their row length); then ST y[r].  Records = 3 nnz + 3 n."""
+    past their row length); then ST y[r].  Records = 3 nnz + 3 n.
+    row_range=(lo, hi): only the rows [lo, hi) (multiples of 32: whole warps;
+    one rank's slice of the job); max_records: stop after the first chunk that
+    reaches it (a prefix of whole warps, for bounded CPU samples)."""
     dev = torch.device(device)
     ro, ci = rmat_csr(scale, edgefactor, seed, device)
     n = ro.shape[0] - 1
@@ -269,8 +273,13 @@ def spmv(scale=15, edgefactor=16, seed=0x5EED0004, device="cpu", rows_per_chunk=
                (b_va, 4 * nnz, SPACE_GLOBAL, 2, "values"), (b_x, 4 * n, SPACE_GLOBAL, 3, "x"),
                (b_y, 4 * n, SPACE_GLOBAL, 4, "y")]
     parts = []
-    for r0 in range(0, n, rows_per_chunk):
-        r1 = min(n, r0 + rows_per_chunk)
+    lo, hi = (0, n) if row_range is None else (max(0, row_range[0]), min(n, row_range[1]))
+    assert lo % 32 == 0 and (hi % 32 == 0 or hi == n), "row ranges hold whole warps"
+    done = 0
+    for r0 in range(lo, hi, rows_per_chunk):
+        if max_records is not None and done >= max_records:
+            break
+        r1 = min(hi, r0 + rows_per_chunk)
         r = torch.arange(r0, r1, dtype=torch.int64, device=dev)
         ln = ro[r0 + 1:r1 + 1] - ro[r0:r1]
         w = r // 32
@@ -306,8 +315,9 @@ def spmv(scale=15, edgefactor=16, seed=0x5EED0004, device="cpu", rows_per_chunk=
         first = torch.ones_like(ins)
         first[1:] = ((ins[1:] != ins[:-1]) | (wv[1:] != wv[:-1])).to(torch.int64)
         parts.append(pack_records(addr, 2, kind, SPACE_GLOBAL, first, wv, pc, 0))
+        done += parts[-1].shape[0]
     return Trace(f"spmv-s{scale}-ef{edgefactor}", objects, _concat(parts, dev),
-                 meta=dict(n=n, nnz=nnz, scale=scale, edgefactor=edgefactor))
+                 meta=dict(n=n, nnz=nnz, scale=scale, edgefactor=edgefactor, rows=(lo, hi)))
 
 
 # --------------------------------------------------------------------------
