@@ -493,6 +493,55 @@ def run_ours(args, workload, ws, rank, local, steps, warmup, headline):
     return line
 
 
+def run_local_shards(args, P):
+    """P in-process shards of the sharded mode on one GPU (thermo_create_local_shards,
+    the same exchange algorithm as the NCCL ranks, device-to-device copies):
+    the trace split at instruction heads into P slices, one host thread per
+    rank.  Reports, per rank, the sectors its dense rows cover (storage falls
+    as 1/P by construction), the keys it counts after the exchange, the bytes
+    it sends, and its device times per phase; the ranks share one GPU, so the
+    times show the per-rank work, not a multi-GPU speed-up."""
+    import torch
+    from paper_2507_18729_b200 import BOTH, Thermo
+    from paper_2507_18729_b200.dist import run_ranks, split_at_heads
+    t = make_trace(args.workload, "cuda")
+    cfg = dict(max_launches=max(1, int(t.meta.get("launches", 1))),
+               max_warps_per_launch=max(1, int(t.meta.get("warps", 1 << 20))), max_pcs=int(t.meta.get("pcs", 256)))
+    cuts = split_at_heads(t.records, P)
+    slices = [t.records[a:b] for a, b in cuts]
+    shards = Thermo.local_shards(P, **cfg) if P > 1 else [Thermo(**cfg)]
+    for th in shards:
+        th.register_objects(t.objects)
+
+    def step(r):
+        def f():
+            th = shards[r]
+            th.reset()
+            if slices[r].shape[0]:
+                th.ingest(slices[r])
+            th.build(BOTH)
+            th.classify()
+            return th.stats()
+        return f
+
+    for _ in range(max(1, args.warmup)):
+        run_ranks([step(r) for r in range(P)])
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sts = run_ranks([step(r) for r in range(P)])
+    torch.cuda.synchronize()
+    el = (time.perf_counter() - t0) / args.steps
+    ranks = [{"rank": r, "records": int(slices[r].shape[0]), "local_sectors": st["local_sectors"],
+              "dense_row_bytes": 36 * st["local_sectors"], "keys_counted": st["keys_emitted"],
+              "exchange_bytes_sent": st["exchange_bytes"], "ms_ingest": st["ms_ingest"], "ms_build": st["ms_build"],
+              "ms_classify": st["ms_classify"], "ms_exchange": st["ms_exchange"],
+              "ms_kernel": {k: v for k, v in st["ms_kernel"].items() if v > 0}} for r, st in enumerate(sts)]
+    S_tot = sum((o[1] + 31) // 32 for o in t.objects)
+    print(json.dumps({"mode": "local_shards", "workload": args.workload, "P": P, "records": t.n, "S_tot": S_tot,
+                      "wall_ms_per_step": el * 1e3, "ranks": ranks}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -510,6 +559,8 @@ def main():
     ap.add_argument("--format", default="lane", choices=["lane", "warp"],
                     help="record format: 16-B per-lane records (default, the contract) or 272-B "
                          "warp-instruction records (SURVEY §8f item 4)")
+    ap.add_argument("--local-shards", type=int, default=0,
+                    help="P in-process shards on one GPU: per-rank storage, keys and phase times (no bench line)")
     ap.add_argument("--force-dist", action="store_true",
                     help="one GPU through the sharded NCCL path (checks that code path on one GPU)")
     args = ap.parse_args()
@@ -524,6 +575,9 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
+    if args.local_shards:
+        run_local_shards(args, args.local_shards)
+        return
     if args.force_dist:
         os.environ["THERMO_FORCE_COMM"] = "1"
     h = run_ours(args, args.workload, ws, rank, local, args.steps, args.warmup, True)

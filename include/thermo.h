@@ -232,6 +232,9 @@ typedef struct {
    * on the context stream around each kernel or kernel group; 0 if it did not
    * run): THERMO_K_* indices */
   double ms_kernel[9];
+  /* sectors this context's dense rows and count workspace cover: all
+   * registered sectors, or (sharded mode) the rank's own 2048-sector chunks */
+  uint64_t local_sectors;
 } thermo_stats;
 enum {
   THERMO_K_DECODE = 0,         /* decode_kernel: fast per-instruction decode (a2+a3)        */

@@ -197,11 +197,13 @@ __device__ __forceinline__ void agg_add(uint32_t* s_hist, ull* g_hist, bool use_
 // a6 per-object histograms over the dense rows, one sector per lane (the 8
 // word counts as two 16-byte loads, a warp reads 1 KB contiguous); the
 // object is looked up once per warp while its 32 sectors stay inside it.
+// sharded mode: lane sector l < n_local is the rank's local index (global
+// g = shard_global(l)); one rank: l = g, n_local = total
 __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __restrict__ wc,
                                                           const uint32_t* __restrict__ sc, const ull* __restrict__ soff,
                                                           const ull* __restrict__ nwords, uint32_t nobj,
-                                                          ull* __restrict__ hist, ull total, int use_smem,
-                                                          uint32_t rank, uint32_t nranks) {
+                                                          ull* __restrict__ hist, ull total, ull n_local,
+                                                          int use_smem, uint32_t rank, uint32_t nranks) {
   extern __shared__ uint32_t s_hist[];  // [nobj][2][33] when use_smem
   const uint32_t nb = nobj * 2 * kLevels;
   if (use_smem) {
@@ -212,10 +214,14 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
   const ull wstride = (ull)gridDim.x * blockDim.x;
   uint32_t o0 = 0;
   ull olo = 1, ohi = 0;  // sectors [olo, ohi) of object o0 (the last one looked up)
-  for (ull g0 = ((ull)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); g0 < total; g0 += wstride) {
+  for (ull l0 = ((ull)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); l0 < n_local; l0 += wstride) {
+    // a warp's 32 local sectors lie in one 2048-sector chunk: contiguous globally
+    const ull g0 = shard_global(l0, rank, nranks);
+    const ull l = l0 + lane;
     const ull g = g0 + lane;
-    const bool in = g < total && shard_owner(g, nranks) == rank;
+    const bool in = l < n_local && g < total;
     const ull glast = (g0 + 31 < total ? g0 + 31 : total - 1);
+    if (g0 >= total) continue;
     // warp-uniform object when the first and last sector of the 32 agree
     if (g0 < olo || g0 >= ohi) {  // (uniform) search only when leaving the object
       o0 = obj_of_sector(soff, nobj, g0);
@@ -227,9 +233,9 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
     uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
     uint32_t c = 0;
     if (in) {
-      lo = reinterpret_cast<const uint4*>(wc + 8 * g)[0];
-      hi = reinterpret_cast<const uint4*>(wc + 8 * g)[1];
-      c = sc[g];
+      lo = reinterpret_cast<const uint4*>(wc + 8 * l)[0];
+      hi = reinterpret_cast<const uint4*>(wc + 8 * l)[1];
+      c = sc[l];
     }
     const ull nwo = nwords[o];
     const ull wl0 = in ? (g - soff[o]) * 8 : 0;
@@ -250,16 +256,16 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
 }
 
 void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj, const ull* obj_nwords,
-                        ull* hist, ull total_sectors, uint32_t rank, uint32_t nranks, int num_sms,
+                        ull* hist, ull total_sectors, ull n_local, uint32_t rank, uint32_t nranks, int num_sms,
                         cudaStream_t s) {
   const uint32_t nb = obj.n * 2 * kLevels;
   const int use_smem = nb * sizeof(uint32_t) <= 96 * 1024;
   size_t smem = use_smem ? nb * sizeof(uint32_t) : 0;
   smem_optin((const void*)object_hist_kernel, 96 * 1024);
-  unsigned grid = (unsigned)std::min<ull>((total_sectors + 255) / 256, (ull)num_sms * 8);
+  unsigned grid = (unsigned)std::min<ull>((n_local + 255) / 256, (ull)num_sms * 8);
   if (grid < 1) grid = 1;
   object_hist_kernel<<<grid, 256, smem, s>>>(word_cnt, sector_cnt, obj.soff, obj_nwords, obj.n, hist,
-                                              total_sectors, use_smem, rank, nranks);
+                                              total_sectors, n_local, use_smem, rank, nranks);
 }
 
 // ---- a6: per-PC histograms ---------------------------------------------------------

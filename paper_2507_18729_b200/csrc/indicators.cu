@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   const ull soff = a.obj.soff[o];
   const ull nw = a.obj_nwords[o];
   const thermo_params& P = a.prm;
+  // the rows of an owned tile (one 2048-sector chunk) at their local index
+  const long long ldelta = (long long)shard_local(g0, a.nranks) - (long long)g0;
+  const uint32_t* const sector_cnt = a.sector_cnt + ldelta;
+  const uint32_t* const word_cnt = a.word_cnt + 8 * ldelta;
   const ull cand = mode ? a.ind[(ull)o * kIndFields + F_CAND] : 0;
   // no surviving vote: no gap holds a majority, the verify count is not needed
   if (mode == 1 && a.ind[(ull)o * kIndFields + F_CANDCNT] == 0) return;
@@ -112,9 +116,9 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   uint32_t c_n = 0;
   uint4 lo_n = make_uint4(0, 0, 0, 0), hi_n = lo_n;
   if (gs < g1) {
-    c_n = a.sector_cnt[gs];
-    lo_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * gs)[0];
-    hi_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * gs)[1];
+    c_n = sector_cnt[gs];
+    lo_n = reinterpret_cast<const uint4*>(word_cnt + 8 * gs)[0];
+    hi_n = reinterpret_cast<const uint4*>(word_cnt + 8 * gs)[1];
   }
   for (int i = 0; i < kSecPerThread; ++i) {
     const ull g = gs + i;
@@ -122,9 +126,9 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     const uint32_t c = c_n;
     const uint4 lo = lo_n, hi = hi_n;
     if (i + 1 < kSecPerThread && g + 1 < g1) {
-      c_n = a.sector_cnt[g + 1];
-      lo_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * (g + 1))[0];
-      hi_n = reinterpret_cast<const uint4*>(a.word_cnt + 8 * (g + 1))[1];
+      c_n = sector_cnt[g + 1];
+      lo_n = reinterpret_cast<const uint4*>(word_cnt + 8 * (g + 1))[0];
+      hi_n = reinterpret_cast<const uint4*>(word_cnt + 8 * (g + 1))[1];
     }
     const uint32_t xs[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     ull mw = 0;

@@ -87,8 +87,12 @@ __global__ void __launch_bounds__(kShardThreads) shard_scatter_kernel(const ull*
         const ull pm = ((1ull << kl.P) - 1) << 8;
         key = (key & ~pm) | ((ull)pc_map[key_pcid(key, kl)] << 8);
       }
-      k[u] = key;
       own[u] = in ? shard_owner(key_g(key, kl), nranks) : 0xFFFFFFFFu;
+      if (in) {  // the owner counts into its own chunks: global sector -> its local index
+        const uint32_t gs = 8 + kl.P + kl.L + kl.W;
+        key = (key & ((1ull << gs) - 1)) | (shard_local(key_g(key, kl), nranks) << gs);
+      }
+      k[u] = key;
       const unsigned peers = __match_any_sync(0xFFFFFFFFu, own[u]);
       const int leader = __ffs(peers) - 1;
       uint32_t base = 0;

@@ -55,6 +55,7 @@ struct thermo_ctx {
   std::vector<ull> h_lo, h_hi, h_soff, h_nwords;
   std::vector<uint32_t> h_space;
   ull S_tot = 0;
+  ull S_own = 0;   // sectors of the dense rows / count workspace: S_tot, or (sharded) the owned chunks
   KeyLayout kl{};
   uint32_t n_tiles = 0;
 
@@ -641,6 +642,13 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   obj_tile0[n] = (uint32_t)tile_obj.size();
   ctx->h_soff[n] = soff;
   ctx->S_tot = soff;
+  if (ctx->nranks > 1) {  // the rank's own 2048-sector chunks only (SURVEY §8e local index)
+    const ull nch = (soff + kTileSectors - 1) / kTileSectors;
+    const ull own = nch > (ull)ctx->rank ? (nch - ctx->rank + ctx->nranks - 1) / ctx->nranks : 0;
+    ctx->S_own = std::max<ull>(1, own) * kTileSectors;
+  } else {
+    ctx->S_own = soff;
+  }
   ctx->n_tiles = (uint32_t)tile_obj.size();
   const thermo_config& c = ctx->cfg;
   KeyLayout kl;
@@ -663,7 +671,7 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   CK(cudaMemcpy(ctx->d_soff, ctx->h_soff.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_nwords, ctx->h_nwords.data(), n * 8, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_space, ctx->h_space.data(), n * 4, cudaMemcpyHostToDevice));
-  if (dalloc(&ctx->d_wc, 8 * soff) != cudaSuccess || dalloc(&ctx->d_sc, soff) != cudaSuccess)
+  if (dalloc(&ctx->d_wc, 8 * ctx->S_own) != cudaSuccess || dalloc(&ctx->d_sc, ctx->S_own) != cudaSuccess)
     return fail(ctx, THERMO_ENOMEM, "dense heat-map arrays");
   CK(dalloc(&ctx->d_instr, (size_t)c.max_launches * n * 2));
   CK(dalloc(&ctx->d_launch_ctr, (size_t)c.max_launches * 2));
@@ -949,8 +957,8 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   cudaStream_t s = ctx->stream;
   CK(cudaEventRecord(ctx->ev0, s));
   const ull l0 = ctx->launches;
-  CK(cudaMemsetAsync(ctx->d_wc, 0, 8 * ctx->S_tot * sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(ctx->d_sc, 0, ctx->S_tot * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->d_wc, 0, 8 * ctx->S_own * sizeof(uint32_t), s));
+  CK(cudaMemsetAsync(ctx->d_sc, 0, ctx->S_own * sizeof(uint32_t), s));
   CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
@@ -960,12 +968,12 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   // 2^26 sectors 127 vs 170 ms; synthetic 2^28 sectors 60 vs 82 ms); its
   // per-sector workspace (28 B/sector) decides the limit
   uint32_t mode = ctx->cfg.dedup;
-  const ull dense_words = (ull)ctx->cfg.max_launches * ctx->S_tot * 8;  // DENSE masks (u64 each)
+  const ull dense_words = (ull)ctx->cfg.max_launches * ctx->S_own * 8;  // DENSE masks (u64 each)
   if (mode == THERMO_DEDUP_AUTO) {
     if (ctx->cfg.block_warps >= 1 && ctx->cfg.block_warps <= 64 && dense_words * 8 <= (4ull << 30))
       mode = THERMO_DEDUP_DENSE;
     else
-      mode = ctx->S_tot <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
+      mode = ctx->S_own <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
   }
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
@@ -978,7 +986,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     CK(cudaEventRecord(ctx->evp[0], s));
     uint32_t maxc = 0;
     ull n_big = 0;
-    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_tot, ctx->seg, ctx->num_sms, s, &maxc, &n_big,
+    e = segment_prepare(ctx->d_keys, ctx->n_keys, kl, ctx->S_own, ctx->seg, ctx->num_sms, s, &maxc, &n_big,
                         ctx->seg_counted);
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment prepare: ") + cudaGetErrorString(e));
     if (ctx->sw.alt_cap < ctx->n_keys) {
@@ -992,7 +1000,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       CK(dalloc(&ctx->d_pckeys, ctx->pckeys_cap));
     }
     CK(cudaEventRecord(ctx->evp[1], s));
-    e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, ctx->d_pckeys, kl, ctx->S_tot, launch_filter, ctx->seg,
+    e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, ctx->d_pckeys, kl, ctx->S_own, launch_filter, ctx->seg,
                       ctx->d_wc, ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
                       ctx->num_sms, s);
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
@@ -1025,10 +1033,10 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     }
     CK(cudaEventRecord(ctx->evp[0], s));
     CK(cudaMemsetAsync(ctx->d_dense, 0, dense_words * 8, s));
-    launch_dense_or(ctx->d_keys, ctx->n_keys, kl, ctx->cfg.block_id * ctx->cfg.block_warps, ctx->S_tot,
+    launch_dense_or(ctx->d_keys, ctx->n_keys, kl, ctx->cfg.block_id * ctx->cfg.block_warps, ctx->S_own,
                     ctx->d_dense, ctx->num_sms, s);
     CK(cudaEventRecord(ctx->evp[1], s));
-    launch_dense_count(ctx->d_dense, ctx->cfg.max_launches, ctx->S_tot, launch_filter, ctx->d_wc, ctx->d_sc,
+    launch_dense_count(ctx->d_dense, ctx->cfg.max_launches, ctx->S_own, launch_filter, ctx->d_wc, ctx->d_sc,
                        ctx->d_ctr, ctx->num_sms, s);
     ctx->launches += 2;
   } else if (mode == THERMO_DEDUP_HASH) {
@@ -1048,8 +1056,8 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->evp[2], s));
   // ---- a6 histograms ----
-  launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->rank,
-                     ctx->nranks, ctx->num_sms, s);
+  launch_object_hist(ctx->d_wc, ctx->d_sc, obj_table(ctx), ctx->d_nwords, ctx->d_hist, ctx->S_tot, ctx->S_own,
+                     ctx->rank, ctx->nranks, ctx->num_sms, s);
   ctx->launches += 1;
   CK(cudaEventRecord(ctx->evp[3], s));
   if (ctx->cfg.track_pc && !pc_done) {
@@ -1074,7 +1082,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       launch_pc_hist_sorted(ctx->d_pckeys, ctx->n_pckeys, kl, site_tab, launch_filter, ctx->d_wc, ctx->d_sc,
                             ctx->d_pchist, ctx->d_ctr, ctx->num_sms, s);
     } else {
-      const ull bound = std::min<ull>(ctx->n_pckeys, std::max<ull>(1, n_pc) * ctx->S_tot);
+      const ull bound = std::min<ull>(ctx->n_pckeys, std::max<ull>(1, n_pc) * ctx->S_own);
       ull cap = next_pow2(std::max<ull>(1024, 2 * bound));
       if (ctx->pctable_cap < cap) {
         dfree(ctx->d_pctable);
@@ -1132,6 +1140,35 @@ thermo_status thermo_query_heatmap(thermo_ctx* ctx, uint32_t object_id, thermo_g
   size_t need = g == THERMO_WORD ? nw : g == THERMO_SECTOR ? ns : 9 * ns;
   if (n_out) *n_out = need;
   if (!out || cap < need) return fail(ctx, THERMO_ERANGE, "output capacity too small");
+  if (ctx->nranks > 1) {
+    // sharded: this rank's chunks of the object, from their local rows (one
+    // copy of the contiguous local range), other ranks' cells 0
+    const ull P = (ull)ctx->nranks, R = (ull)ctx->rank, C = kTileSectors;
+    const ull c_lo = so / C, c_hi = (so + ns - 1) / C;
+    ull f = c_lo + (R + P - c_lo % P) % P;  // first owned chunk >= c_lo
+    std::memset(out, 0, need * 4);
+    if (ns == 0 || f > c_hi) return THERMO_OK;
+    const ull last = c_hi - (c_hi + P - R) % P;          // last owned chunk <= c_hi (>= f)
+    const ull l0 = (f / P) * C, l1 = (last / P + 1) * C;   // local sectors [l0, l1)
+    std::vector<uint32_t> hw(8 * (l1 - l0)), hs(l1 - l0);
+    CK(cudaMemcpy(hw.data(), ctx->d_wc + 8 * l0, hw.size() * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hs.data(), ctx->d_sc + l0, hs.size() * 4, cudaMemcpyDeviceToHost));
+    for (ull c = f; c <= c_hi; c += P) {
+      const ull gs0 = std::max(so, c * C), gs1 = std::min(so + ns, (c + 1) * C);
+      for (ull gs = gs0; gs < gs1; ++gs) {
+        const ull li = shard_local(gs, ctx->nranks) - l0, s2 = gs - so;
+        for (int b = 0; b < 8; ++b) {
+          const ull w = 8 * s2 + b;
+          if (w >= nw) break;
+          if (g == THERMO_WORD) out[w] = hw[8 * li + b];
+          else if (g == THERMO_BOTH) out[9 * s2 + b] = hw[8 * li + b];
+        }
+        if (g == THERMO_SECTOR) out[s2] = hs[li];
+        else if (g == THERMO_BOTH) out[9 * s2 + 8] = hs[li];
+      }
+    }
+    return THERMO_OK;
+  }
   if (g == THERMO_WORD) {
     CK(cudaMemcpy(out, ctx->d_wc + 8 * so, nw * 4, cudaMemcpyDeviceToHost));
   } else if (g == THERMO_SECTOR) {
@@ -1372,6 +1409,7 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
   out->ms_exchange = ctx->ms_exchange;
   out->exchange_bytes = ctx->exchange_bytes;
   for (int k = 0; k < 9; ++k) out->ms_kernel[k] = ctx->ms_kernel[k];
+  out->local_sectors = ctx->S_own;
   return THERMO_OK;
 }
 

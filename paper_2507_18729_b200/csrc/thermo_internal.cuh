@@ -79,6 +79,18 @@ constexpr int kMaxRanks = 64;
 __host__ __device__ __forceinline__ uint32_t shard_owner(unsigned long long g, uint32_t nranks) {
   return nranks <= 1 ? 0u : (uint32_t)((g >> kShardShift) % nranks);
 }
+// local index of global sector g on its owner: the owned chunks packed in
+// chunk order (l = ((g >> c) / P) << c | (g & (2^c - 1))); an
+// owner's dense rows and count workspace cover only its chunks
+__host__ __device__ __forceinline__ unsigned long long shard_local(unsigned long long g, uint32_t nranks) {
+  return nranks <= 1 ? g
+                     : (((g >> kShardShift) / nranks) << kShardShift) | (g & ((1ull << kShardShift) - 1));
+}
+__host__ __device__ __forceinline__ unsigned long long shard_global(unsigned long long l, uint32_t rank,
+                                                                   uint32_t nranks) {
+  return nranks <= 1 ? l
+                     : ((((l >> kShardShift) * nranks) + rank) << kShardShift) | (l & ((1ull << kShardShift) - 1));
+}
 
 // ---- key layout -----------------------------------------------------------
 // key:     [ g : S ][ launch : L ][ warp : W ][ pcid : P ][ mask : 8 ]  (S+L+W+P <= 56)
@@ -213,8 +225,9 @@ void launch_dense_count(const ull* dm, uint32_t L, ull S_tot, uint32_t filter, u
 
 // a6 histograms over dense arrays, per object
 // (sharded mode: only the sectors rank owns; nranks = 1: all)
+// (sharded mode: rows of the rank's own chunks, local indices [0, n_local))
 void launch_object_hist(const uint32_t* word_cnt, const uint32_t* sector_cnt, ObjTable obj,
-                        const ull* obj_nwords, ull* hist /*[n_obj][2][33]*/, ull total_sectors,
+                        const ull* obj_nwords, ull* hist /*[n_obj][2][33]*/, ull total_sectors, ull n_local,
                         uint32_t rank, uint32_t nranks, int num_sms, cudaStream_t s);
 // a6 per-pc histograms from deduped pc keys
 void launch_pc_hist_sorted(const ull* pckeys, ull n, KeyLayout kl, const uint32_t* site_of,

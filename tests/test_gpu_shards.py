@@ -52,6 +52,14 @@ def compare(t, ref, shards):
     from paper_2507_18729_b200.dist import run_ranks
     P = len(shards)
     assert [s.sharding()[:2] for s in shards] == [(r, P) for r in range(P)]
+    # per-rank storage by construction (SURVEY §8e local index): rank r's dense
+    # rows cover its own 2048-sector chunks only
+    S_tot = sum((o[1] + 31) // 32 for o in t.objects)
+    nch = (S_tot + 2047) // 2048
+    for r, sh in enumerate(shards):
+        own = (nch - r + P - 1) // P if nch > r else 0
+        assert sh.stats()["local_sectors"] == (S_tot if P == 1 else max(1, own) * 2048)
+    assert ref.stats()["local_sectors"] == S_tot
     for obj in t.objects:
         oid = obj[3]
         for gran in (WORD, SECTOR, BOTH):
