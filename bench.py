@@ -533,7 +533,7 @@ def run_local_shards(args, P):
     torch.cuda.synchronize()
     el = (time.perf_counter() - t0) / args.steps
     ranks = [{"rank": r, "records": int(slices[r].shape[0]), "local_sectors": st["local_sectors"],
-              "dense_row_bytes": 36 * st["local_sectors"], "keys_counted": st["keys_emitted"],
+              "dense_row_bytes": 36 * st["local_sectors"], "keys_counted": st["local_keys"],
               "exchange_bytes_sent": st["exchange_bytes"], "ms_ingest": st["ms_ingest"], "ms_build": st["ms_build"],
               "ms_classify": st["ms_classify"], "ms_exchange": st["ms_exchange"],
               "ms_kernel": {k: v for k, v in st["ms_kernel"].items() if v > 0}} for r, st in enumerate(sts)]

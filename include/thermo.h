@@ -235,6 +235,9 @@ typedef struct {
   /* sectors this context's dense rows and count workspace cover: all
    * registered sectors, or (sharded mode) the rank's own 2048-sector chunks */
   uint64_t local_sectors;
+  /* keys this context counts in its build (sharded mode: the keys it owns
+   * after the exchange; one rank: every key) */
+  uint64_t local_keys;
 } thermo_stats;
 enum {
   THERMO_K_DECODE = 0,         /* decode_kernel: fast per-instruction decode (a2+a3)        */

@@ -1410,6 +1410,7 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
   out->exchange_bytes = ctx->exchange_bytes;
   for (int k = 0; k < 9; ++k) out->ms_kernel[k] = ctx->ms_kernel[k];
   out->local_sectors = ctx->S_own;
+  out->local_keys = ctx->n_keys;
   return THERMO_OK;
 }
 

@@ -71,7 +71,7 @@ class thermo_stats(ctypes.Structure):
                 ("ms_classify", ctypes.c_double), ("ms_decode", ctypes.c_double), ("ms_dedup", ctypes.c_double),
                 ("ms_count", ctypes.c_double), ("ms_hist", ctypes.c_double), ("ms_pc", ctypes.c_double),
                 ("ms_indicators", ctypes.c_double), ("kernel_launches", u64),
-                ("ms_exchange", ctypes.c_double), ("exchange_bytes", u64), ("ms_kernel", ctypes.c_double * 9), ("local_sectors", u64)]
+                ("ms_exchange", ctypes.c_double), ("exchange_bytes", u64), ("ms_kernel", ctypes.c_double * 9), ("local_sectors", u64), ("local_keys", u64)]
 
 
 # every symbol include/thermo.h declares

@@ -60,7 +60,7 @@ def test_struct_sizes():
     assert ctypes.sizeof(thermo.thermo_params) == 22 * 8
     assert ctypes.sizeof(thermo.thermo_indicators) == 8 + 16 * 8
     assert ctypes.sizeof(thermo.thermo_pc_hist) == 8 + 33 * 8
-    assert ctypes.sizeof(thermo.thermo_stats) == 10 * 8 + 8 + 9 * 8 + 8 + 16 + 9 * 8 + 8  # + ms_kernel[9], local_sectors (ABI 5)
+    assert ctypes.sizeof(thermo.thermo_stats) == 10 * 8 + 8 + 9 * 8 + 8 + 16 + 9 * 8 + 16  # + ms_kernel[9], local_sectors, local_keys (ABI 5)
 
 
 def test_create_fails_loudly_without_gpu(lib):
