@@ -76,23 +76,44 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
   ull n_invalid = 0, n_oor = 0, n_mapped = 0, n_unmapped = 0;
   uint32_t cur_launch = 0xFFFFFFFFu;
 
+  // each warp takes a contiguous run of the deferred list (the fast kernel
+  // appends a warp's views 32 at a time, in trace order); the descriptors of
+  // the next 32 views are loaded together and the next view's records are in
+  // flight while the current one is reduced
   const ull n_views = *((volatile ull*)&a.ctr->n_deferred);
   const ull gwarp = ((ull)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const ull nwarps = ((ull)gridDim.x * blockDim.x) >> 5;
-  for (ull v = gwarp; v < n_views; v += nwarps) {
+  const ull per = ((n_views + 31) / 32 + nwarps - 1) / nwarps * 32;
+  const ull v0 = gwarp * per < n_views ? gwarp * per : n_views;
+  const ull v1 = v0 + per < n_views ? v0 + per : n_views;
+  ull dq = 0, vb = v0, e_nxt = 0;
+  uint4 nxt = make_uint4(0, 0, 0, 0);
+  if (v0 < v1) {
+    dq = v0 + lane < v1 ? a.deferred[v0 + lane] : 0ull;
+    e_nxt = __shfl_sync(FULL, dq, 0);
+    if (lane < (int)(e_nxt & 63)) nxt = ld_stream(&a.recs[(e_nxt >> 7) + lane]);
+  }
+  for (ull v = v0; v < v1; ++v) {
     // deferred view: p << 7 | stats_only << 6 | len (len <= 32).  stats_only:
     // the fast kernel already emitted this view's keys and word counters; only
     // the instruction statistics remain (a non-monotone instruction).  A view
     // may hold several whole instructions (short ones packed together by the
     // fast kernel): they start at the view's first record and at every
     // instr_start record inside it (G24)
-    const ull e = a.deferred[v];
-    const ull p = e >> 7;
+    const ull e = e_nxt;
+    const uint4 cur = nxt;
+    if (v + 1 < v1) {
+      if (v + 1 - vb >= 32) {
+        vb = v + 1;
+        dq = vb + lane < v1 ? a.deferred[vb + lane] : 0ull;
+      }
+      e_nxt = __shfl_sync(FULL, dq, (int)(v + 1 - vb));
+      nxt = make_uint4(0, 0, 0, 0);
+      if (lane < (int)(e_nxt & 63)) nxt = ld_stream(&a.recs[(e_nxt >> 7) + lane]);
+    }
     const bool keys_too = ((e >> 6) & 1u) == 0;
     const uint32_t len = (uint32_t)(e & 63);
     const bool act = lane < (int)len;
-    uint4 cur = make_uint4(0, 0, 0, 0);
-    if (act) cur = ld_stream(&a.recs[p + lane]);
     const ull af = ((ull)cur.y << 32) | cur.x;
     const uint32_t warp_id = cur.z, site = cur.w;
     const ull addr = af & ((1ull << 48) - 1);

@@ -61,22 +61,23 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   uint4* const ring = reinterpret_cast<uint4*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
   const uint32_t ring_lane = (uint32_t)__cvta_generic_to_shared(ring + lane);
   // warp-uniform caches kept in shared memory (registers are the kernel's
-  // occupancy limit): window entries e = 0, 1 as {H, blo, bn, sbase},
-  // {tail_s, tail_m, oid, -} at wc[2e], wc[2e + 1]; site -> pc id cache
-  // {site0, id0, site1, id1} at wc[4]
+  // occupancy limit): window entries e = 0..3 as {H, blo, bn, sbase},
+  // {tail_s, tail_m, oid, -} at wc[2e], wc[2e + 1] (four: SpMV's col / val / x
+  // loads alternate between three objects); site -> pc id cache
+  // {site0, id0, site1, id1} {site2, id2, site3, id3} at wc[8], wc[9]
   uint4* const wc = ring + kRingChunks * 32;
-  if (lane == 0) {
-    wc[0] = wc[2] = make_uint4(0xFFFFFFFFu, 0, 0, 0);
-    wc[1] = wc[3] = make_uint4(1, 0xFFu, 0xFFFFFFFFu, 0);
-    wc[4] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
+  if (lane < 4) {
+    wc[2 * lane] = make_uint4(0xFFFFFFFFu, 0, 0, 0);
+    wc[2 * lane + 1] = make_uint4(1, 0xFFu, 0xFFFFFFFFu, 0);
   }
-  DeferBuf dq{reinterpret_cast<ull*>(wc + 5), 0};
+  if (lane == 0) wc[8] = wc[9] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
+  uint32_t win_rr = 0, pc_rr = 0;  // round-robin replacement (uniform)
+  DeferBuf dq{reinterpret_cast<ull*>(wc + 10), 0};
   __syncwarp();
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
   InstrRegs ir;  // (launch, object) instruction counters for ids < 32
-  bool last1 = false;
   // this lane's two most recent dedup entries: (pc id << 32 | g) -> mask
   ull c0 = 0, c1 = 0;
   uint32_t m0 = 0, m1 = 0;
@@ -148,25 +149,27 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
       // Listing 1); its lanes are all in lane 0's interval, merge into lane 0
       // and span one sector run (never misaligned), so those steps are skipped
       const bool bcast = __ballot_sync(FULL, act & (x != x0)) == 0;
-      const uint4 A0 = wc[0], A1 = wc[2];
-      const bool h0 = (A0.x == H) & (xs0 - A0.y < A0.z), h1 = (A1.x == H) & (xs0 - A1.y < A1.z);
+      // lane e < 4 tests window entry e; one ballot finds the hit
+      uint4 Ae = make_uint4(0, 0, 0, 0);
+      if (lane < 4) Ae = wc[2 * lane];
+      const unsigned hits = __ballot_sync(FULL, (lane < 4) & (Ae.x == H) & (xs0 - Ae.y < Ae.z));
       uint32_t blo, bn, sbase, tail_s, tail_m;
       int oid0;
-      if (!(h0 | h1)) {  // uniform miss: replace the entry not used last
+      if (!hits) {  // uniform miss: replace the round-robin entry
         const WinEnt ne = win_lookup(sm.lo, sm.hi, sm.soff, nobj, steps, H, xs0);
-        const int e = last1 ? 0 : 1;
+        const uint32_t e = win_rr;
+        win_rr = (win_rr + 1) & 3u;
         __syncwarp();  // every lane has read the entries before lane 0 replaces one
         if (lane == 0) {
           wc[2 * e] = make_uint4(ne.H, ne.blo, ne.bn, ne.sbase);
           wc[2 * e + 1] = make_uint4(ne.tail_s, ne.tail_m, (uint32_t)ne.oid, 0);
         }
         __syncwarp();  // and the warp sees it from the next view on
-        last1 = e == 1;
         blo = ne.blo; bn = ne.bn; sbase = ne.sbase; tail_s = ne.tail_s; tail_m = ne.tail_m; oid0 = ne.oid;
       } else {
-        last1 = !h0;
-        const uint4 A = last1 ? A1 : A0;
-        const uint4 B = wc[last1 ? 3 : 1];
+        const uint32_t e = __ffs(hits) - 1;
+        const uint4 A = wc[2 * e];
+        const uint4 B = wc[2 * e + 1];
         blo = A.y; bn = A.z; sbase = A.w; tail_s = B.x; tail_m = B.y; oid0 = (int)B.z;
       }
       // lane 0's first word is mapped (uniform, from lane 0's interval): its
@@ -228,19 +231,21 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         }
         uint32_t pcid = 0;
         if (a.track_pc) {
-          const uint4 pcc = wc[4];  // two most recent sites (uniform)
-          if (w0 == pcc.x) {
-            pcid = pcc.y;
-          } else if (w0 == pcc.z) {
-            pcid = pcc.w;
+          // four cached sites (uniform): lane e < 4 tests entry e
+          const uint32_t* const pcw = reinterpret_cast<const uint32_t*>(wc + 8);
+          const unsigned ph = __ballot_sync(FULL, (lane < 4) && pcw[2 * (lane & 3)] == w0);
+          if (ph) {
+            pcid = pcw[2 * (__ffs(ph) - 1) + 1];
           } else {
             uint32_t id = 0;
             __syncwarp();  // (as for the window entries)
             if (lane == 0) {
               id = pc_lookup(sm.pc, a.pcmap, w0, a.ctr);
               id = id < a.pcmap.max_pcs ? id : 0u;  // overflow is reported at build (ERANGE)
-              wc[4] = make_uint4(w0, id, pcc.x, pcc.y);
+              reinterpret_cast<uint32_t*>(wc + 8)[2 * pc_rr] = w0;
+              reinterpret_cast<uint32_t*>(wc + 8)[2 * pc_rr + 1] = id;
             }
+            pc_rr = (pc_rr + 1) & 3u;
             __syncwarp();
             pcid = __shfl_sync(FULL, id, 0);
           }

@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   }
   if (!pc_hist) return;
   // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
-  for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
+  for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
   for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
   __syncthreads();
   const ull pmask = (1ull << kl.P) - 1;
