@@ -978,6 +978,19 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
   bool pc_done = false;
+  // measurement hook (SORT vs CUB): THERMO_DUMP_KEYS=<path> writes
+  // the retained keys (u64, little-endian) and their prefix width to <path> at
+  // build; never set in tests or the bench
+  if (const char* dump = getenv("THERMO_DUMP_KEYS")) {
+    std::vector<ull> hk(ctx->n_keys);
+    if (ctx->n_keys) CK(cudaMemcpy(hk.data(), ctx->d_keys, ctx->n_keys * 8, cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(dump, "wb")) {
+      const ull hdr[2] = {ctx->n_keys, (ull)(kl.S + kl.L + kl.W + kl.P)};
+      fwrite(hdr, 8, 2, f);
+      fwrite(hk.data(), 8, hk.size(), f);
+      fclose(f);
+    }
+  }
   // ---- a4 dedup + a5 count (+ a6 per-pc on the segment path) ----
   if (mode == THERMO_DEDUP_SEGMENT) {
     // counting sort by sector (two partition passes) + per-chunk shared-memory
