@@ -190,8 +190,11 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
       ull pb = fb ? (((((ull)gb << LW) | lw) << P) | pcid) : ~0ull;
       bool ha = fa != 0, hb = fb != 0;
       uint32_t mA = fa, mB = fb;
-      adjacent_merge(pa, mA, ha, lane);
-      if (__any_sync(FULL, hb)) adjacent_merge(pb, mB, hb, lane);
+      // (the general kernel does not use the warp's record ring: its first 32
+      // words are the merge scratch)
+      uint32_t* const scr = reinterpret_cast<uint32_t*>(sm.warp + wib * kWarpRegion + kStage * sizeof(ull));
+      group_merge(pa, mA, ha, scr, lane);
+      if (__any_sync(FULL, hb)) group_merge(pb, mB, hb, scr, lane);
       STAGE_PUSH(st, ha, (pa << 8) | mA, a.keys, &a.ctr->n_keys);
       STAGE_PUSH(st, hb, (pb << 8) | mB, a.keys, &a.ctr->n_keys);
     }

@@ -83,6 +83,24 @@ __device__ __forceinline__ void adjacent_merge(ull& prefix, uint32_t& mask, bool
   if (same) has = false;
 }
 
+// merge equal 64-bit prefixes held by ANY lanes of the view (general path:
+// a view of packed short instructions holds one source warp's consecutive
+// col[e], col[e+1] loads on non-adjacent lanes): the lowest lane of each
+// group gets the OR of the group's masks (through the warp's 32-word scratch),
+// the others drop their key
+__device__ __forceinline__ void group_merge(ull prefix, uint32_t& mask, bool& has, uint32_t* scr, int lane) {
+  const unsigned grp = __match_any_sync(FULL, has ? prefix : ~0ull);
+  if (!__any_sync(FULL, has && grp != (1u << lane))) return;
+  const int ldr = __ffs(grp) - 1;
+  if (has && ldr == lane) scr[lane] = mask;
+  __syncwarp();
+  if (has && ldr != lane) atomicOr(&scr[ldr], mask);
+  __syncwarp();
+  if (has && ldr == lane) mask = scr[lane];
+  has = has && ldr == lane;
+  __syncwarp();
+}
+
 // same on 32-bit sector ids (fast path: launch/warp are uniform)
 // (g < 2^31 where has: the previous lane's g is shuffled as kNoG when it has no key)
 __device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, bool& has, int lane) {
