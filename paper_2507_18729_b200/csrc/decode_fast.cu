@@ -87,7 +87,15 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   const uint32_t gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
 
-  for (uint32_t r = gwarp; r < a.n_ranges; r += nwarps) {
+  // ranges are handed out dynamically (their costs differ: SpMV rows), so the
+  // warps finish together instead of waiting for the slowest static share
+  (void)gwarp;
+  (void)nwarps;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = (uint32_t)atomicAdd(&a.ctr->next_range, 1ull);
+    r = __shfl_sync(FULL, r, 0);
+    if (r >= a.n_ranges) break;
     const ull p0 = a.heads[r];
     const uint32_t rlen = (uint32_t)(a.heads[r + 1] - p0);  // ingest calls hold < 2^32 records
     const uint4* const rbase = a.recs + p0;

@@ -245,7 +245,7 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n, bool time
     ctx->deferred_cap = n + n / 4 + 1024;
     CK(dalloc(&ctx->d_deferred, ctx->deferred_cap));
   }
-  CK(cudaMemsetAsync(&ctx->d_ctr->n_deferred, 0, sizeof(ull), ctx->stream));
+  CK(cudaMemsetAsync(&ctx->d_ctr->n_deferred, 0, 2 * sizeof(ull), ctx->stream));  // + next_range
   launch_find_heads(recs, n, kRangeLen, (uint32_t)n_ranges, ctx->d_heads, ctx->stream);
   DecodeArgs a = decode_args(ctx);
   a.recs = recs;

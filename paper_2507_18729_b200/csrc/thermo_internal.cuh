@@ -52,7 +52,8 @@ struct DevCounters {
   ull distinct_pc;     // set by the per-pc kernel
   ull hash_fail;       // hash-table insert failures (probe limit)
   ull n_deferred;      // views deferred to the general decode kernel (per call)
-  ull pad[6];
+  ull next_range;      // decode work ranges handed out so far (per call)
+  ull pad[5];
 };
 
 // ---- object table in device memory, sorted by (space << 48 | base) -------
