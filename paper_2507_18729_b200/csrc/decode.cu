@@ -214,13 +214,35 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_general_kernel(DecodeAr
       const uint32_t i_launch = __shfl_sync(FULL, launch, f);
       // min / max byte over the instruction's valid records: segmented scans
       ull mn = valid ? lo : ~0ull, mx = valid ? hi : 0ull;
-      for (int d = 1; d < 32; d <<= 1) {
-        const ull omn = __shfl_down_sync(FULL, mn, d), omx = __shfl_down_sync(FULL, mx, d);
-        if (lane + d < e0) { mn = omn < mn ? omn : mn; mx = omx > mx ? omx : mx; }
+      uint32_t distinct;
+      const bool any_strad = __ballot_sync(FULL, valid && strad) != 0;
+      // every instruction of the view is one record (SpMV's divergent rows):
+      // its min and max are its own bytes, and it touches one sector
+      const bool all_single = !any_strad && __all_sync(FULL, !valid || segm == (1u << lane));
+      // all valid bytes in one 4 GiB window (space, addr[32, 48)): 32-bit scans
+      const uint32_t hw0 = __shfl_sync(FULL, (uint32_t)(lo >> 32), f);
+      const bool win32 = __all_sync(FULL, !valid || (((uint32_t)(lo >> 32) == hw0) && ((uint32_t)(hi >> 32) == hw0)));
+      if (all_single) {
+        distinct = 1;
+      } else if (win32 && !any_strad) {
+        uint32_t mn32 = valid ? (uint32_t)lo : 0xFFFFFFFFu, mx32 = valid ? (uint32_t)hi : 0u;
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t omn = __shfl_down_sync(FULL, mn32, d), omx = __shfl_down_sync(FULL, mx32, d);
+          if (lane + d < e0) { mn32 = omn < mn32 ? omn : mn32; mx32 = omx > mx32 ? omx : mx32; }
+        }
+        mn = ((ull)hw0 << 32) | mn32;
+        mx = ((ull)hw0 << 32) | mx32;
+        const unsigned m = __match_any_sync(FULL, valid ? ((uint32_t)lo >> 5) : (0xF8000000u | (uint32_t)lane));
+        distinct = __popc(__ballot_sync(FULL, valid && (__ffs(m & segm) - 1 == lane)) & segm);
+      } else {
+        for (int d = 1; d < 32; d <<= 1) {
+          const ull omn = __shfl_down_sync(FULL, mn, d), omx = __shfl_down_sync(FULL, mx, d);
+          if (lane + d < e0) { mn = omn < mn ? omn : mn; mx = omx > mx ? omx : mx; }
+        }
       }
       // (lane s0 now holds its instruction's min and max)
-      uint32_t distinct;
-      if (__ballot_sync(FULL, valid && strad) == 0) {
+      if (all_single || (win32 && !any_strad)) {
+      } else if (!any_strad) {
         const unsigned m = __match_any_sync(FULL, valid ? sa : (0xFFFF000000000000ull | (ull)lane));
         distinct = __popc(__ballot_sync(FULL, valid && (__ffs(m & segm) - 1 == lane)) & segm);
       } else {

@@ -735,7 +735,8 @@ __global__ void seg_big_plan_kernel(const ull* __restrict__ boff, const ull* __r
       const ull K = (i + 1 < nbs ? boff[i + 1] : tot[2]) - boff[i];
       v0 = (K + kBigFill - 1) / kBigFill;
       const ull kp = K < npc ? K : npc;
-      v1 = (kp + kBigFill - 1) / kBigFill;
+      // one-pass sectors bin their pc ids in the main kernel (counts final there)
+      v1 = v0 == 1 ? 0 : (kp + kBigFill - 1) / kBigFill;
     }
     ull i0 = v0, i1 = v1;
     for (int d = 1; d < 32; d <<= 1) {
@@ -773,7 +774,9 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
                                                              const ull* __restrict__ bg, const ull* __restrict__ tot,
                                                              const ull* __restrict__ pre, KeyLayout kl,
                                                              uint32_t filter, uint32_t* __restrict__ wc,
-                                                             uint32_t* __restrict__ sc, DevCounters* ctr) {
+                                                             uint32_t* __restrict__ sc,
+                                                             const uint32_t* __restrict__ site_of,
+                                                             ull* __restrict__ pc_hist, DevCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots]
   __shared__ uint32_t s_cnt[9];
@@ -823,6 +826,33 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
     atomicAdd(threadIdx.x == 8 ? &sc[g] : &wc[8 * g + threadIdx.x], s_cnt[threadIdx.x]);
     if (threadIdx.x == 8) atomicAdd(&ctr->distinct_pairs, (ull)s_cnt[8]);
   }
+  if (P != 1 || !pc_hist || !kl.P) return;
+  // ---- one-pass sector: its counts are final here, so its distinct pc ids
+  // (at most K <= kBigFill) are binned at once (G11) ----
+  const ull pmask = (1ull << kl.P) - 1;
+  const uint32_t scnt = s_cnt[8];
+  __syncthreads();
+  for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
+    const ull k = big[b0 + j];
+    const ull id = (k >> 8) & pmask;
+    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) continue;
+    if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+  }
+  __syncthreads();
+  uint32_t npc = 0;
+  for (int j = threadIdx.x; j < T; j += kSegThreads) {
+    const ull v = tab[j];
+    if (v == kHEmpty) continue;
+    ++npc;
+    const uint32_t pcid = (uint32_t)(v >> 8);
+    atomicAdd(&pc_hist[(pcid * 2 + 1) * kLevels + level_of_g(scnt)], 1ull);
+    for (uint32_t m = (uint32_t)v & 0xFFu; m; m &= m - 1)
+      atomicAdd(&pc_hist[(pcid * 2) * kLevels + level_of_g(s_cnt[__ffs(m) - 1])], 1ull);
+  }
+  for (int d = 16; d; d >>= 1) npc += __shfl_xor_sync(GFULL, npc, d);
+  if ((threadIdx.x & 31) == 0 && npc) atomicAdd(&ctr->distinct_pc, (ull)npc);
 }
 
 __global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __restrict__ big,
@@ -1010,7 +1040,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     smem_optin((const void*)seg_big_kernel, (int)bsm);
     smem_optin((const void*)seg_big_pc_kernel, (int)bsm);
     seg_big_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre, kl, filter, wc, sc,
-                                                             ctr);
+                                                             site_of, pc_hist, ctr);
     ws.launches += 2;
     if (pc_hist && kl.P) {
       seg_big_pc_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre + ws.big_cap,
