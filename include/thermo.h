@@ -404,7 +404,8 @@ thermo_status thermo_query_runs(thermo_ctx *ctx, uint32_t object_id, thermo_run 
  * they stand for; each record is one instruction (G24).  Instructions the fast
  * path does not take (invalid header, lanes in different 4 GiB windows,
  * straddling accesses) are reduced through their per-lane records.  Device
- * memory: up to 32 n per-lane records of spill space.  stats.records counts
+ * memory: spill space for the per-lane records of one chunk of instructions
+ * (2^20 host / 2^23 device records per chunk: at most 4 GiB).  stats.records counts
  * lane records.  Errors: EINVAL (NULL, misaligned, n >= 2^27), ESTATE, ENOMEM,
  * ECUDA.
  */

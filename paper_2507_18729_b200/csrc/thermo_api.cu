@@ -19,6 +19,7 @@ namespace {
 constexpr ull kRangeLen = 8192;          // records per decode work range
 constexpr ull kHostChunk = 1ull << 24;   // records per staged host chunk
 constexpr ull kWarpChunk = 1ull << 20;   // warp records per staged host chunk (272 MB)
+constexpr ull kWarpChunkDev = 1ull << 23;  // warp records per device-resident chunk (spill space <= 4 GiB)
 constexpr ull kTileSectors = 2048;       // indicator tile (256 threads x 8 sectors) = 1 << kShardShift
 static_assert(kTileSectors == (1ull << kShardShift), "a tile is one ownership chunk");
 
@@ -863,7 +864,7 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
   // chunk's decode (the device path is one chunk)
   // device records are decoded in the same chunks, so the spill space and the
   // key-buffer growth are bounded by one chunk, not by the whole call
-  const ull C = std::min<ull>(n, kWarpChunk);
+  const ull C = std::min<ull>(n, on_device ? kWarpChunkDev : kWarpChunk);
   const ull lanes_max = 32 * C;
   if (ctx->spill_cap < lanes_max) {  // worst case: every instruction of a chunk spills
     dfree(ctx->d_spill);
