@@ -1,15 +1,16 @@
 // segment.cu -- rows a4 + a5 (+ the per-pc part of a6), "sector-segmented"
-// dedup path: a counting sort of the keys by sector id, then one CTA per chunk
-// of consecutive sectors deduplicates its keys in shared memory, writes the
-// chunk's dense word/sector counts (the paper's popcount flush) and,
-// from the same keys, the per-pc level histograms (G11).
+// dedup path: a counting sort of the keys by sector id, then shared-memory
+// sets per chunk of consecutive sectors, which write the chunk's dense word /
+// sector counts (the paper's popcount flush) and, from the same keys,
+// the per-pc level histograms (G11).
 //
-// Why: a5 only needs the keys grouped per sector, and the sector range is
-// small (SGEMM: 163,840 sectors), so an exact counting sort by sector
-// (histogram, scan, scatter) groups them in ~3 streaming passes instead of one
-// LSD pass per 8 key bits; the (launch, warp) and (pc) dedup then runs in a
-// shared-memory hash set per chunk (one insert per key, no sort).  Sectors with more keys than a chunk holds make the caller
-// fall back to the onesweep path (thermo_api.cu).
+// Why: a5 only needs the keys grouped per sector.  The decoder counts keys per
+// sector as it writes them; scans give every sector its segment; two
+// onesweep-style partition passes (coarse buckets balanced by key count, then
+// chunks) move the keys there with coalesced writes; one CTA per chunk (< 4096
+// keys) dedups in shared memory.  Sectors with >= 2048 keys (hot sectors, e.g.
+// SpMV's power-law x columns) get their own segments and are reduced by one CTA
+// per (sector, warp-hash pass) in seg_big_kernel.
 #include "thermo_internal.cuh"
 
 namespace thermo {
