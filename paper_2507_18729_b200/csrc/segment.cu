@@ -256,6 +256,15 @@ __device__ __forceinline__ uint32_t block_excl_scan(const uint32_t* cnt, uint32_
   return tot;
 }
 
+// pass 1 needs only kCoarse bins: a smaller layout (more CTAs per SM)
+struct CoarseSmem {
+  uint32_t cnt[kCoarse];
+  uint32_t excl[kCoarse];
+  ull base[kCoarse];
+  ull stage[kPTile];
+  uint16_t sd[kPTile];
+  uint32_t wsum[kPT / 32];
+};
 struct PartSmem {
   uint32_t cnt[kFineBins];
   uint32_t excl[kFineBins];
@@ -270,7 +279,7 @@ __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restric
                                                          const uint16_t* __restrict__ cb, uint32_t ncoarse,
                                                          ull* __restrict__ ccur, ull* __restrict__ tmp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
+  CoarseSmem& sm = *reinterpret_cast<CoarseSmem*>(smem_raw);
   const int lane = threadIdx.x & 31;
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
@@ -559,12 +568,16 @@ __device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint
 // memory (or, for a chunk spanning > kHWin sectors, with warp-aggregated
 // global atomics); (b) distinct (sector, pc id) with OR-ed masks -> per-pc
 // level histograms (G11)
+// Persistent: a CTA takes chunks from a counter until none are left, so the
+// table and the per-pc bin table are initialised once per CTA (between chunks
+// only the slots a pass used are cleared) and the bins are flushed once.
 __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ off,
                                                                ull nsec, KeyLayout kl, uint32_t filter,
                                                                uint32_t* __restrict__ wc, uint32_t* __restrict__ sc,
                                                                const uint32_t* __restrict__ site_of,
                                                                ull* __restrict__ pc_hist, DevCounters* ctr,
-                                                               const ull* __restrict__ cs0) {
+                                                               const ull* __restrict__ cs0, ull nchunks,
+                                                               ull* __restrict__ chunk_ctr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ull* tab = reinterpret_cast<ull*>(smem_raw);                    // [kHSlots]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + kHSlots);     // [kHWin][5]: words (2b, 2b+1) as u16 pairs, sector
@@ -572,105 +585,123 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   uint32_t* tcnt = tbin + kPcBins;                                // [kPcBins]
   uint16_t* list = reinterpret_cast<uint16_t*>(tcnt + kPcBins);   // [2 kSegCap] occupied slots
   __shared__ uint32_t s_n[2];
+  __shared__ ull s_c;
   const int lane = threadIdx.x & 31;
-  const ull c = blockIdx.x;
-  const ull s0 = cs0[c], s1 = cs0[c + 1];
-  if (s0 >= s1) return;
-  const ull k0 = off[s0];
-  const uint32_t nk = (uint32_t)(off[s1] - k0);  // < 2 kSegCap
-  const ull win = s1 - s0;
-  const bool local = win <= (ull)kHWin;
   const uint32_t LW = kl.L + kl.W, RS = 8 + kl.P;
   const ull lwmask = (1ull << LW) - 1;
+  const ull pmask = (1ull << kl.P) - 1;
   for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
-  if (threadIdx.x < 2) s_n[threadIdx.x] = 0;
-  if (local)
-    for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
-  __syncthreads();
-  // ---- (a) distinct (sector, launch, warp) ----
-  chunk_insert_pass(tab, list, &s_n[0], seg, k0, nk, s0, kl, filter, LW, RS, lwmask);
-  __syncthreads();
-  const uint32_t nent = s_n[0];
-  for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
-    const uint32_t i = base + lane;
-    const bool occ = i < nent;
-    const ull v = occ ? tab[list[i]] : kHEmpty;
-    const uint32_t gl = occ ? (uint32_t)(v >> (8 + LW)) : 0xFFFFFFFFu;
-    const uint32_t m = occ ? (uint32_t)v & 0xFFu : 0u;
-    const unsigned peers = __match_any_sync(GFULL, gl);
-    uint32_t cb[8];
+  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
+  ull distinct = 0, distinct_pc = 0;  // thread 0's running totals
+  for (;;) {
+    __syncthreads();  // the previous chunk is done with s_c, s_n and its table slots
+    if (threadIdx.x == 0) {
+      s_c = atomicAdd(chunk_ctr, 1ull);
+      s_n[0] = s_n[1] = 0;
+    }
+    __syncthreads();
+    const ull c = s_c;
+    if (c >= nchunks) break;
+    const ull s0 = cs0[c], s1 = cs0[c + 1];
+    if (s0 >= s1) continue;  // (uniform)
+    const ull k0 = off[s0];
+    const uint32_t nk = (uint32_t)(off[s1] - k0);  // < 2 kSegCap
+    const ull win = s1 - s0;
+    const bool local = win <= (ull)kHWin;
+    if (local)
+      for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
+    __syncthreads();
+    // ---- (a) distinct (sector, launch, warp) ----
+    chunk_insert_pass(tab, list, &s_n[0], seg, k0, nk, s0, kl, filter, LW, RS, lwmask);
+    __syncthreads();
+    const uint32_t nent = s_n[0];
+    for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
+      const uint32_t i = base + lane;
+      const bool occ = i < nent;
+      const ull v = occ ? tab[list[i]] : kHEmpty;
+      const uint32_t gl = occ ? (uint32_t)(v >> (8 + LW)) : 0xFFFFFFFFu;
+      const uint32_t m = occ ? (uint32_t)v & 0xFFu : 0u;
+      const unsigned peers = __match_any_sync(GFULL, gl);
+      uint32_t cb[8];
 #pragma unroll
-    for (int b = 0; b < 8; ++b) cb[b] = __popc(__ballot_sync(GFULL, (m >> b) & 1u) & peers);
-    if (occ && lane == __ffs(peers) - 1) {
-      const uint32_t cs = __popc(peers);
-      if (local) {
-        uint32_t* cg = cnt + gl * 5;
+      for (int b = 0; b < 8; ++b) cb[b] = __popc(__ballot_sync(GFULL, (m >> b) & 1u) & peers);
+      if (occ && lane == __ffs(peers) - 1) {
+        const uint32_t cs = __popc(peers);
+        if (local) {
+          uint32_t* cg = cnt + gl * 5;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
-        atomicAdd(&cg[4], cs);
-      } else {
-        const ull g = s0 + gl;
-        atomicAdd(&sc[g], cs);
+          for (int j = 0; j < 4; ++j)
+            if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
+          atomicAdd(&cg[4], cs);
+        } else {
+          const ull g = s0 + gl;
+          atomicAdd(&sc[g], cs);
 #pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (cb[b]) atomicAdd(&wc[8 * g + b], cb[b]);
+          for (int b = 0; b < 8; ++b)
+            if (cb[b]) atomicAdd(&wc[8 * g + b], cb[b]);
+        }
       }
     }
-  }
-  if (threadIdx.x == 0 && nent) atomicAdd(&ctr->distinct_pairs, (ull)nent);
-  __syncthreads();
-  if (local) {  // the chunk owns its sectors: plain stores of the nonzero rows
-    for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
-      const uint32_t* cg = cnt + j * 5;
-      if (cg[4] == 0) continue;
-      const ull g = s0 + j;
-      sc[g] = cg[4];
-      uint4 lo, hi;
-      lo.x = cg[0] & 0xFFFFu; lo.y = cg[0] >> 16; lo.z = cg[1] & 0xFFFFu; lo.w = cg[1] >> 16;
-      hi.x = cg[2] & 0xFFFFu; hi.y = cg[2] >> 16; hi.z = cg[3] & 0xFFFFu; hi.w = cg[3] >> 16;
-      reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
-      reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
+    distinct += nent;
+    __syncthreads();
+    if (local) {  // the chunk owns its sectors: plain stores of the nonzero rows
+      for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
+        const uint32_t* cg = cnt + j * 5;
+        if (cg[4] == 0) continue;
+        const ull g = s0 + j;
+        sc[g] = cg[4];
+        uint4 lo, hi;
+        lo.x = cg[0] & 0xFFFFu; lo.y = cg[0] >> 16; lo.z = cg[1] & 0xFFFFu; lo.w = cg[1] >> 16;
+        hi.x = cg[2] & 0xFFFFu; hi.y = cg[2] >> 16; hi.z = cg[3] & 0xFFFFu; hi.w = cg[3] >> 16;
+        reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
+        reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
+      }
     }
-  }
-  if (!pc_hist) return;
-  // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
-  for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
-  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
-  __syncthreads();
-  const ull pmask = (1ull << kl.P) - 1;
-  chunk_insert_pass(tab, list, &s_n[1], seg, k0, nk, s0, kl, filter, kl.P, 8, pmask);
-  __syncthreads();
-  const uint32_t npc = s_n[1];
-  for (uint32_t base = threadIdx.x & ~31u; base < npc; base += kSegThreads) {
-    const uint32_t i = base + lane;
-    const bool head = i < npc;
-    const ull v = head ? tab[list[i]] : kHEmpty;
-    const uint32_t gl = (uint32_t)(v >> (8 + kl.P));
-    const uint32_t pcid = (uint32_t)((v >> 8) & pmask);
-    const uint32_t m = (uint32_t)v & 0xFFu;
-    const uint32_t* cg = cnt + gl * 5;
-    const ull g = s0 + gl;
-    {
-      const uint32_t scv = head ? (local ? cg[4] : __ldcg(&sc[g])) : 0u;
-      const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(scv) : 0xFFFFFFFFu;
-      const unsigned mm = __match_any_sync(GFULL, bin);
-      if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
-    }
+    for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
+    if (!pc_hist) continue;  // (uniform)
+    __syncthreads();
+    // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
+    chunk_insert_pass(tab, list, &s_n[1], seg, k0, nk, s0, kl, filter, kl.P, 8, pmask);
+    __syncthreads();
+    const uint32_t npc = s_n[1];
+    for (uint32_t base = threadIdx.x & ~31u; base < npc; base += kSegThreads) {
+      const uint32_t i = base + lane;
+      const bool head = i < npc;
+      const ull v = head ? tab[list[i]] : kHEmpty;
+      const uint32_t gl = (uint32_t)(v >> (8 + kl.P));
+      const uint32_t pcid = (uint32_t)((v >> 8) & pmask);
+      const uint32_t m = (uint32_t)v & 0xFFu;
+      const uint32_t* cg = cnt + gl * 5;
+      const ull g = s0 + gl;
+      {
+        const uint32_t scv = head ? (local ? cg[4] : __ldcg(&sc[g])) : 0u;
+        const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(scv) : 0xFFFFFFFFu;
+        const unsigned mm = __match_any_sync(GFULL, bin);
+        if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+      }
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const bool hb = head && ((m >> b) & 1u);
-      uint32_t wv = 0;
-      if (hb) wv = local ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : __ldcg(&wc[8 * g + b]);
-      const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wv) : 0xFFFFFFFFu;
-      const unsigned mm = __match_any_sync(GFULL, bin);
-      if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+      for (int b = 0; b < 8; ++b) {
+        const bool hb = head && ((m >> b) & 1u);
+        uint32_t wv = 0;
+        if (hb) wv = local ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : __ldcg(&wc[8 * g + b]);
+        const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wv) : 0xFFFFFFFFu;
+        const unsigned mm = __match_any_sync(GFULL, bin);
+        if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+      }
     }
+    distinct_pc += npc;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < npc; i += kSegThreads) tab[list[i]] = kHEmpty;
   }
-  if (threadIdx.x == 0 && npc) atomicAdd(&ctr->distinct_pc, (ull)npc);
-  __syncthreads();
-  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
-    if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
+  if (threadIdx.x == 0) {
+    if (distinct) atomicAdd(&ctr->distinct_pairs, distinct);
+    if (distinct_pc) atomicAdd(&ctr->distinct_pc, distinct_pc);
+  }
+  if (pc_hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
+      if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
+  }
   (void)site_of;
   (void)nsec;
 }
@@ -1002,8 +1033,8 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     if ((e = cudaMalloc(&ws.tmp, (n + n / 8 + 1024) * sizeof(ull)))) return e;
     ws.tmp_cap = n + n / 8 + 1024;
   }
-  const size_t psm = sizeof(PartSmem);
-  smem_optin((const void*)seg_coarse_kernel, (int)psm);
+  const size_t psm = sizeof(PartSmem), csm = sizeof(CoarseSmem);
+  smem_optin((const void*)seg_coarse_kernel, (int)csm);
   smem_optin((const void*)seg_fine_kernel, (int)psm);
   for (int k = 0; k < 4; ++k) ws.ran[k] = false;
   if (ws.ev[0]) cudaEventRecord(ws.ev[0], s);
@@ -1011,7 +1042,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
     seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
     const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
-    seg_coarse_kernel<<<g1, kPT, psm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
+    seg_coarse_kernel<<<g1, kPT, csm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
     if (ws.ev[1]) cudaEventRecord(ws.ev[1], s);
     const ull g2 = (n + kPTile - 1) / kPTile + ws.ncoarse;  // >= the tiles of all buckets
     seg_fine_kernel<<<(unsigned)g2, kPT, psm, s>>>(ws.tmp, kl, ws.ncoarse, ws.cstart, ws.cinfo, ws.tpre, ws.dst,
@@ -1025,8 +1056,13 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   const ull chunks = (n + kSegCap - 1) / kSegCap;
   if (chunks) {
     if (ws.ev[2] && !n) cudaEventRecord(ws.ev[2], s);
-    seg_chunk_kernel<<<(unsigned)chunks, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
-                                                                  pc_hist, ctr, ws.cs0);
+    if (!ws.chunk_ctr && (e = cudaMalloc(&ws.chunk_ctr, sizeof(ull)))) return e;
+    cudaMemsetAsync(ws.chunk_ctr, 0, sizeof(ull), s);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_chunk_kernel, kSegThreads, smem);
+    const ull grid = std::min<ull>(chunks, (ull)num_sms * (per_sm < 1 ? 1 : per_sm));
+    seg_chunk_kernel<<<(unsigned)grid, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
+                                                               pc_hist, ctr, ws.cs0, chunks, ws.chunk_ctr);
     ws.launches += 1;
     ws.ran[2] = true;
   }

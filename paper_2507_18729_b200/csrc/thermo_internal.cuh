@@ -186,6 +186,7 @@ struct SegWorkspace {
   ull* bcur = nullptr;       // [n big sectors] pass-2 cursors
   ull* bpre = nullptr;       // [2][big_cap] first CTA of each big sector (main, pc passes)
   ull big_cap = 0, n_bigsec = 0, n_big_keys = 0;
+  ull* chunk_ctr = nullptr;  // persistent chunk kernel: chunks handed out
   // per-kernel timers (created by the caller): before coarse, after coarse,
   // after fine, after chunk, after big; ran[] says which intervals ran
   cudaEvent_t ev[5] = {};
