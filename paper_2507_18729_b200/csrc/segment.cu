@@ -256,15 +256,30 @@ __device__ __forceinline__ uint32_t block_excl_scan(const uint32_t* cnt, uint32_
   return tot;
 }
 
-// pass 1 needs only kCoarse bins: a smaller layout (more CTAs per SM)
+// pass 1 needs only kCoarse bins; two tile buffers: the next tile's keys land
+// (cp.async) while the current one is ranked, staged and written
 struct CoarseSmem {
   uint32_t cnt[kCoarse];
   uint32_t excl[kCoarse];
   ull base[kCoarse];
-  ull stage[kPTile];
+  ull buf[2][kPTile];   // [cur]: this tile's keys, then its staged order; [cur ^ 1]: the next tile
   uint16_t sd[kPTile];
   uint32_t wsum[kPT / 32];
 };
+
+// this thread's share of tile t0's keys -> dst (8-byte cp.async, zero-filled past n)
+__device__ __forceinline__ void tile_prefetch(ull* dst, const ull* __restrict__ keys, ull t0, ull n) {
+#pragma unroll
+  for (int u = 0; u < kPPer; ++u) {
+    const uint32_t j = u * kPT + threadIdx.x;
+    const ull i = t0 + j;
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + j);
+    const ull* src = keys + (i < n ? i : 0);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(i < n ? 8 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
 struct PartSmem {
   uint32_t cnt[kFineBins];
   uint32_t excl[kFineBins];
@@ -274,7 +289,7 @@ struct PartSmem {
   uint32_t wsum[kPT / 32];
 };
 
-// pass 1: tiles of 4096 keys -> coarse buckets
+// pass 1: tiles of 4096 keys -> coarse buckets (persistent, double-buffered)
 __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restrict__ keys, ull n, KeyLayout kl,
                                                          const uint16_t* __restrict__ cb, uint32_t ncoarse,
                                                          ull* __restrict__ ccur, ull* __restrict__ tmp) {
@@ -283,15 +298,22 @@ __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restric
   const int lane = threadIdx.x & 31;
   unsigned lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  for (ull t0 = (ull)blockIdx.x * kPTile; t0 < n; t0 += (ull)gridDim.x * kPTile) {
-    for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT) sm.cnt[i] = 0;
-    __syncthreads();
+  const ull stride = (ull)gridDim.x * kPTile;
+  ull t0 = (ull)blockIdx.x * kPTile;
+  for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT) sm.cnt[i] = 0;
+  if (t0 < n) tile_prefetch(sm.buf[0], keys, t0, n);
+  int cur = 0;
+  for (; t0 < n; t0 += stride) {
+    if (t0 + stride < n) tile_prefetch(sm.buf[cur ^ 1], keys, t0 + stride, n);
+    else asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this tile's keys (own copies) landed
+    __syncthreads();                                          // everyone's
     ull k[kPPer];
     uint32_t b[kPPer], r[kPPer];
 #pragma unroll
     for (int u = 0; u < kPPer; ++u) {
       const ull i = t0 + (ull)u * kPT + threadIdx.x;
-      k[u] = i < n ? keys[i] : 0ull;
+      k[u] = sm.buf[cur][u * kPT + threadIdx.x];
       b[u] = i < n ? (uint32_t)cb[key_g(k[u], kl) / kGroup] : 0xFFFFFFFFu;
     }
 #pragma unroll
@@ -306,20 +328,24 @@ __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restric
     for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT)
       if (sm.cnt[i]) sm.base[i] = atomicAdd(&ccur[i], (ull)sm.cnt[i]);
     const uint32_t tot = block_excl_scan(sm.cnt, sm.excl, ncoarse, sm.wsum);
+    ull* const stage = sm.buf[cur];  // every thread has its keys in registers by now
 #pragma unroll
     for (int u = 0; u < kPPer; ++u)
       if (b[u] != 0xFFFFFFFFu) {
         const uint32_t q = sm.excl[b[u]] + r[u];
-        sm.stage[q] = k[u];
+        stage[q] = k[u];
         sm.sd[q] = (uint16_t)b[u];
       }
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < tot; i += kPT) {
       const uint32_t bb = sm.sd[i];
-      tmp[sm.base[bb] + (i - sm.excl[bb])] = sm.stage[i];
+      tmp[sm.base[bb] + (i - sm.excl[bb])] = stage[i];
     }
-    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT) sm.cnt[i] = 0;
+    __syncthreads();  // stage read out, counters clear: buf[cur] takes the tile after next
+    cur ^= 1;
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // tiles of every coarse bucket (tpre[b] = first tile of bucket b) and the
