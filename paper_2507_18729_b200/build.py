@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJDIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libthermo.so")
-SOURCES = ["decode.cu", "decode_fast.cu", "decode_warp.cu", "sort.cu", "segment.cu", "dense.cu", "count.cu", "indicators.cu", "shard.cu", "export.cu", "thermo_api.cu"]
+SOURCES = ["decode.cu", "decode_fast.cu", "decode_lane.cu", "decode_warp.cu", "sort.cu", "segment.cu", "dense.cu", "count.cu", "indicators.cu", "shard.cu", "export.cu", "thermo_api.cu"]
 HEADERS = ["thermo_internal.cuh", "decode_common.cuh", "shard.cuh", os.path.join("..", "..", "include", "thermo.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -229,7 +229,9 @@ constexpr int kAhead = 6;               // chunks in flight ahead of the current
 constexpr uint32_t kShortView = 8;      // instructions shorter than this are packed for the general kernel
 constexpr size_t kWarpCache = 10 * 16;  // fast kernel: four window-cache entries (4 x 2 uint4) + pc-id cache (2 uint4)
 constexpr int kDeferBuf = 32;           // fast kernel: deferred-view descriptors staged per warp
-constexpr size_t kWarpRegion = kStage * sizeof(ull) + kRingChunks * 32 * 16 + kWarpCache + kDeferBuf * sizeof(ull);
+// + 32 words of merge scratch (lane decoder)
+constexpr size_t kOffScratch = kStage * sizeof(ull) + kRingChunks * 32 * 16 + kWarpCache + kDeferBuf * sizeof(ull);
+constexpr size_t kWarpRegion = kOffScratch + 32 * sizeof(uint32_t);
 // fixed-size parts first, at compile-time offsets (addresses are immediates,
 // nothing to keep in registers); the object table (3 x n u64) last
 constexpr size_t kOffIval = 0;                                         // [kInstrSlots][2] u64

@@ -254,7 +254,10 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n, bool time
   a.heads = ctx->d_heads;
   a.n_ranges = (uint32_t)n_ranges;
   CK(cudaEventRecord(ctx->evk[0], ctx->stream));
-  launch_decode(a, ctx->num_sms, ctx->stream);
+  // THERMO_DECODER=view: the view-per-instruction kernel (decode_fast.cu), for comparison
+  static const bool view = getenv("THERMO_DECODER") && std::string(getenv("THERMO_DECODER")) == "view";
+  if (view) launch_decode(a, ctx->num_sms, ctx->stream);
+  else launch_decode_lane(a, ctx->num_sms, ctx->stream);
   CK(cudaEventRecord(ctx->evk[1], ctx->stream));
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());
