@@ -551,6 +551,43 @@ __device__ __forceinline__ bool hset_or(ull* tab, ull id, uint32_t m, uint32_t& 
   }
 }
 
+// the chunk's keys, held in registers for both insert passes: thread t holds
+// keys t, t + 256, ... (a chunk holds < 2 kSegCap = 16 x 256 keys)
+constexpr int kKPT = 2 * kSegCap / kSegThreads;
+__device__ __forceinline__ void chunk_load(ull (&kk)[kKPT], const ull* __restrict__ seg, ull k0, uint32_t nk) {
+#pragma unroll
+  for (int j = 0; j < kKPT; ++j) {
+    const uint32_t i = j * kSegThreads + threadIdx.x;
+    kk[j] = i < nk ? __ldcs(&seg[k0 + i]) : 0ull;  // (streamed: read once)
+  }
+}
+// one insert pass over the chunk's keys kk: id = (sector - s0) << A | (key >> B)
+// & M, mask = the key's low 8 bits; new slots appended to `list`
+__device__ __forceinline__ void chunk_insert_regs(ull* tab, uint16_t* list, uint32_t* nlist, const ull (&kk)[kKPT],
+                                                  uint32_t nk, ull s0, const KeyLayout& kl, uint32_t filter,
+                                                  uint32_t A, uint32_t B, ull M) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;  // (uniform)
+#pragma unroll
+  for (int j = 0; j < kKPT; ++j) {
+    if ((uint32_t)j >= jmax) break;
+    const ull k = kk[j];
+    bool ok = j * kSegThreads + threadIdx.x < nk;
+    if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
+    uint32_t slot = 0;
+    const bool nw = ok && hset_or(tab, ((key_g(k, kl) - s0) << A) | ((k >> B) & M), (uint32_t)k & 0xFFu, slot);
+    const unsigned b = __ballot_sync(GFULL, nw);
+    if (b) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(nlist, (uint32_t)__popc(b));
+      base = __shfl_sync(GFULL, base, 0);
+      if (nw) list[base + __popc(b & lt)] = (uint16_t)slot;
+    }
+  }
+}
+
 // one insert pass over the chunk's keys seg[k0, k0 + nk): id = (sector - s0) <<
 // A | (key >> B) & M, mask = the key's low 8 bits.  Each warp takes 32 x kIns
 // consecutive keys per iteration, all loads in flight before the inserts
@@ -638,7 +675,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
       for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
     __syncthreads();
     // ---- (a) distinct (sector, launch, warp) ----
-    chunk_insert_pass(tab, list, &s_n[0], seg, k0, nk, s0, kl, filter, LW, RS, lwmask);
+    ull kk[kKPT];
+    chunk_load(kk, seg, k0, nk);
+    chunk_insert_regs(tab, list, &s_n[0], kk, nk, s0, kl, filter, LW, RS, lwmask);
     __syncthreads();
     const uint32_t nent = s_n[0];
     for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
@@ -687,7 +726,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     if (!pc_hist) continue;  // (uniform)
     __syncthreads();
     // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
-    chunk_insert_pass(tab, list, &s_n[1], seg, k0, nk, s0, kl, filter, kl.P, 8, pmask);
+    chunk_insert_regs(tab, list, &s_n[1], kk, nk, s0, kl, filter, kl.P, 8, pmask);
     __syncthreads();
     const uint32_t npc = s_n[1];
     for (uint32_t base = threadIdx.x & ~31u; base < npc; base += kSegThreads) {
