@@ -52,6 +52,30 @@ __global__ void find_heads_kernel(const uint4* __restrict__ recs, ull n, ull ran
   if (lane == 0) heads[r] = found;
 }
 
+// instruction heads among sampled 32-record chunks (every stride-th chunk):
+// out[0] += records sampled, out[1] += heads among them
+__global__ void head_sample_kernel(const uint4* __restrict__ recs, ull n, ull stride, uint32_t nsample,
+                                   ull* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= nsample) return;
+  const ull i = (ull)c * stride * 32 + lane;
+  const bool in = i < n;
+  const bool st = in && ((__ldg(&recs[i].y) >> 23) & 1u);
+  const unsigned b = __ballot_sync(FULL, st), v = __ballot_sync(FULL, in);
+  if (lane == 0 && v) {
+    atomicAdd(&out[0], (ull)__popc(v));
+    atomicAdd(&out[1], (ull)__popc(b));
+  }
+}
+
+void launch_head_sample(const uint4* recs, ull n, ull* out, cudaStream_t s) {
+  const ull chunks = (n + 31) / 32;
+  const uint32_t nsample = (uint32_t)std::min<ull>(chunks, 4096);
+  const ull stride = chunks / nsample;
+  head_sample_kernel<<<(nsample * 32 + 255) / 256, 256, 0, s>>>(recs, n, stride, nsample, out);
+}
+
 void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_ranges, ull* heads, cudaStream_t s) {
   ull threads = ((ull)n_ranges + 1) * 32;
   find_heads_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(recs, n, range_len, n_ranges, heads);

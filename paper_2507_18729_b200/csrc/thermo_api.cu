@@ -106,6 +106,7 @@ struct thermo_ctx {
   float ms_phase[6] = {0, 0, 0, 0, 0, 0};  // decode, dedup, count, hist, pc, indicators
   double ms_kernel[9] = {};                // THERMO_K_* (thermo.h)
   cudaEvent_t evk[4] = {};                 // decode kernel timers
+  bool decoder_view = false;               // the last decode ran the view kernel
 
   uint32_t built_filter = THERMO_ALL_LAUNCHES;
   uint32_t built_gran = THERMO_BOTH;
@@ -253,11 +254,30 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n, bool time
   a.n = n;
   a.heads = ctx->d_heads;
   a.n_ranges = (uint32_t)n_ranges;
+  // Decoder choice by the trace's shape: the view-per-instruction kernel
+  // (decode_fast.cu) for long instructions (full warps: SGEMM, stencil), the
+  // lane-per-record kernel (decode_lane.cu) for short ones (divergent loops:
+  // SpMV), from the mean instruction length of a 4096-chunk sample (measured
+  // crossover); THERMO_DECODER=view|lane forces one
+  const char* force = getenv("THERMO_DECODER");
+  bool view;
+  if (force && std::string(force) == "view") {
+    view = true;
+  } else if (force && std::string(force) == "lane") {
+    view = false;
+  } else {
+    CK(cudaMemsetAsync(ctx->d_tmp + 200, 0, 2 * sizeof(ull), ctx->stream));
+    launch_head_sample(recs, n, ctx->d_tmp + 200, ctx->stream);
+    ull hv[2];
+    CK(cudaMemcpyAsync(hv, ctx->d_tmp + 200, sizeof hv, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    view = hv[1] == 0 || hv[0] >= 16 * hv[1];  // mean instruction length >= 16 records
+    ctx->launches += 1;
+  }
   CK(cudaEventRecord(ctx->evk[0], ctx->stream));
-  // THERMO_DECODER=view: the view-per-instruction kernel (decode_fast.cu), for comparison
-  static const bool view = getenv("THERMO_DECODER") && std::string(getenv("THERMO_DECODER")) == "view";
   if (view) launch_decode(a, ctx->num_sms, ctx->stream);
   else launch_decode_lane(a, ctx->num_sms, ctx->stream);
+  ctx->decoder_view = view;
   CK(cudaEventRecord(ctx->evk[1], ctx->stream));
   launch_decode_general(a, ctx->num_sms, ctx->stream);
   CK(cudaGetLastError());

@@ -142,6 +142,8 @@ void launch_find_heads(const uint4* recs, ull n, ull range_len, uint32_t n_range
 void launch_decode(const DecodeArgs& a, int num_sms, cudaStream_t s);
 // the lane-per-record decoder (decode_lane.cu): windows of whole instructions
 void launch_decode_lane(const DecodeArgs& a, int num_sms, cudaStream_t s);
+// records and instruction heads of a sample of 32-record chunks (out[0], out[1] +=)
+void launch_head_sample(const uint4* recs, ull n, ull* out, cudaStream_t s);
 void launch_decode_general(const DecodeArgs& a, int num_sms, cudaStream_t s);
 // warp-instruction records (decode_warp.cu); spill_ctr[0] = spilled per-lane
 // records written to spill, spill_ctr[1] += lane records seen

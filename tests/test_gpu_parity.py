@@ -120,6 +120,22 @@ def test_random_hot_cv_boundary(lo, hi, want):
     assert oracle.label_names(th.classify()[0]["labels"]) == [want]
 
 
+@pytest.mark.parametrize("decoder", ["view", "lane"])
+@pytest.mark.parametrize("make", [lambda: tg.random_trace(n=30000, seed=31, n_warps=300, n_launches=3),
+                                  lambda: tg.spmv(11, 8), lambda: tg.gemm(64, 64, 16, "v00"),
+                                  lambda: tg.stencil(96), lambda: tg.hot_spots(tg.hot_temps(2048, "bimodal"))])
+def test_both_decoders(decoder, make, monkeypatch):
+    """Both per-lane decoders (the view-per-instruction kernel and the
+    lane-per-record kernel; AUTO picks one by the mean instruction length)
+    forced on the same traces, every output against the oracle."""
+    monkeypatch.setenv("THERMO_DECODER", decoder)
+    t = make()
+    t.meta.setdefault("launches", 3)
+    calls = [t.records[a:b] for a, b in tg.split_calls(t.n, t.records, 3)]
+    orc, th = run_both(t, calls=calls)
+    compare(orc, th, t)
+
+
 def test_launch_filter_rebuild_and_host_ingest():
     t = tg.random_trace(n=20000, seed=21, n_launches=4)
     t.meta["launches"] = 4
