@@ -92,8 +92,26 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   const uint32_t o = (uint32_t)a.tile_obj[tile];
   const ull g0 = a.tile_first[tile], g1 = a.tile_end[tile];
   if (shard_owner(g0, a.nranks) != a.rank) {  // another rank's tile (sharded mode)
-    if (mode == 0 && threadIdx.x < 4) a.tile_info[(ull)tile * 4 + threadIdx.x] = 0;  // identity of the sum
+    if (mode == 0 && threadIdx.x < kTileInfo) a.tile_info[(ull)tile * kTileInfo + threadIdx.x] = 0;  // sum identity
     return;
+  }
+  if (mode == 1) {
+    // a tile whose gaps all equal the object's candidate (its vote never lost
+    // a count: cnt = touched words - 1) needs no re-scan: its verify count is
+    // its gaps, plus the gap from the previous touched word if that is equal
+    const ull* ti = a.tile_info + (ull)tile * kTileInfo;
+    const ull cand0 = a.ind[(ull)o * kIndFields + F_CAND];
+    if (a.ind[(ull)o * kIndFields + F_CANDCNT] == 0) return;
+    const ull tw = ti[4];
+    if (tw == 0) return;
+    if (ti[2] == cand0 && ti[3] == tw - 1) {
+      if (threadIdx.x == 0) {
+        const ull tp = a.tile_prev[tile];
+        const ull v = (tw - 1) + ((tp != kNone && ti[0] - tp == cand0) ? 1 : 0);
+        if (v) atomicAdd(&a.ind[(ull)o * kIndFields + F_VERIFY], v);
+      }
+      return;
+    }
   }
   const ull soff = a.obj.soff[o];
   const ull nw = a.obj_nwords[o];
@@ -225,11 +243,12 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     if (acc[5]) atomicAdd(&ind[F_LE1], acc[5]);
     if (acc[6]) atomicMax(&ind[F_MAXSEC], acc[6]);
     if (s2) atomic_add_u128(&ind[F_SUMX2_LO], &ind[F_SUMX2_HI], s2);
-    ull* ti = a.tile_info + (ull)tile * 4;
+    ull* ti = a.tile_info + (ull)tile * kTileInfo;
     ti[0] = acc[11];
     ti[1] = bl == 0 ? kNone : bl - 1;
     ti[2] = bv.c;
     ti[3] = bv.n;
+    ti[4] = acc[1];
   }
 }
 
@@ -249,7 +268,7 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
     ull first = kNone, last = kNone;
     Vote tv{0, 0};
     if (t < t1) {
-      const ull* ti = a.tile_info + (ull)t * 4;
+      const ull* ti = a.tile_info + (ull)t * kTileInfo;
       first = ti[0]; last = ti[1]; tv = Vote{ti[2], ti[3]};
     }
     ull prev = block_prev_last(last, s_w);

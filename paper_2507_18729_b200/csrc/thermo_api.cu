@@ -704,7 +704,7 @@ thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs
   CK(dalloc(&ctx->d_ind, n * kIndFields));
   const size_t nt = std::max<size_t>(1, ctx->n_tiles);
   CK(dalloc(&ctx->d_tile_obj, nt)); CK(dalloc(&ctx->d_tile_first, nt)); CK(dalloc(&ctx->d_tile_end, nt));
-  CK(dalloc(&ctx->d_tile_info, nt * 4));
+  CK(dalloc(&ctx->d_tile_info, nt * kTileInfo));
   CK(dalloc(&ctx->d_tile_prev, nt + (n + 2) / 2 + 1));
   if (ctx->n_tiles) {
     CK(cudaMemcpy(ctx->d_tile_obj, tile_obj.data(), ctx->n_tiles * 8, cudaMemcpyHostToDevice));
@@ -1366,7 +1366,7 @@ thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, ther
     launch_indicator_pack(ctx->d_ind, (uint32_t)n, sums, maxs, nullptr, 0, s);
     DCK(c->allreduce(sums, n * kIndSumFields, false, s));
     DCK(c->allreduce(maxs, n, true, s));
-    if (ctx->n_tiles) DCK(c->allreduce(ctx->d_tile_info, (size_t)ctx->n_tiles * 4, false, s));
+    if (ctx->n_tiles) DCK(c->allreduce(ctx->d_tile_info, (size_t)ctx->n_tiles * kTileInfo, false, s));
     launch_indicator_pack(ctx->d_ind, (uint32_t)n, sums, maxs, nullptr, 1, s);
     launch_indicator_stitch(a, s);
     launch_indicator_tiles(a, 1, s);
