@@ -20,7 +20,7 @@
 //  * pre-dedup (P:325's OR is idempotent): a window of one instruction merges
 //    adjacent equal sectors (broadcast: the whole window is one key) as
 //    decode_fast.cu does; a window of several instructions merges equal keys
-//    anywhere (match_any); each lane then keeps its two most recent keys with
+//    anywhere (match_any); each lane then keeps its four most recent keys with
 //    their OR-ed masks in registers and emits a key when it is replaced;
 //  * instruction statistics (G24): a one-instruction window
 //    takes decode_fast.cu's uniform tests (broadcast, stride, non-decreasing);
@@ -77,9 +77,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
   uint32_t cur_launch = 0xFFFFFFFFu;
   InstrRegs ir;  // (launch, object) instruction counters for ids < 32
-  // this lane's two most recent keys (full prefix) with their OR-ed masks
-  ull c0 = ~0ull, c1 = ~0ull;
-  uint32_t m0 = 0, m1 = 0;
+  // this lane's four most recent keys (full prefix) with their OR-ed masks
+  ull c0 = ~0ull, c1 = ~0ull, c2 = ~0ull, c3 = ~0ull;
+  uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
 
   for (;;) {
     uint32_t r = 0;
@@ -249,13 +249,19 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
         } else {
           group_merge(pre, mk, has, scr, lane);
         }
-        // ---- this lane's two most recent keys ----
-        const bool hit0 = c0 == pre, hit1 = c1 == pre;
-        STAGE_PUSH(st, has & !hit0 & !hit1 & (m1 != 0), (c1 << 8) | m1, gkeys, gnk);
-        const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : 0u);
-        const bool shift = has & !hit0;
-        c1 = shift ? c0 : c1;
-        m1 = shift ? m0 : m1;
+        // ---- this lane's four most recent keys ----
+        // (move-to-front over four entries: SpMV's col / val / x loads of one
+        // lane cycle through three keys, which a two-entry LRU thrashes)
+        const bool hit0 = c0 == pre, hit1 = c1 == pre, hit2 = c2 == pre, hit3 = c3 == pre;
+        const bool s1 = has & !hit0, s2 = s1 & !hit1, s3 = s2 & !hit2;
+        STAGE_PUSH(st, s3 & !hit3 & (m3 != 0), (c3 << 8) | m3, gkeys, gnk);
+        const uint32_t mprev = hit0 ? m0 : (hit1 ? m1 : (hit2 ? m2 : (hit3 ? m3 : 0u)));
+        c3 = s3 ? c2 : c3;
+        m3 = s3 ? m2 : m3;
+        c2 = s2 ? c1 : c2;
+        m2 = s2 ? m1 : m2;
+        c1 = s1 ? c0 : c1;
+        m1 = s1 ? m0 : m1;
         c0 = has ? pre : c0;
         m0 = has ? (mprev | mk) : m0;
       }
@@ -319,6 +325,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
   }
   STAGE_PUSH(st, m0 != 0, (c0 << 8) | m0, gkeys, gnk);
   STAGE_PUSH(st, m1 != 0, (c1 << 8) | m1, gkeys, gnk);
+  STAGE_PUSH(st, m2 != 0, (c2 << 8) | m2, gkeys, gnk);
+  STAGE_PUSH(st, m3 != 0, (c3 << 8) | m3, gkeys, gnk);
   st.flush(gkeys, gnk, lane);
   dq.flush(a.deferred, &a.ctr->n_deferred, lane);
   if (cur_launch != 0xFFFFFFFFu) {
