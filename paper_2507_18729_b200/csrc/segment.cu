@@ -809,6 +809,24 @@ __device__ __forceinline__ bool big_or(ull* tab, uint32_t tb, ull id, uint32_t m
   }
   return false;
 }
+// f(key) over big[b0, b0 + K), kBigUnroll loads in flight per thread (the
+// keys are re-read from L2 by each pass of the sector: latency-bound with one
+// load at a time)
+constexpr int kBigUnroll = 8;
+template <typename F>
+__device__ __forceinline__ void big_for_keys(const ull* __restrict__ big, ull b0, uint32_t K, F f) {
+  for (uint32_t base = 0; base < K; base += kSegThreads * kBigUnroll) {
+    ull kk[kBigUnroll];
+#pragma unroll
+    for (int u = 0; u < kBigUnroll; ++u) {
+      const uint32_t j = base + u * kSegThreads + threadIdx.x;
+      kk[u] = j < K ? big[b0 + j] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kBigUnroll; ++u)
+      if (base + u * kSegThreads + threadIdx.x < K) f(kk[u]);
+  }
+}
 __device__ __forceinline__ uint32_t big_table_bits(uint32_t keys_per_pass) {
   uint32_t tb = 8;
   while ((1u << tb) * 3u < keys_per_pass * 4u && (1u << tb) < (uint32_t)kBigSlots) ++tb;
@@ -891,13 +909,12 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
   const int T = 1 << tb;
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
-    const ull k = big[b0 + j];
+  big_for_keys(big, b0, K, [&](ull k) {
     const ull id = (k >> RS) & lwmask;
-    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) continue;
-    if (big_pass_of(id, P) != p) continue;
+    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) return;
+    if (big_pass_of(id, P) != p) return;
     if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-  }
+  });
   __syncthreads();
   uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs = 0;
   for (int j = threadIdx.x; j < T; j += kSegThreads) {
@@ -931,12 +948,11 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
   __syncthreads();
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
-    const ull k = big[b0 + j];
+  big_for_keys(big, b0, K, [&](ull k) {
     const ull id = (k >> 8) & pmask;
-    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) continue;
+    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) return;
     if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-  }
+  });
   __syncthreads();
   uint32_t npc = 0;
   for (int j = threadIdx.x; j < T; j += kSegThreads) {
@@ -976,13 +992,12 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __re
   const int T = 1 << tb;
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < K; j += kSegThreads) {
-    const ull k = big[b0 + j];
+  big_for_keys(big, b0, K, [&](ull k) {
     const ull id = (k >> 8) & pmask;
-    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) continue;
-    if (big_pass_of(id, P) != p) continue;
+    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) return;
+    if (big_pass_of(id, P) != p) return;
     if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-  }
+  });
   __syncthreads();
   const uint32_t scnt = sc[g];
   uint32_t npc = 0;

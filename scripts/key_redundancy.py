@@ -59,3 +59,13 @@ for k, nm in enumerate(names):
                            "distinct_sector_launch_warp": d_pair})
     del sel
 print(json.dumps(res, indent=1))
+
+# SEGMENT's big sectors (>= 2048 keys): keys, passes of 6144, re-read volume
+cnt = torch.bincount(g, minlength=soff[-1])
+big = cnt[cnt >= 2048].to(torch.int64)
+passes = (big + 6143) // 6144
+rest = cnt[(cnt > 0) & (cnt < 2048)].to(torch.int64)
+print(json.dumps({"big_sectors": int(big.numel()), "big_keys": int(big.sum()), "big_key_reads": int((big * passes).sum()),
+                  "big_passes": int(passes.sum()), "max_keys": int(big.max()) if big.numel() else 0,
+                  "normal_sectors": int(rest.numel()), "normal_keys": int(rest.sum()),
+                  "normal_hist_log2": torch.bincount(torch.log2(rest.float()).long()).tolist()}))
