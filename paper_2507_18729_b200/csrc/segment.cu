@@ -505,6 +505,7 @@ __global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, u
 // per-block (pc, level) bin table in shared memory: open addressing on the
 // bin id; a full table falls back to the global atomic
 constexpr int kPcBins = 512;
+constexpr uint32_t kFewPcs = 8;  // direct bins + byte masks up to this many pc ids (8 x 2 x 33 <= 2 kPcBins)
 __device__ __forceinline__ void bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, uint32_t bin, uint32_t v) {
   uint32_t h = (bin * 0x9E3779B1u) >> (32 - 9);
   for (int probe = 0; probe < 16; ++probe) {
@@ -640,7 +641,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
                                                                const uint32_t* __restrict__ site_of,
                                                                ull* __restrict__ pc_hist, DevCounters* ctr,
                                                                const ull* __restrict__ cs0, ull nchunks,
-                                                               ull* __restrict__ chunk_ctr) {
+                                                               ull* __restrict__ chunk_ctr, uint32_t few_pcs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ull* tab = reinterpret_cast<ull*>(smem_raw);                    // [kHSlots]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + kHSlots);     // [kHWin][5]: words (2b, 2b+1) as u16 pairs, sector
@@ -654,7 +655,15 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   const ull lwmask = (1ull << LW) - 1;
   const ull pmask = (1ull << kl.P) - 1;
   for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
-  for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
+  // few_pcs (at most kFewPcs pc ids in the job): the bin region is a direct
+  // [pc][word | sector][level] table, and a local chunk collects its (sector,
+  // pc) word masks as bytes (one shared OR per key) instead of the second set
+  uint32_t* const dir = tbin;  // [kFewPcs * 2 * kLevels] <= 2 kPcBins
+  if (few_pcs) {
+    for (int i = threadIdx.x; i < 2 * kPcBins; i += kSegThreads) dir[i] = 0;
+  } else {
+    for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
+  }
   ull distinct = 0, distinct_pc = 0;  // thread 0's running totals
   for (;;) {
     __syncthreads();  // the previous chunk is done with s_c, s_n and its table slots
@@ -725,6 +734,51 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
     if (!pc_hist) continue;  // (uniform)
     __syncthreads();
+    if (few_pcs && local) {
+      // ---- (b') the chunk's (sector, pc) word masks as bytes: pcm[2 j + pc / 4]
+      // byte pc % 4 = OR of the masks of sector s0 + j's keys of that pc, in the
+      // (now clear) first win u64 slots of the table ----
+      uint32_t* const pcm = reinterpret_cast<uint32_t*>(tab);
+      for (uint32_t j = threadIdx.x; j < 2 * (uint32_t)win; j += kSegThreads) pcm[j] = 0;
+      __syncthreads();
+      const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;
+#pragma unroll
+      for (int j = 0; j < kKPT; ++j) {
+        if ((uint32_t)j >= jmax) break;
+        const ull k = kk[j];
+        bool ok = j * kSegThreads + threadIdx.x < nk;
+        if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
+        if (ok) {
+          const uint32_t gl = (uint32_t)(key_g(k, kl) - s0), pcid = (uint32_t)(k >> 8) & 7u;
+          atomicOr(&pcm[2 * gl + (pcid >> 2)], ((uint32_t)k & 0xFFu) << (8 * (pcid & 3u)));
+        }
+      }
+      __syncthreads();
+      uint32_t npcs = 0;
+      for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
+        const uint32_t p0 = pcm[2 * j], p1 = pcm[2 * j + 1];
+        if ((p0 | p1) == 0) continue;
+        const uint32_t* cg = cnt + j * 5;
+        const uint32_t ls = level_of_g(cg[4]);
+        uint32_t lw[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) lw[b] = level_of_g((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t m = ((q < 4 ? p0 : p1) >> (8 * (q & 3))) & 0xFFu;
+          if (!m) continue;
+          ++npcs;
+          atomicAdd(&dir[(q * 2 + 1) * kLevels + ls], 1u);
+#pragma unroll
+          for (int b = 0; b < 8; ++b)
+            if ((m >> b) & 1u) atomicAdd(&dir[(q * 2) * kLevels + lw[b]], 1u);
+        }
+      }
+      distinct_pc += npcs;  // (per thread: summed below)
+      __syncthreads();
+      for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) tab[j] = kHEmpty;
+      continue;
+    }
     // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
     chunk_insert_regs(tab, list, &s_n[1], kk, nk, s0, kl, filter, kl.P, 8, pmask);
     __syncthreads();
@@ -742,7 +796,10 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
         const uint32_t scv = head ? (local ? cg[4] : __ldcg(&sc[g])) : 0u;
         const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(scv) : 0xFFFFFFFFu;
         const unsigned mm = __match_any_sync(GFULL, bin);
-        if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+        if (head && (__ffs(mm) - 1) == lane) {
+          if (few_pcs) atomicAdd(&dir[bin], (uint32_t)__popc(mm));
+          else bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+        }
       }
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
@@ -751,21 +808,28 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
         if (hb) wv = local ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : __ldcg(&wc[8 * g + b]);
         const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wv) : 0xFFFFFFFFu;
         const unsigned mm = __match_any_sync(GFULL, bin);
-        if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+        if (hb && (__ffs(mm) - 1) == lane) {
+          if (few_pcs) atomicAdd(&dir[bin], (uint32_t)__popc(mm));
+          else bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
+        }
       }
     }
-    distinct_pc += npc;
+    if (threadIdx.x == 0) distinct_pc += npc;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < npc; i += kSegThreads) tab[list[i]] = kHEmpty;
   }
-  if (threadIdx.x == 0) {
-    if (distinct) atomicAdd(&ctr->distinct_pairs, distinct);
-    if (distinct_pc) atomicAdd(&ctr->distinct_pc, distinct_pc);
-  }
+  if (threadIdx.x == 0 && distinct) atomicAdd(&ctr->distinct_pairs, distinct);
+  for (int d = 16; d; d >>= 1) distinct_pc += __shfl_xor_sync(GFULL, distinct_pc, d);
+  if (lane == 0 && distinct_pc) atomicAdd(&ctr->distinct_pc, distinct_pc);
   if (pc_hist) {
     __syncthreads();
-    for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
-      if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
+    if (few_pcs) {
+      for (int i = threadIdx.x; i < 2 * kPcBins; i += kSegThreads)
+        if (dir[i]) atomicAdd(&pc_hist[i], (ull)dir[i]);
+    } else {
+      for (int i = threadIdx.x; i < kPcBins; i += kSegThreads)
+        if (tbin[i] != 0xFFFFFFFFu && tcnt[i]) atomicAdd(&pc_hist[tbin[i]], (ull)tcnt[i]);
+    }
   }
   (void)site_of;
   (void)nsec;
@@ -1104,7 +1168,7 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
 // -> dense counts (+ per-pc histograms)
 cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout kl, ull nsec, uint32_t filter,
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
-                          DevCounters* ctr, int num_sms, cudaStream_t s) {
+                          ull n_pc, DevCounters* ctr, int num_sms, cudaStream_t s) {
   cudaError_t e;
   if (n && ws.tmp_cap < n) {
     cudaFree(ws.tmp);
@@ -1142,7 +1206,8 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_chunk_kernel, kSegThreads, smem);
     const ull grid = std::min<ull>(chunks, (ull)num_sms * (per_sm < 1 ? 1 : per_sm));
     seg_chunk_kernel<<<(unsigned)grid, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
-                                                               pc_hist, ctr, ws.cs0, chunks, ws.chunk_ctr);
+                                                               pc_hist, ctr, ws.cs0, chunks, ws.chunk_ctr,
+                                                               pc_hist && n_pc <= kFewPcs ? 1u : 0u);
     ws.launches += 1;
     ws.ran[2] = true;
   }

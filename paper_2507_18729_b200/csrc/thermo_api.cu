@@ -1038,7 +1038,7 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
     }
     CK(cudaEventRecord(ctx->evp[1], s));
     e = segment_count(ctx->d_keys, ctx->n_keys, ctx->sw.alt, ctx->d_pckeys, kl, ctx->S_own, launch_filter, ctx->seg,
-                      ctx->d_wc, ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, ctx->d_ctr,
+                      ctx->d_wc, ctx->d_sc, site_tab, ctx->cfg.track_pc ? ctx->d_pchist : nullptr, n_pc, ctx->d_ctr,
                       ctx->num_sms, s);
     if (e) return fail(ctx, THERMO_ECUDA, std::string("segment count: ") + cudaGetErrorString(e));
     ctx->launches += ctx->seg.launches;

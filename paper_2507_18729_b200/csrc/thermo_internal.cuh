@@ -206,7 +206,7 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
 // big: receives the keys of the big sectors (capacity n_big from prepare)
 cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout kl, ull nsec, uint32_t filter,
                           SegWorkspace& ws, uint32_t* wc, uint32_t* sc, const uint32_t* site_of, ull* pc_hist,
-                          DevCounters* ctr, int num_sms, cudaStream_t s);
+                          ull n_pc, DevCounters* ctr, int num_sms, cudaStream_t s);
 ull segment_chunk_cap();
 
 // hash-set dedup: insert keys (prefix<<8 | mask) into table; EMPTY = ~0.
