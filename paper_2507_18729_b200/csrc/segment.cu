@@ -386,10 +386,18 @@ __global__ void seg_tiles_kernel(const ull* __restrict__ tot, uint32_t ncoarse, 
   if (threadIdx.x == 0) tpre[ncoarse] = carry;
 }
 
+// tbk[t] = the coarse bucket of pass-2 tile t (one thread per bucket)
+__global__ void seg_tilemap_kernel(const ull* __restrict__ tpre, uint32_t ncoarse, uint32_t* __restrict__ tbk) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= ncoarse) return;
+  for (ull t = tpre[b]; t < tpre[b + 1]; ++t) tbk[t] = b;
+}
+
 // pass 2: tile t of coarse bucket b -> its chunks (out) and big sectors (big)
 __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict__ tmp, KeyLayout kl,
                                                        uint32_t ncoarse, const ull* __restrict__ cstart,
                                                        const ull* __restrict__ cinfo, const ull* __restrict__ tpre,
+                                                       const uint32_t* __restrict__ tbk,
                                                        const uint32_t* __restrict__ dst, ull* __restrict__ cur,
                                                        ull* __restrict__ bcur, ull* __restrict__ out,
                                                        ull* __restrict__ big) {
@@ -400,12 +408,7 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   const ull t = blockIdx.x;
   if (t >= tpre[ncoarse]) return;
-  uint32_t lo = 0, hi = ncoarse;  // bucket b: tpre[b] <= t < tpre[b + 1]
-  while (hi - lo > 1) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (tpre[mid] <= t) lo = mid; else hi = mid;
-  }
-  const uint32_t b = lo;
+  const uint32_t b = tbk[t];  // bucket b: tpre[b] <= t < tpre[b + 1]
   const ull k0 = cstart[b] + (t - tpre[b]) * kPTile;
   const ull k1 = k0 + kPTile < cstart[b + 1] ? k0 + kPTile : cstart[b + 1];
   const ull nl0 = cinfo[2 * b], nl1 = cinfo[2 * b + 2];
@@ -449,13 +452,15 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   }
   for (uint32_t i = threadIdx.x; i < nbins; i += kPT) sm.cnt[i] = 0;
   __syncthreads();
+  unsigned pe[kPPer];
+#pragma unroll
+  for (int u = 0; u < kPPer; ++u) pe[u] = __match_any_sync(GFULL, d[u]);
 #pragma unroll
   for (int u = 0; u < kPPer; ++u) {
-    const unsigned peers = __match_any_sync(GFULL, d[u]);
-    const int ldr = __ffs(peers) - 1;
+    const int ldr = __ffs(pe[u]) - 1;
     uint32_t r0 = 0;
-    if (d[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[d[u]], (uint32_t)__popc(peers));
-    r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(peers & lt);
+    if (d[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[d[u]], (uint32_t)__popc(pe[u]));
+    r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(pe[u] & lt);
   }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nbins; i += kPT)
@@ -1189,10 +1194,18 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     seg_coarse_kernel<<<g1, kPT, csm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
     if (ws.ev[1]) cudaEventRecord(ws.ev[1], s);
     const ull g2 = (n + kPTile - 1) / kPTile + ws.ncoarse;  // >= the tiles of all buckets
-    seg_fine_kernel<<<(unsigned)g2, kPT, psm, s>>>(ws.tmp, kl, ws.ncoarse, ws.cstart, ws.cinfo, ws.tpre, ws.dst,
+    if (ws.tbk_cap < g2) {
+      cudaFree(ws.tbk);
+      ws.tbk = nullptr;
+      ws.tbk_cap = 0;
+      if ((e = cudaMalloc(&ws.tbk, g2 * sizeof(uint32_t)))) return e;
+      ws.tbk_cap = g2;
+    }
+    seg_tilemap_kernel<<<(ws.ncoarse + 255) / 256, 256, 0, s>>>(ws.tpre, ws.ncoarse, ws.tbk);
+    seg_fine_kernel<<<(unsigned)g2, kPT, psm, s>>>(ws.tmp, kl, ws.ncoarse, ws.cstart, ws.cinfo, ws.tpre, ws.tbk, ws.dst,
                                                    ws.cur, ws.bcur, out, big);
     if (ws.ev[2]) cudaEventRecord(ws.ev[2], s);
-    ws.launches += 3;
+    ws.launches += 4;
     ws.ran[0] = ws.ran[1] = true;
   }
   const size_t smem = segment_chunk_smem();

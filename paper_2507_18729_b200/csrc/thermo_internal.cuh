@@ -183,6 +183,8 @@ struct SegWorkspace {
   ull* cinfo = nullptr;      // [ncoarse + 1][2] normal keys / big sectors before the bucket
   ull* ccur = nullptr;       // [ncoarse] pass-1 cursors
   ull* tpre = nullptr;       // [ncoarse + 1] first pass-2 tile of each bucket
+  uint32_t* tbk = nullptr;   // [pass-2 tiles] bucket of each tile
+  ull tbk_cap = 0;
   ull* tmp = nullptr;        // pass-1 output
   size_t tmp_cap = 0;
   ull* bg = nullptr;         // [n big sectors] sector id of big sector i
