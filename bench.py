@@ -318,7 +318,8 @@ def touched_sectors(t):
 
 
 # algorithmic bytes per launch of each kernel:
-#   decode_kernel       16 B per record (the trace, read once)
+#   decode_kernel       16 B per record (the trace, read once); the same for
+#                       decode_lane_kernel (the lane-per-record decoder)
 #   seg_coarse_kernel   16 B per key (read + write)          [partition pass 1]
 #   seg_fine_kernel     16 B per key (read + write)          [partition pass 2]
 #   seg_chunk_kernel     8 B per key (read once) + 36 B per touched sector (its row written)
@@ -328,7 +329,7 @@ def touched_sectors(t):
 # sizes the library does not report; they are listed with their times only)
 def kernel_bytes(k, n, st, S_tot, touched):
     keys = st["keys_emitted"]
-    return {"decode_kernel": 16 * n, "seg_coarse_kernel": 16 * keys, "seg_fine_kernel": 16 * keys,
+    return {"decode_kernel": 16 * n, "decode_lane_kernel": 16 * n, "seg_coarse_kernel": 16 * keys, "seg_fine_kernel": 16 * keys,
             "seg_chunk_kernel": 8 * keys + 36 * touched, "object_hist_kernel": 36 * S_tot,
             "indicator_kernels": 72 * S_tot}.get(k)
 
@@ -428,11 +429,15 @@ def run_ours(args, workload, ws, rank, local, steps, warmup, headline):
     k_mean = {k: statistics.mean(v) for k, v in kern.items()}
     traffic_db = load_traffic().get(workload if args.format == "lane" else workload + "-warp", {})
     kernels = {}
+    # the decode timer covers whichever decoder the ingest chose (stats.decoder_used)
+    dec_name = {2: "decode_lane_kernel", 3: "decode_warp_kernel"}.get(st.get("decoder_used", 1), "decode_kernel")
     for k, v in k_mean.items():
         if v <= 0:
             continue
+        if k == "decode_kernel":
+            k = dec_name
         b = kernel_bytes(k, n, st, S_tot, touched)
-        if k == "decode_kernel" and args.format == "warp":
+        if k in ("decode_kernel", "decode_warp_kernel") and args.format == "warp":
             b = in_bytes
         e = {"ms_per_launch": v}
         if b is not None:

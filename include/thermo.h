@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define THERMO_ABI_VERSION 5u
+#define THERMO_ABI_VERSION 6u
 #define THERMO_ALL_LAUNCHES 0xFFFFFFFFu
 #define THERMO_LEVELS 33        /* heat levels 0..32: level(c) = bit_width(c) (G10) */
 #define THERMO_MAX_OBJECTS 1024
@@ -216,7 +216,11 @@ typedef struct {
   uint64_t distinct_pc_pairs;  /* distinct (launch, pc, sector)                */
   uint64_t n_pcs;              /* distinct (launch, pc) pairs seen             */
   uint32_t dedup_used;         /* THERMO_DEDUP_SORT, _HASH, _SEGMENT or _DENSE  */
-  uint32_t reserved0;
+  uint32_t decoder_used;       /* last ingest: 1 per-instruction view kernel
+                                  (+ general kernel), 2 lane-per-record kernel
+                                  (chosen by the trace's mean instruction length,
+                                  or THERMO_DECODER=view|lane), 3 warp-record
+                                  kernel (thermo_ingest_warp_trace); 0 none   */
   double ms_ingest, ms_build, ms_classify;  /* device time of the last calls   */
   /* device time (CUDA events on the context stream) of the phases of the last
    * ingest / build / classify: decode kernel (a2+a3), main-key dedup (a4),

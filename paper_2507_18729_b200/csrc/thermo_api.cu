@@ -111,6 +111,7 @@ struct thermo_ctx {
   uint32_t built_filter = THERMO_ALL_LAUNCHES;
   uint32_t built_gran = THERMO_BOTH;
   uint32_t dedup_used = THERMO_DEDUP_SORT;
+  uint32_t decoder_used = 0;  // thermo_stats.decoder_used
   ull records = 0;
   float ms_ingest = 0, ms_build = 0, ms_classify = 0;
   bool hist_valid = false;
@@ -277,6 +278,7 @@ thermo_status decode_device(thermo_ctx* ctx, const uint4* recs, ull n, bool time
   CK(cudaEventRecord(ctx->evk[0], ctx->stream));
   if (view) launch_decode(a, ctx->num_sms, ctx->stream);
   else launch_decode_lane(a, ctx->num_sms, ctx->stream);
+  ctx->decoder_used = view ? 1u : 2u;
   ctx->decoder_view = view;
   CK(cudaEventRecord(ctx->evk[1], ctx->stream));
   launch_decode_general(a, ctx->num_sms, ctx->stream);
@@ -930,6 +932,7 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
     CK(cudaMemsetAsync(ctx->d_wctr, 0, 2 * sizeof(ull), s));
     DecodeArgs a = decode_args(ctx);
     launch_decode_warp(a, drec, cnt, ctx->d_spill, ctx->d_wctr, ctx->num_sms, s);
+    ctx->decoder_used = 3u;
     ctx->launches += 1;
     CK(cudaGetLastError());
     if (!on_device) CK(cudaEventRecord(ctx->ev_used[b], s));
@@ -1433,6 +1436,7 @@ thermo_status thermo_get_stats(thermo_ctx* ctx, thermo_stats* out) {
   out->distinct_pc_pairs = hc.distinct_pc;
   out->n_pcs = hc.pc_count;
   out->dedup_used = ctx->dedup_used;
+  out->decoder_used = ctx->decoder_used;
   out->ms_ingest = ctx->ms_ingest;
   out->ms_build = ctx->ms_build;
   out->ms_classify = ctx->ms_classify;

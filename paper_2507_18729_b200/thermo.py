@@ -66,8 +66,8 @@ class thermo_pc_hist(ctypes.Structure):
 class thermo_stats(ctypes.Structure):
     _fields_ = [("records", u64), ("invalid", u64), ("out_of_range", u64), ("unmapped_words", u64),
                 ("mapped_word_accesses", u64), ("keys_emitted", u64), ("pc_keys_emitted", u64),
-                ("distinct_pairs", u64), ("distinct_pc_pairs", u64), ("n_pcs", u64), ("dedup_used", u32),
-                ("reserved0", u32), ("ms_ingest", ctypes.c_double), ("ms_build", ctypes.c_double),
+                ("distinct_pairs", u64), ("distinct_pc_pairs", u64), ("n_pcs", u64), ("dedup_used", u32), ("decoder_used", u32),
+                ("ms_ingest", ctypes.c_double), ("ms_build", ctypes.c_double),
                 ("ms_classify", ctypes.c_double), ("ms_decode", ctypes.c_double), ("ms_dedup", ctypes.c_double),
                 ("ms_count", ctypes.c_double), ("ms_hist", ctypes.c_double), ("ms_pc", ctypes.c_double),
                 ("ms_indicators", ctypes.c_double), ("kernel_launches", u64),

@@ -10,8 +10,8 @@ import csv
 import json
 import sys
 
-NAMES = ("decode_kernel", "decode_general_kernel", "seg_coarse_kernel", "seg_fine_kernel", "seg_chunk_kernel",
-         "seg_big_kernel", "object_hist_kernel")
+NAMES = ("decode_kernel", "decode_lane_kernel", "decode_warp_kernel", "decode_general_kernel", "seg_coarse_kernel",
+         "seg_fine_kernel", "seg_chunk_kernel", "seg_big_kernel", "seg_big_pc_kernel", "object_hist_kernel")
 out = {}
 for arg in sys.argv[1:]:
     w, path = arg.split("=", 1)

@@ -50,7 +50,7 @@ def test_defaults(lib):
     p = thermo.default_params()
     import oracle
     assert p == oracle.DEFAULT_PARAMS   # same S:347 defaults on both sides
-    assert lib.thermo_abi_version() == 5
+    assert lib.thermo_abi_version() == 6
 
 
 def test_struct_sizes():
