@@ -1,7 +1,8 @@
 // decode_lane.cu -- the lane-per-record decode kernel (rows a2 + a3, SURVEY
 // §8a), the default decoder.  A window is up to 32 consecutive records holding
-// whole instructions (G24: it ends at the last instruction head within 32
-// records, or after 32 records of one instruction); lane l reduces record l of
+// whole instructions (G24: all 32 when record 32 starts an instruction, else
+// it ends at the last instruction head within 32 records, or after 32 records
+// of one instruction); lane l reduces record l of
 // the window.  Unlike the view-per-instruction kernel (decode_fast.cu), a
 // window of many short instructions -- divergent loops, 62 % of SpMV's
 // instructions have one active lane -- is reduced in place from the record
@@ -99,10 +100,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
       const uint32_t rem = rlen - off;
       // records at or past the range end were zero-filled by cp.async
       const uint4 cur = ring[(off + lane) & (kRingChunks * 32 - 1)];
+      // record off + 32 (in the window's second chunk, landed): when it starts
+      // an instruction, the 32 records hold whole instructions
+      const uint32_t y32 = ring[(off + 32) & (kRingChunks * 32 - 1)].y;
       // ---- window: the whole instructions within the next 32 records ----
       const unsigned hb_all = __ballot_sync(FULL, (cur.y >> 23) & 1u) | 1u;  // lane 0 starts one
       uint32_t span;
       if (rem <= 32) span = rem;
+      else if ((y32 >> 23) & 1u) span = 32u;
       else span = (hb_all & ~1u) ? 31u - __clz(hb_all & ~1u) : 32u;
       const unsigned actm = span >= 32 ? FULL : ((1u << span) - 1u);
       const bool act = lane < (int)span;

@@ -316,14 +316,11 @@ __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restric
       k[u] = sm.buf[cur][u * kPT + threadIdx.x];
       b[u] = i < n ? (uint32_t)cb[key_g(k[u], kl) / kGroup] : 0xFFFFFFFFu;
     }
+    // rank within the bucket: one shared atomic per key (the order within a
+    // bucket is free; with ~1024 buckets a warp's keys rarely share one, so a
+    // match_any aggregation costs more than it saves)
 #pragma unroll
-    for (int u = 0; u < kPPer; ++u) {
-      const unsigned peers = __match_any_sync(GFULL, b[u]);
-      const int ldr = __ffs(peers) - 1;
-      uint32_t r0 = 0;
-      if (b[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[b[u]], (uint32_t)__popc(peers));
-      r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(peers & lt);
-    }
+    for (int u = 0; u < kPPer; ++u) r[u] = b[u] != 0xFFFFFFFFu ? atomicAdd(&sm.cnt[b[u]], 1u) : 0u;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < ncoarse; i += kPT)
       if (sm.cnt[i]) sm.base[i] = atomicAdd(&ccur[i], (ull)sm.cnt[i]);
