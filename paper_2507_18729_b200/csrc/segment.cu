@@ -98,41 +98,50 @@ __global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __r
   }
 }
 
-// one block: exclusive scan of the block sums (three columns); totals -> tot[0..3)
-__global__ void seg_scan_blocks(ull* bsum3, ull nb, ull* tot) {
-  __shared__ ull carry[3];
-  __shared__ ull ws[3][kSegWarps];
-  if (threadIdx.x < 3) carry[threadIdx.x] = 0;
-  __syncthreads();
+// one block: exclusive scan of the block sums (three columns); totals -> tot[0..3);
+// the chunk table's end (chunk ceil(NL / kSegCap): no sector, all NL keys
+// before it; seg_scan_apply overwrites it when a sector starts there)
+constexpr int kScanBT = 1024;  // seg_scan_blocks threads: each scans a contiguous run of block sums
+__global__ void __launch_bounds__(kScanBT) seg_scan_blocks(ull* bsum3, ull nb, ull* tot, ull nsec, ull* cs0,
+                                                           ull* cko) {
+  __shared__ ull ws[3][kScanBT / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (ull b0 = 0; b0 < nb; b0 += kSegThreads) {
-    const ull i = b0 + threadIdx.x;
-    const Sum3 v = i < nb ? Sum3{bsum3[3 * i], bsum3[3 * i + 1], bsum3[3 * i + 2]} : Sum3{0, 0, 0};
-    const Sum3 incl = warp_incl_scan3(v, lane);
-    if (lane == 31) { ws[0][w] = incl.nl; ws[1][w] = incl.bs; ws[2][w] = incl.bk; }
-    __syncthreads();
-    Sum3 pre{carry[0], carry[1], carry[2]};
-    for (int k = 0; k < w; ++k) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
-    if (i < nb) {
-      bsum3[3 * i] = pre.nl + incl.nl - v.nl;
-      bsum3[3 * i + 1] = pre.bs + incl.bs - v.bs;
-      bsum3[3 * i + 2] = pre.bk + incl.bk - v.bk;
-    }
-    __syncthreads();
-    if (threadIdx.x == kSegThreads - 1) {
-      carry[0] = pre.nl + incl.nl; carry[1] = pre.bs + incl.bs; carry[2] = pre.bk + incl.bk;
-    }
-    __syncthreads();
+  const ull per = (nb + kScanBT - 1) / kScanBT;
+  const ull i0 = (ull)threadIdx.x * per, i1 = i0 + per < nb ? i0 + per : nb;
+  Sum3 t{0, 0, 0};
+  for (ull i = i0; i < i1; ++i) { t.nl += bsum3[3 * i]; t.bs += bsum3[3 * i + 1]; t.bk += bsum3[3 * i + 2]; }
+  const Sum3 incl = warp_incl_scan3(t, lane);
+  if (lane == 31) { ws[0][w] = incl.nl; ws[1][w] = incl.bs; ws[2][w] = incl.bk; }
+  __syncthreads();
+  Sum3 pre{0, 0, 0}, all{0, 0, 0};
+  for (int k = 0; k < kScanBT / 32; ++k) {
+    if (k < w) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
+    all.nl += ws[0][k]; all.bs += ws[1][k]; all.bk += ws[2][k];
   }
-  if (threadIdx.x < 3) tot[threadIdx.x] = carry[threadIdx.x];
+  pre.nl += incl.nl - t.nl; pre.bs += incl.bs - t.bs; pre.bk += incl.bk - t.bk;
+  for (ull i = i0; i < i1; ++i) {
+    const Sum3 v{bsum3[3 * i], bsum3[3 * i + 1], bsum3[3 * i + 2]};
+    bsum3[3 * i] = pre.nl; bsum3[3 * i + 1] = pre.bs; bsum3[3 * i + 2] = pre.bk;
+    pre.nl += v.nl; pre.bs += v.bs; pre.bk += v.bk;
+  }
+  if (threadIdx.x == 0) {
+    tot[0] = all.nl; tot[1] = all.bs; tot[2] = all.bk;
+    const ull nch = (all.nl + kSegCap - 1) / kSegCap;
+    cs0[nch] = nsec;
+    cko[nch] = all.nl;
+  }
 }
 
-// off[g] (normal-key prefix), dst[g] = chunk of g's normal keys, or 0x80000000
-// | big index for a big sector (then bg[i] = g, boff[i] = big-key prefix);
+// With off[g] = the normal-key prefix at sector g (the sector's segment in the
+// chunked layout, never stored): dst[g] = chunk off[g] / kSegCap of g's normal
+// keys, or 0x80000000 | big index for a big sector (then bg[i] = g, boff[i] =
+// big-key prefix); chunk c starts at the first sector with off >= c kSegCap:
+// cs0[c] = that sector, cko[c] = its off (a normal segment is shorter than
+// kSegCap, so at most one chunk starts at each sector);
 // gpre[q] = (NL, BS, BK) at the first sector of group q (kGroup sectors)
 __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum3,
-                               ull* __restrict__ off, uint32_t* __restrict__ dst, ull* __restrict__ bg,
-                               ull* __restrict__ boff, ull* __restrict__ gpre) {
+                               ull* __restrict__ cs0, ull* __restrict__ cko, uint32_t* __restrict__ dst,
+                               ull* __restrict__ bg, ull* __restrict__ boff, ull* __restrict__ gpre) {
   __shared__ ull ws[3][kSegWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
@@ -151,11 +160,16 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
   Sum3 pre{bsum3[3 * blockIdx.x], bsum3[3 * blockIdx.x + 1], bsum3[3 * blockIdx.x + 2]};
   for (int k = 0; k < w; ++k) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
   pre.nl += incl.nl - t.nl; pre.bs += incl.bs - t.bs; pre.bk += incl.bk - t.bk;
+  uint32_t vprev = (base > 0 && base - 1 < n) ? in[base - 1] : 0u;  // the previous sector's keys
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
     if (j < n) {
-      off[j] = pre.nl;
+      const ull c = pre.nl / (ull)kSegCap;
+      if (j == 0 || c * kSegCap > pre.nl - seg_len(vprev)) {  // (the previous sector's off < c kSegCap)
+        cs0[c] = j;
+        cko[c] = pre.nl;
+      }
       const bool big = v[k] >= (uint32_t)kSegCap;
       if (big) {
         dst[j] = 0x80000000u | (uint32_t)pre.bs;
@@ -172,6 +186,7 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
     }
     const Sum3 q = sum3_of(v[k]);
     pre.nl += q.nl; pre.bs += q.bs; pre.bk += q.bk;
+    vprev = v[k];
   }
 }
 
@@ -349,13 +364,11 @@ __global__ void __launch_bounds__(kPT, 2) seg_coarse_kernel(const ull* __restric
 // sentinels of the bucket tables; one block
 __global__ void seg_tiles_kernel(const ull* __restrict__ tot, uint32_t ncoarse, ull* __restrict__ cstart,
                                  ull* __restrict__ cinfo, ull* __restrict__ ccur, ull* __restrict__ tpre,
-                                 ull* __restrict__ off, ull nsec) {
+                                 ull nsec) {
   __shared__ ull carry;
   __shared__ ull wsum[kSegWarps];
-  if (threadIdx.x == 0) {
-    off[nsec] = tot[0];  // end of the last normal segment
-    carry = 0;
-  }
+  if (threadIdx.x == 0) carry = 0;
+  (void)nsec;
   (void)cinfo;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -480,29 +493,8 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
 
 // ---- 4. per-chunk shared-memory dedup + count --------------------------------------
 // chunk c owns the sectors whose segment starts in [c*kSegCap, (c+1)*kSegCap);
-// their keys lie in [off[s0], off[s1]) and number < 2*kSegCap when every
+// their keys lie in [cko[c], cko[c + 1]) and number < 2*kSegCap when every
 // sector has < kSegCap keys (checked by the caller).
-__device__ __forceinline__ ull first_sector_at(const ull* off, ull nsec, ull pos) {
-  ull lo = 0, hi = nsec;  // smallest s with off[s] >= pos (off[nsec] = total)
-  while (lo < hi) {
-    const ull mid = (lo + hi) >> 1;
-    if (off[mid] >= pos) hi = mid; else lo = mid + 1;
-  }
-  return lo;
-}
-
-// chunk cursors: chunk c's keys start where its first sector's segment does
-// (and each chunk's first sector, so the chunk kernel needs no search)
-__global__ void seg_chunk_cursor_kernel(const ull* __restrict__ off, ull nsec, ull nchunks, ull* __restrict__ cur,
-                                        ull* __restrict__ cs0) {
-  const ull c = (ull)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c <= nchunks) {
-    const ull s = first_sector_at(off, nsec, c * kSegCap);
-    cs0[c] = s;
-    if (c < nchunks) cur[c] = off[s];
-  }
-}
-
 
 // per-block (pc, level) bin table in shared memory: open addressing on the
 // bin id; a full table falls back to the global atomic
@@ -627,7 +619,7 @@ __device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint
 }
 
 // chunk c owns the sectors [cs0[c], cs0[c + 1]) (those whose segment starts in
-// [c kSegCap, (c + 1) kSegCap)); their keys are seg[off[s0], off[s1]), fewer
+// [c kSegCap, (c + 1) kSegCap)); their keys are seg[cko[c], cko[c + 1]), fewer
 // than 2 kSegCap.  (a) distinct (sector, launch, warp) with OR-ed masks in a
 // shared-memory hash set -> sector count = #entries, word b's count = #entries
 // with bit b (the popcount flush of P:328, G6), summed per sector in shared
@@ -637,7 +629,7 @@ __device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint
 // Persistent: a CTA takes chunks from a counter until none are left, so the
 // table and the per-pc bin table are initialised once per CTA (between chunks
 // only the slots a pass used are cleared) and the bins are flushed once.
-__global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ off,
+__global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __restrict__ seg, const ull* __restrict__ cko,
                                                                ull nsec, KeyLayout kl, uint32_t filter,
                                                                uint32_t* __restrict__ wc, uint32_t* __restrict__ sc,
                                                                const uint32_t* __restrict__ site_of,
@@ -678,8 +670,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     if (c >= nchunks) break;
     const ull s0 = cs0[c], s1 = cs0[c + 1];
     if (s0 >= s1) continue;  // (uniform)
-    const ull k0 = off[s0];
-    const uint32_t nk = (uint32_t)(off[s1] - k0);  // < 2 kSegCap
+    const ull k0 = cko[c];
+    const uint32_t nk = (uint32_t)(cko[c + 1] - k0);  // < 2 kSegCap
     const ull win = s1 - s0;
     const bool local = win <= (ull)kHWin;
     if (local)
@@ -893,6 +885,47 @@ __device__ __forceinline__ void big_for_keys(const ull* __restrict__ big, ull b0
       if (base + u * kSegThreads + threadIdx.x < K) f(kk[u]);
   }
 }
+// f(key) over the keys of big[b0, b0 + K) that keep(key) selects: a pass of
+// a P-pass sector keeps ~1/P of what it reads, so each warp first compacts its
+// selected keys into its own 64-key buffer and inserts them 32 at a time with
+// every lane busy (filtering in place leaves most lanes idle in the insert)
+constexpr int kBigWBuf = 64;
+template <typename Keep, typename F>
+__device__ __forceinline__ void big_for_kept(const ull* __restrict__ big, ull b0, uint32_t K, ull* wbuf, Keep keep,
+                                             F f) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t wn = 0;  // keys in the warp's buffer (uniform, < 32 between appends)
+  const uint32_t K32 = (K + 31) & ~31u;  // whole warps iterate (inactive lanes keep nothing)
+  for (uint32_t base = 0; base < K32; base += kSegThreads * kBigUnroll) {
+    ull kk[kBigUnroll];
+#pragma unroll
+    for (int u = 0; u < kBigUnroll; ++u) {
+      const uint32_t j = base + u * kSegThreads + threadIdx.x;
+      kk[u] = j < K ? big[b0 + j] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kBigUnroll; ++u) {
+      const bool ok = base + u * kSegThreads + threadIdx.x < K && keep(kk[u]);
+      const unsigned b = __ballot_sync(GFULL, ok);
+      if (ok) wbuf[wn + __popc(b & lt)] = kk[u];
+      wn += __popc(b);
+      if (wn >= 32) {  // (uniform)
+        __syncwarp();
+        const ull k = wbuf[lane];
+        const ull k2 = wbuf[32 + lane];
+        __syncwarp();
+        if ((uint32_t)lane < wn - 32) wbuf[lane] = k2;
+        wn -= 32;
+        __syncwarp();
+        f(k);
+      }
+    }
+  }
+  __syncwarp();
+  if ((uint32_t)lane < wn) f(wbuf[lane]);
+}
 __device__ __forceinline__ uint32_t big_table_bits(uint32_t keys_per_pass) {
   uint32_t tb = 8;
   while ((1u << tb) * 3u < keys_per_pass * 4u && (1u << tb) < (uint32_t)kBigSlots) ++tb;
@@ -959,7 +992,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
                                                              const uint32_t* __restrict__ site_of,
                                                              ull* __restrict__ pc_hist, DevCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots]
+  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots], then [warps][kBigWBuf] compaction buffers
   __shared__ uint32_t s_cnt[9];
   const ull nbs = tot[1];
   ull i;
@@ -975,12 +1008,22 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
   const int T = 1 << tb;
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
-  big_for_keys(big, b0, K, [&](ull k) {
-    const ull id = (k >> RS) & lwmask;
-    if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) return;
-    if (big_pass_of(id, P) != p) return;
-    if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-  });
+  if (P == 1) {
+    big_for_keys(big, b0, K, [&](ull k) {
+      if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) return;
+      if (!big_or(tab, tb, (k >> RS) & lwmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+    });
+  } else {
+    big_for_kept(
+        big, b0, K, tab + kBigSlots + (threadIdx.x >> 5) * kBigWBuf,
+        [&](ull k) {
+          return (filter == THERMO_ALL_LAUNCHES || key_launch(k, kl) == filter) &&
+                 big_pass_of((k >> RS) & lwmask, P) == p;
+        },
+        [&](ull k) {
+          if (!big_or(tab, tb, (k >> RS) & lwmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+        });
+  }
   __syncthreads();
   uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs = 0;
   for (int j = threadIdx.x; j < T; j += kSegThreads) {
@@ -1044,7 +1087,7 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __re
                                                                 const uint32_t* __restrict__ site_of,
                                                                 ull* __restrict__ pc_hist, DevCounters* ctr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots]
+  ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots], then [warps][kBigWBuf] compaction buffers
   const ull nbs = tot[1];
   ull i;
   uint32_t p, P;
@@ -1058,12 +1101,23 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __re
   const int T = 1 << tb;
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
-  big_for_keys(big, b0, K, [&](ull k) {
-    const ull id = (k >> 8) & pmask;
-    if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) return;
-    if (big_pass_of(id, P) != p) return;
-    if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-  });
+  if (P == 1) {
+    big_for_keys(big, b0, K, [&](ull k) {
+      const ull id = (k >> 8) & pmask;
+      if (filter != THERMO_ALL_LAUNCHES && (site_of[id] >> 20) != filter) return;
+      if (!big_or(tab, tb, id, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+    });
+  } else {
+    big_for_kept(
+        big, b0, K, tab + kBigSlots + (threadIdx.x >> 5) * kBigWBuf,
+        [&](ull k) {
+          const ull id = (k >> 8) & pmask;
+          return (filter == THERMO_ALL_LAUNCHES || (site_of[id] >> 20) == filter) && big_pass_of(id, P) == p;
+        },
+        [&](ull k) {
+          if (!big_or(tab, tb, (k >> 8) & pmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+        });
+  }
   __syncthreads();
   const uint32_t scnt = sc[g];
   uint32_t npc = 0;
@@ -1090,12 +1144,12 @@ ull segment_chunk_cap() { return kSegCap; }
 cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
   cudaError_t e;
   if (ws.cap_sec < nsec + 1) {
-    cudaFree(ws.cnt); cudaFree(ws.off); cudaFree(ws.cur); cudaFree(ws.bsum); cudaFree(ws.cs0); cudaFree(ws.dst);
-    ws.cnt = nullptr; ws.off = ws.cur = ws.bsum = ws.cs0 = nullptr;
+    cudaFree(ws.cnt); cudaFree(ws.cko); cudaFree(ws.cur); cudaFree(ws.bsum); cudaFree(ws.cs0); cudaFree(ws.dst);
+    ws.cnt = nullptr; ws.cko = ws.cur = ws.bsum = ws.cs0 = nullptr;
     ws.dst = nullptr;
     ws.cap_sec = 0;
     if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
-    if ((e = cudaMalloc(&ws.off, (nsec + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cko, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.cs0, (nsec + 2) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.dst, (nsec + 1) * sizeof(uint32_t)))) return e;
@@ -1147,18 +1201,19 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
   ull* tot = reinterpret_cast<ull*>(ws.maxc) + 1;
   const ull nb = (nsec + kScanBlock - 1) / kScanBlock;
   seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
-  seg_scan_blocks<<<1, kSegThreads, 0, s>>>(ws.bsum, nb, tot);
-  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.off, ws.dst, ws.bg, ws.boff,
+  seg_scan_blocks<<<1, kScanBT, 0, s>>>(ws.bsum, nb, tot, nsec, ws.cs0, ws.cko);
+  seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.cs0, ws.cko, ws.dst, ws.bg, ws.boff,
                                                       ws.gpre);
   seg_groups_kernel<<<(unsigned)((ngroups + 256) / 256), 256, 0, s>>>(ws.gpre, ngroups, tot, ws.ncoarse, ws.cb,
                                                                       ws.cstart, ws.cinfo);
-  seg_tiles_kernel<<<1, kSegThreads, 0, s>>>(tot, ws.ncoarse, ws.cstart, ws.cinfo, ws.ccur, ws.tpre, ws.off, nsec);
+  seg_tiles_kernel<<<1, kSegThreads, 0, s>>>(tot, ws.ncoarse, ws.cstart, ws.cinfo, ws.ccur, ws.tpre, nsec);
   ws.launches += 5;
   ull hv[4];
   if ((e = cudaMemcpyAsync(hv, ws.maxc, 4 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
   if ((e = cudaStreamSynchronize(s))) return e;
   *max_per_sector = (uint32_t)hv[0];
   *n_big = hv[3];         // keys of big sectors
+  ws.n_normal = hv[1];  // keys of normal sectors (the chunks')
   ws.n_bigsec = hv[2];
   ws.n_big_keys = hv[3];
   if (ws.n_bigsec)  // big-sector cursors start at their segments
@@ -1185,8 +1240,10 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   for (int k = 0; k < 4; ++k) ws.ran[k] = false;
   if (ws.ev[0]) cudaEventRecord(ws.ev[0], s);
   if (n) {
-    const ull nch = (n + kSegCap - 1) / kSegCap;  // <= nsec + 1 = the cursor array's size
-    seg_chunk_cursor_kernel<<<(unsigned)((nch + 256) / 256), 256, 0, s>>>(ws.off, nsec, nch, ws.cur, ws.cs0);
+    // chunk cursors start at the chunks' first keys (chunks cover the NL normal
+    // keys: ceil(NL / kSegCap) <= nsec of them)
+    const ull nch = (ws.n_normal + kSegCap - 1) / kSegCap;
+    if (nch && (e = cudaMemcpyAsync(ws.cur, ws.cko, nch * sizeof(ull), cudaMemcpyDeviceToDevice, s))) return e;
     const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
     seg_coarse_kernel<<<g1, kPT, csm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
     if (ws.ev[1]) cudaEventRecord(ws.ev[1], s);
@@ -1207,7 +1264,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   }
   const size_t smem = segment_chunk_smem();
   smem_optin((const void*)seg_chunk_kernel, (int)smem);
-  const ull chunks = (n + kSegCap - 1) / kSegCap;
+  const ull chunks = (ws.n_normal + kSegCap - 1) / kSegCap;
   if (chunks) {
     if (ws.ev[2] && !n) cudaEventRecord(ws.ev[2], s);
     if (!ws.chunk_ctr && (e = cudaMalloc(&ws.chunk_ctr, sizeof(ull)))) return e;
@@ -1215,7 +1272,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_chunk_kernel, kSegThreads, smem);
     const ull grid = std::min<ull>(chunks, (ull)num_sms * (per_sm < 1 ? 1 : per_sm));
-    seg_chunk_kernel<<<(unsigned)grid, kSegThreads, smem, s>>>(out, ws.off, nsec, kl, filter, wc, sc, site_of,
+    seg_chunk_kernel<<<(unsigned)grid, kSegThreads, smem, s>>>(out, ws.cko, nsec, kl, filter, wc, sc, site_of,
                                                                pc_hist, ctr, ws.cs0, chunks, ws.chunk_ctr,
                                                                pc_hist && n_pc <= kFewPcs ? 1u : 0u);
     ws.launches += 1;
@@ -1228,7 +1285,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     seg_big_plan_kernel<<<1, kSegThreads, 0, s>>>(ws.boff, tot, npc, ws.bpre, ws.bpre + ws.big_cap);
     // CTAs: at most one per kBigFill keys plus one per sector
     const ull grid = ws.n_big_keys / kBigFill + ws.n_bigsec + 1;
-    const size_t bsm = kBigSlots * sizeof(ull);
+    const size_t bsm = ((size_t)kBigSlots + kSegWarps * kBigWBuf) * sizeof(ull);
     smem_optin((const void*)seg_big_kernel, (int)bsm);
     smem_optin((const void*)seg_big_pc_kernel, (int)bsm);
     seg_big_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre, kl, filter, wc, sc,

@@ -586,7 +586,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->d_instr, ctx->d_launch_ctr, ctx->d_hist, ctx->d_pchist, ctx->d_ind, ctx->d_tile_obj,
                   ctx->d_tile_first, ctx->d_tile_end, ctx->d_tile_info, ctx->d_tile_prev, ctx->d_heads,
                   ctx->d_table, ctx->d_pctable, ctx->d_dense, ctx->d_wl, ctx->d_deferred, ctx->sw.alt, ctx->sw.status, ctx->sw.hist, ctx->sw.counters,
-                  ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.off, ctx->seg.cur,
+                  ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.cko, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->seg.gpre, ctx->seg.cb,
                   ctx->seg.cstart, ctx->seg.cinfo, ctx->seg.ccur, ctx->seg.tpre, ctx->seg.tbk, ctx->seg.tmp, ctx->seg.bg,
                   ctx->seg.boff, ctx->seg.bcur, ctx->seg.bpre, ctx->seg.chunk_ctr, ctx->d_stage[0],

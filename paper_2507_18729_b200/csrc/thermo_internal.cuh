@@ -167,9 +167,9 @@ ull* radix_sort_keys(ull* keys, ull n, int lo_bit, int nbits, SortWorkspace& ws,
 // shared-memory dedup and count
 struct SegWorkspace {
   uint32_t* cnt = nullptr;   // [S_tot + 1] keys per sector
-  ull* off = nullptr;        // [S_tot + 1] exclusive prefix (off[S_tot] = total)
+  ull* cko = nullptr;        // [chunks + 1] first key of each chunk (+ end = the normal keys)
   ull* cur = nullptr;        // [S_tot + 1] scatter cursors (one per chunk)
-  ull* cs0 = nullptr;        // [S_tot + 2] first sector of each chunk (+ end)
+  ull* cs0 = nullptr;        // [chunks + 1 <= S_tot + 2] first sector of each chunk (+ end)
   uint32_t* dst = nullptr;   // [S_tot + 1] chunk of each sector's keys (~0: a big sector's, hash path)
   ull* bsum = nullptr;       // scan block sums
   uint32_t* maxc = nullptr;  // [8 u64]: max keys in one sector | totals: normal keys, big sectors, big keys
@@ -191,7 +191,7 @@ struct SegWorkspace {
   ull* boff = nullptr;       // [n big sectors] its first key in `big`
   ull* bcur = nullptr;       // [n big sectors] pass-2 cursors
   ull* bpre = nullptr;       // [2][big_cap] first CTA of each big sector (main, pc passes)
-  ull big_cap = 0, n_bigsec = 0, n_big_keys = 0;
+  ull big_cap = 0, n_bigsec = 0, n_big_keys = 0, n_normal = 0;
   ull* chunk_ctr = nullptr;  // persistent chunk kernel: chunks handed out
   // per-kernel timers (created by the caller): before coarse, after coarse,
   // after fine, after chunk, after big; ran[] says which intervals ran
