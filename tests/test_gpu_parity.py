@@ -302,6 +302,34 @@ def test_hot_sector_and_short_instructions(dedup):
         assert th.stats()["dedup_used"] == 3  # SEGMENT with its big-sector side path, no fallback
 
 
+def _one_sector_trace(n_warps=60000):
+    """Every warp loads the 8 words of a 32-byte counter block (one sector) and
+    one word of a 256-byte array: 9 registered sectors for 120 k keys, far
+    below keys / 2048 (the SEGMENT chunk tables are sized by sectors)."""
+    objects = [(0x300000, 32, 0, 0, "counter"), (0x400000, 256, 0, 1, "arr")]
+    w = torch.arange(n_warps, dtype=torch.int64)
+    lane = torch.arange(32, dtype=torch.int64)
+    a0 = (0x300000 + 4 * (lane % 8)).unsqueeze(0).expand(n_warps, 32)
+    a1 = (0x400000 + 4 * ((w % 64).unsqueeze(1) + 0 * lane)).expand(n_warps, 32)
+    act0 = (lane < 8).unsqueeze(0).expand(n_warps, 32)
+    act1 = (lane == 0).unsqueeze(0).expand(n_warps, 32)
+    addr = torch.stack([a0, a1], 1).reshape(-1, 32)
+    act = torch.stack([act0, act1], 1).reshape(-1, 32)
+    wid = w.repeat_interleave(2)
+    pc = torch.tensor([0x600, 0x610], dtype=torch.int64).repeat(n_warps)
+    rec = tg.from_instructions(addr, act, wid, pc, 0, 2)
+    return tg.Trace("one-sector", objects, rec, meta=dict(warps=n_warps, launches=1))
+
+
+@pytest.mark.parametrize("dedup", [0, 1, 2])
+def test_one_hot_sector_many_warps(dedup):
+    t = _one_sector_trace()
+    orc, th = run_both(t, dedup=dedup)
+    compare(orc, th, t)
+    assert th.heatmap(0, SECTOR).tolist() == [60000]
+    assert th.heatmap(0, WORD).tolist() == [60000] * 8
+
+
 @pytest.mark.parametrize("case", ["tiny", "fig3a", "fig3b", "gemm", "stencil", "random", "hot"])
 def test_access_counts(case):
     """Access counts: lane accesses per word, every
