@@ -19,6 +19,11 @@ constexpr unsigned GFULL = 0xFFFFFFFFu;
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kSegCap = 2048;            // chunk window (keys); a chunk holds < 2 * kSegCap keys
+constexpr int kChunkSec = 1024;          // a chunk spans at most this many sectors (its rows fit the CTA)
+// chunk of sector j with normal-key prefix off: both terms are non-decreasing
+// in j, so a chunk (the sectors with one value) lies in one kSegCap window of
+// keys (< 2 kSegCap keys) and in one kChunkSec block of sectors
+__host__ __device__ __forceinline__ ull chunk_of(ull off, ull j) { return off / kSegCap + j / kChunkSec; }
 constexpr int kScanBlock = 2048;         // scan elements per block (256 threads x 8)
 
 __device__ __forceinline__ unsigned lanemask_lt_g() {
@@ -98,9 +103,7 @@ __global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __r
   }
 }
 
-// one block: exclusive scan of the block sums (three columns); totals -> tot[0..3);
-// the chunk table's end (chunk ceil(NL / kSegCap): no sector, all NL keys
-// before it; seg_scan_apply overwrites it when a sector starts there)
+// one block: exclusive scan of the block sums (three columns); totals -> tot[0..3)
 constexpr int kScanBT = 1024;  // seg_scan_blocks threads: each scans a contiguous run of block sums
 __global__ void __launch_bounds__(kScanBT) seg_scan_blocks(ull* bsum3, ull nb, ull* tot, ull nsec, ull* cs0,
                                                            ull* cko) {
@@ -124,24 +127,22 @@ __global__ void __launch_bounds__(kScanBT) seg_scan_blocks(ull* bsum3, ull nb, u
     bsum3[3 * i] = pre.nl; bsum3[3 * i + 1] = pre.bs; bsum3[3 * i + 2] = pre.bk;
     pre.nl += v.nl; pre.bs += v.bs; pre.bk += v.bk;
   }
-  if (threadIdx.x == 0) {
-    tot[0] = all.nl; tot[1] = all.bs; tot[2] = all.bk;
-    const ull nch = (all.nl + kSegCap - 1) / kSegCap;
-    cs0[nch] = nsec;
-    cko[nch] = all.nl;
-  }
+  if (threadIdx.x == 0) { tot[0] = all.nl; tot[1] = all.bs; tot[2] = all.bk; }
+  (void)nsec; (void)cs0; (void)cko;
 }
 
 // With off[g] = the normal-key prefix at sector g (the sector's segment in the
-// chunked layout, never stored): dst[g] = chunk off[g] / kSegCap of g's normal
+// chunked layout, never stored): dst[g] = chunk_of(off[g], g) of g's normal
 // keys, or 0x80000000 | big index for a big sector (then bg[i] = g, boff[i] =
-// big-key prefix); chunk c starts at the first sector with off >= c kSegCap:
-// cs0[c] = that sector, cko[c] = its off (a normal segment is shorter than
-// kSegCap, so at most one chunk starts at each sector);
+// big-key prefix); the chunks (chunk_of(g - 1), chunk_of(g)] start at g
+// (at most two: a normal segment is shorter than kSegCap): cs0[c] = g, cko[c]
+// = off[g]; after the last sector the end of the table (cs0 = n, cko = NL) and
+// the chunk count -> *nch;
 // gpre[q] = (NL, BS, BK) at the first sector of group q (kGroup sectors)
 __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull* __restrict__ bsum3,
                                ull* __restrict__ cs0, ull* __restrict__ cko, uint32_t* __restrict__ dst,
-                               ull* __restrict__ bg, ull* __restrict__ boff, ull* __restrict__ gpre) {
+                               ull* __restrict__ bg, ull* __restrict__ boff, ull* __restrict__ gpre,
+                               ull* __restrict__ nch) {
   __shared__ ull ws[3][kSegWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
@@ -165,10 +166,15 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
     if (j < n) {
-      const ull c = pre.nl / (ull)kSegCap;
-      if (j == 0 || c * kSegCap > pre.nl - seg_len(vprev)) {  // (the previous sector's off < c kSegCap)
-        cs0[c] = j;
-        cko[c] = pre.nl;
+      const ull c = chunk_of(pre.nl, j);
+      for (ull cc = j == 0 ? 0 : chunk_of(pre.nl - seg_len(vprev), j - 1) + 1; cc <= c; ++cc) {
+        cs0[cc] = j;
+        cko[cc] = pre.nl;
+      }
+      if (j == n - 1) {
+        cs0[c + 1] = n;
+        cko[c + 1] = pre.nl + seg_len(v[k]);
+        *nch = c + 1;
       }
       const bool big = v[k] >= (uint32_t)kSegCap;
       if (big) {
@@ -176,7 +182,7 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
         bg[pre.bs] = j;
         boff[pre.bs] = pre.bk;
       } else {
-        dst[j] = (uint32_t)(pre.nl / (ull)kSegCap);
+        dst[j] = (uint32_t)c;
       }
       if ((j & (kGroup - 1)) == 0) {
         gpre[3 * (j / kGroup)] = pre.nl;
@@ -192,11 +198,12 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
 
 // coarse buckets balanced by key count: group q (kGroup sectors) goes to
 // bucket cb[q] = (keys before q) * ncoarse / n, non-decreasing in q; bucket b
-// starts at its first group's prefixes (cstart = all keys, cinfo = (NL, BS));
+// starts at its first group's prefixes (cstart = all keys, cinfo = (NL, BS,
+// first sector));
 // buckets no group maps to are empty (the next group's / the totals' start)
 __global__ void seg_groups_kernel(const ull* __restrict__ gpre, ull ngroups, const ull* __restrict__ tot,
                                   uint32_t ncoarse, uint16_t* __restrict__ cb, ull* __restrict__ cstart,
-                                  ull* __restrict__ cinfo) {
+                                  ull* __restrict__ cinfo, ull nsec) {
   const ull q = (ull)blockIdx.x * blockDim.x + threadIdx.x;
   if (q > ngroups) return;
   const ull n = tot[0] + tot[2];
@@ -211,10 +218,12 @@ __global__ void seg_groups_kernel(const ull* __restrict__ gpre, ull ngroups, con
   const uint32_t bp = q == 0 ? 0u : bucket(q - 1) + 1;  // buckets (bucket(q-1), bucket(q)] start here
   const ull nl = q < ngroups ? gpre[3 * q] : tot[0], bs = q < ngroups ? gpre[3 * q + 1] : tot[1];
   const ull all = q < ngroups ? gpre[3 * q] + gpre[3 * q + 2] : n;
+  const ull g0 = q < ngroups ? q * kGroup : nsec;
   for (uint32_t b = bp; b <= bq; ++b) {
     cstart[b] = all;
-    cinfo[2 * b] = nl;
-    cinfo[2 * b + 1] = bs;
+    cinfo[3 * b] = nl;
+    cinfo[3 * b + 1] = bs;
+    cinfo[3 * b + 2] = g0;
   }
 }
 
@@ -421,13 +430,14 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   const uint32_t b = tbk[t];  // bucket b: tpre[b] <= t < tpre[b + 1]
   const ull k0 = cstart[b] + (t - tpre[b]) * kPTile;
   const ull k1 = k0 + kPTile < cstart[b + 1] ? k0 + kPTile : cstart[b + 1];
-  const ull nl0 = cinfo[2 * b], nl1 = cinfo[2 * b + 2];
-  const ull bs0 = cinfo[2 * b + 1], bs1 = cinfo[2 * b + 3];
-  const ull c_lo = nl0 / kSegCap;
-  const uint32_t nbn = nl1 > nl0 ? (uint32_t)((nl1 - 1) / kSegCap - c_lo + 1) : 0u;  // chunk bins
+  const ull nl0 = cinfo[3 * b], nl1 = cinfo[3 * b + 3];
+  const ull bs0 = cinfo[3 * b + 1], bs1 = cinfo[3 * b + 4];
+  // the bucket's chunks lie in [chunk_of(nl0, g0), chunk_of(nl1, g1)] (monotone)
+  const ull c_lo = chunk_of(nl0, cinfo[3 * b + 2]);
+  const uint32_t nbn = nl1 > nl0 ? (uint32_t)(chunk_of(nl1, cinfo[3 * b + 5]) - c_lo + 1) : 0u;  // chunk bins
   const uint32_t nbins = nbn + (uint32_t)(bs1 - bs0);
   ull k[kPPer];
-  uint32_t d[kPPer], r[kPPer];
+  uint32_t d[kPPer];  // destination, ~0 = none; below kFineBins bins: | rank << 16
 #pragma unroll
   for (int u = 0; u < kPPer; ++u) {
     const ull i = k0 + (ull)u * kPT + threadIdx.x;
@@ -462,16 +472,11 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   }
   for (uint32_t i = threadIdx.x; i < nbins; i += kPT) sm.cnt[i] = 0;
   __syncthreads();
-  unsigned pe[kPPer];
+  // rank within the destination: one shared atomic per key (order within a
+  // destination is free)
 #pragma unroll
-  for (int u = 0; u < kPPer; ++u) pe[u] = __match_any_sync(GFULL, d[u]);
-#pragma unroll
-  for (int u = 0; u < kPPer; ++u) {
-    const int ldr = __ffs(pe[u]) - 1;
-    uint32_t r0 = 0;
-    if (d[u] != 0xFFFFFFFFu && lane == ldr) r0 = atomicAdd(&sm.cnt[d[u]], (uint32_t)__popc(pe[u]));
-    r[u] = __shfl_sync(GFULL, r0, ldr) + __popc(pe[u] & lt);
-  }
+  for (int u = 0; u < kPPer; ++u)
+    if (d[u] != 0xFFFFFFFFu) d[u] |= atomicAdd(&sm.cnt[d[u]], 1u) << 16;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nbins; i += kPT)
     if (sm.cnt[i]) sm.base[i] = atomicAdd(i < nbn ? &cur[c_lo + i] : &bcur[bs0 + i - nbn], (ull)sm.cnt[i]);
@@ -480,9 +485,10 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
 #pragma unroll
   for (int u = 0; u < kPPer; ++u)
     if (d[u] != 0xFFFFFFFFu) {
-      const uint32_t q = sm.excl[d[u]] + r[u];
+      const uint32_t dd = d[u] & 0xFFFFu;
+      const uint32_t q = sm.excl[dd] + (d[u] >> 16);
       sm.stage[q] = k[u];
-      sm.sd[q] = (uint16_t)d[u];
+      sm.sd[q] = (uint16_t)dd;
     }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < tot; i += kPT) {
@@ -492,9 +498,10 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
 }
 
 // ---- 4. per-chunk shared-memory dedup + count --------------------------------------
-// chunk c owns the sectors whose segment starts in [c*kSegCap, (c+1)*kSegCap);
-// their keys lie in [cko[c], cko[c + 1]) and number < 2*kSegCap when every
-// sector has < kSegCap keys (checked by the caller).
+// chunk c owns the sectors g with chunk_of(off[g], g) = c: at most kChunkSec of
+// them, whose segments start in one kSegCap window; their keys lie in
+// [cko[c], cko[c + 1]) and number < 2*kSegCap (every normal sector has fewer
+// than kSegCap keys).
 
 // per-block (pc, level) bin table in shared memory: open addressing on the
 // bin id; a full table falls back to the global atomic
@@ -520,6 +527,7 @@ __device__ __forceinline__ void bin_add(uint32_t* tbin, uint32_t* tcnt, ull* g, 
 // word's accesses is idempotent)
 constexpr int kHSlots = 5120;  // > 1.25 x the chunk's < 2 * kSegCap keys (typically ~2/3 of that)
 constexpr int kHWin = 1024;    // chunks spanning at most this many sectors count them in shared memory
+static_assert(kHWin >= kChunkSec, "every chunk counts its sectors in shared memory");
 constexpr ull kHEmpty = ~0ull;
 // insert returns true when the id takes a new slot (*slot); the caller appends
 // new slots to the chunk's list (one atomic per warp), so the scans visit
@@ -618,14 +626,13 @@ __device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint
   }
 }
 
-// chunk c owns the sectors [cs0[c], cs0[c + 1]) (those whose segment starts in
-// [c kSegCap, (c + 1) kSegCap)); their keys are seg[cko[c], cko[c + 1]), fewer
-// than 2 kSegCap.  (a) distinct (sector, launch, warp) with OR-ed masks in a
-// shared-memory hash set -> sector count = #entries, word b's count = #entries
-// with bit b (the popcount flush of P:328, G6), summed per sector in shared
-// memory (or, for a chunk spanning > kHWin sectors, with warp-aggregated
-// global atomics); (b) distinct (sector, pc id) with OR-ed masks -> per-pc
-// level histograms (G11)
+// chunk c owns the sectors [cs0[c], cs0[c + 1]) (at most kChunkSec); their
+// keys are seg[cko[c], cko[c + 1]), fewer than 2 kSegCap.  (a) distinct
+// (sector, launch, warp) with OR-ed masks in a shared-memory hash set ->
+// sector count = #entries, word b's count = #entries with bit b (the popcount
+// flush of P:328, G6), summed per sector in shared memory and stored as the
+// chunk's rows; (b) distinct (sector, pc id) with OR-ed masks -> per-pc level
+// histograms (G11)
 // Persistent: a CTA takes chunks from a counter until none are left, so the
 // table and the per-pc bin table are initialised once per CTA (between chunks
 // only the slots a pass used are cleared) and the bins are flushed once.
@@ -650,8 +657,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   const ull pmask = (1ull << kl.P) - 1;
   for (int i = threadIdx.x; i < kHSlots; i += kSegThreads) tab[i] = kHEmpty;
   // few_pcs (at most kFewPcs pc ids in the job): the bin region is a direct
-  // [pc][word | sector][level] table, and a local chunk collects its (sector,
-  // pc) word masks as bytes (one shared OR per key) instead of the second set
+  // [pc][word | sector][level] table, and a chunk collects its (sector, pc)
+  // word masks as bytes (one shared OR per key) instead of the second set
   uint32_t* const dir = tbin;  // [kFewPcs * 2 * kLevels] <= 2 kPcBins
   if (few_pcs) {
     for (int i = threadIdx.x; i < 2 * kPcBins; i += kSegThreads) dir[i] = 0;
@@ -672,10 +679,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     if (s0 >= s1) continue;  // (uniform)
     const ull k0 = cko[c];
     const uint32_t nk = (uint32_t)(cko[c + 1] - k0);  // < 2 kSegCap
-    const ull win = s1 - s0;
-    const bool local = win <= (ull)kHWin;
-    if (local)
-      for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
+    const ull win = s1 - s0;  // <= kChunkSec <= kHWin: the chunk's rows are counted in shared memory
+    for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
     __syncthreads();
     // ---- (a) distinct (sector, launch, warp) ----
     ull kk[kKPT];
@@ -694,41 +699,31 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
 #pragma unroll
       for (int b = 0; b < 8; ++b) cb[b] = __popc(__ballot_sync(GFULL, (m >> b) & 1u) & peers);
       if (occ && lane == __ffs(peers) - 1) {
-        const uint32_t cs = __popc(peers);
-        if (local) {
-          uint32_t* cg = cnt + gl * 5;
+        uint32_t* cg = cnt + gl * 5;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
-          atomicAdd(&cg[4], cs);
-        } else {
-          const ull g = s0 + gl;
-          atomicAdd(&sc[g], cs);
-#pragma unroll
-          for (int b = 0; b < 8; ++b)
-            if (cb[b]) atomicAdd(&wc[8 * g + b], cb[b]);
-        }
+        for (int j = 0; j < 4; ++j)
+          if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
+        atomicAdd(&cg[4], (uint32_t)__popc(peers));
       }
     }
     distinct += nent;
     __syncthreads();
-    if (local) {  // the chunk owns its sectors: plain stores of the nonzero rows
-      for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
-        const uint32_t* cg = cnt + j * 5;
-        if (cg[4] == 0) continue;
-        const ull g = s0 + j;
-        sc[g] = cg[4];
-        uint4 lo, hi;
-        lo.x = cg[0] & 0xFFFFu; lo.y = cg[0] >> 16; lo.z = cg[1] & 0xFFFFu; lo.w = cg[1] >> 16;
-        hi.x = cg[2] & 0xFFFFu; hi.y = cg[2] >> 16; hi.z = cg[3] & 0xFFFFu; hi.w = cg[3] >> 16;
-        reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
-        reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
-      }
+    // the chunk owns its sectors: plain stores of the nonzero rows
+    for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
+      const uint32_t* cg = cnt + j * 5;
+      if (cg[4] == 0) continue;
+      const ull g = s0 + j;
+      sc[g] = cg[4];
+      uint4 lo, hi;
+      lo.x = cg[0] & 0xFFFFu; lo.y = cg[0] >> 16; lo.z = cg[1] & 0xFFFFu; lo.w = cg[1] >> 16;
+      hi.x = cg[2] & 0xFFFFu; hi.y = cg[2] >> 16; hi.z = cg[3] & 0xFFFFu; hi.w = cg[3] >> 16;
+      reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
+      reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
     }
     for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
     if (!pc_hist) continue;  // (uniform)
     __syncthreads();
-    if (few_pcs && local) {
+    if (few_pcs) {
       // ---- (b') the chunk's (sector, pc) word masks as bytes: pcm[2 j + pc / 4]
       // byte pc % 4 = OR of the masks of sector s0 + j's keys of that pc, in the
       // (now clear) first win u64 slots of the table ----
@@ -784,28 +779,20 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
       const uint32_t gl = (uint32_t)(v >> (8 + kl.P));
       const uint32_t pcid = (uint32_t)((v >> 8) & pmask);
       const uint32_t m = (uint32_t)v & 0xFFu;
-      const uint32_t* cg = cnt + gl * 5;
-      const ull g = s0 + gl;
+      const uint32_t* cg = cnt + (head ? gl : 0u) * 5;
       {
-        const uint32_t scv = head ? (local ? cg[4] : __ldcg(&sc[g])) : 0u;
+        const uint32_t scv = head ? cg[4] : 0u;
         const uint32_t bin = head ? (pcid * 2 + 1) * kLevels + level_of_g(scv) : 0xFFFFFFFFu;
         const unsigned mm = __match_any_sync(GFULL, bin);
-        if (head && (__ffs(mm) - 1) == lane) {
-          if (few_pcs) atomicAdd(&dir[bin], (uint32_t)__popc(mm));
-          else bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
-        }
+        if (head && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
       }
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
         const bool hb = head && ((m >> b) & 1u);
-        uint32_t wv = 0;
-        if (hb) wv = local ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : __ldcg(&wc[8 * g + b]);
+        const uint32_t wv = hb ? ((cg[b >> 1] >> (16 * (b & 1))) & 0xFFFFu) : 0u;
         const uint32_t bin = hb ? (pcid * 2) * kLevels + level_of_g(wv) : 0xFFFFFFFFu;
         const unsigned mm = __match_any_sync(GFULL, bin);
-        if (hb && (__ffs(mm) - 1) == lane) {
-          if (few_pcs) atomicAdd(&dir[bin], (uint32_t)__popc(mm));
-          else bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
-        }
+        if (hb && (__ffs(mm) - 1) == lane) bin_add(tbin, tcnt, pc_hist, bin, __popc(mm));
       }
     }
     if (threadIdx.x == 0) distinct_pc += npc;
@@ -1149,9 +1136,10 @@ cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
     ws.dst = nullptr;
     ws.cap_sec = 0;
     if ((e = cudaMalloc(&ws.cnt, (nsec + 1) * sizeof(uint32_t)))) return e;
-    if ((e = cudaMalloc(&ws.cko, (nsec + 1) * sizeof(ull)))) return e;
-    if ((e = cudaMalloc(&ws.cur, (nsec + 1) * sizeof(ull)))) return e;
-    if ((e = cudaMalloc(&ws.cs0, (nsec + 2) * sizeof(ull)))) return e;
+    // chunks: chunk_of(NL, nsec) + 1 <= nsec + nsec / kChunkSec + 1 (NL < kSegCap nsec)
+    if ((e = cudaMalloc(&ws.cko, (nsec + nsec / kChunkSec + 3) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cur, (nsec + nsec / kChunkSec + 3) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cs0, (nsec + nsec / kChunkSec + 3) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.dst, (nsec + 1) * sizeof(uint32_t)))) return e;
     if ((e = cudaMalloc(&ws.bsum, 3 * ((nsec + kScanBlock) / kScanBlock + 1) * sizeof(ull)))) return e;
     cudaFree(ws.gpre); cudaFree(ws.cb);
@@ -1163,7 +1151,7 @@ cudaError_t segment_reserve(SegWorkspace& ws, ull nsec) {
   if (!ws.maxc && (e = cudaMalloc(&ws.maxc, 8 * sizeof(ull)))) return e;  // maxc | totals NL, BS, BK
   if (!ws.cstart) {
     if ((e = cudaMalloc(&ws.cstart, (kCoarse + 1) * sizeof(ull)))) return e;
-    if ((e = cudaMalloc(&ws.cinfo, 2 * (kCoarse + 1) * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.cinfo, 3 * (kCoarse + 1) * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.ccur, kCoarse * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.tpre, (kCoarse + 1) * sizeof(ull)))) return e;
   }
@@ -1203,17 +1191,18 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
   seg_scan_reduce<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.maxc);
   seg_scan_blocks<<<1, kScanBT, 0, s>>>(ws.bsum, nb, tot, nsec, ws.cs0, ws.cko);
   seg_scan_apply<<<(unsigned)nb, kSegThreads, 0, s>>>(ws.cnt, nsec, ws.bsum, ws.cs0, ws.cko, ws.dst, ws.bg, ws.boff,
-                                                      ws.gpre);
+                                                      ws.gpre, tot + 3);
   seg_groups_kernel<<<(unsigned)((ngroups + 256) / 256), 256, 0, s>>>(ws.gpre, ngroups, tot, ws.ncoarse, ws.cb,
-                                                                      ws.cstart, ws.cinfo);
+                                                                      ws.cstart, ws.cinfo, nsec);
   seg_tiles_kernel<<<1, kSegThreads, 0, s>>>(tot, ws.ncoarse, ws.cstart, ws.cinfo, ws.ccur, ws.tpre, nsec);
   ws.launches += 5;
-  ull hv[4];
-  if ((e = cudaMemcpyAsync(hv, ws.maxc, 4 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
+  ull hv[5];
+  if ((e = cudaMemcpyAsync(hv, ws.maxc, 5 * sizeof(ull), cudaMemcpyDeviceToHost, s))) return e;
   if ((e = cudaStreamSynchronize(s))) return e;
   *max_per_sector = (uint32_t)hv[0];
   *n_big = hv[3];         // keys of big sectors
   ws.n_normal = hv[1];  // keys of normal sectors (the chunks')
+  ws.n_chunks = hv[4];
   ws.n_bigsec = hv[2];
   ws.n_big_keys = hv[3];
   if (ws.n_bigsec)  // big-sector cursors start at their segments
@@ -1240,9 +1229,8 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   for (int k = 0; k < 4; ++k) ws.ran[k] = false;
   if (ws.ev[0]) cudaEventRecord(ws.ev[0], s);
   if (n) {
-    // chunk cursors start at the chunks' first keys (chunks cover the NL normal
-    // keys: ceil(NL / kSegCap) <= nsec of them)
-    const ull nch = (ws.n_normal + kSegCap - 1) / kSegCap;
+    // chunk cursors start at the chunks' first keys
+    const ull nch = ws.n_chunks;
     if (nch && (e = cudaMemcpyAsync(ws.cur, ws.cko, nch * sizeof(ull), cudaMemcpyDeviceToDevice, s))) return e;
     const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
     seg_coarse_kernel<<<g1, kPT, csm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
@@ -1264,7 +1252,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   }
   const size_t smem = segment_chunk_smem();
   smem_optin((const void*)seg_chunk_kernel, (int)smem);
-  const ull chunks = (ws.n_normal + kSegCap - 1) / kSegCap;
+  const ull chunks = ws.n_chunks;
   if (chunks) {
     if (ws.ev[2] && !n) cudaEventRecord(ws.ev[2], s);
     if (!ws.chunk_ctr && (e = cudaMalloc(&ws.chunk_ctr, sizeof(ull)))) return e;

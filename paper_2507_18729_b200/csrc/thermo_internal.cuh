@@ -180,7 +180,7 @@ struct SegWorkspace {
   ull* gpre = nullptr;       // [groups][3] (NL, BS, BK) at each 64-sector group
   uint16_t* cb = nullptr;    // [groups] coarse bucket of each group
   ull* cstart = nullptr;     // [ncoarse + 1] first key of each coarse bucket
-  ull* cinfo = nullptr;      // [ncoarse + 1][2] normal keys / big sectors before the bucket
+  ull* cinfo = nullptr;      // [ncoarse + 1][3] normal keys / big sectors before the bucket, its first sector
   ull* ccur = nullptr;       // [ncoarse] pass-1 cursors
   ull* tpre = nullptr;       // [ncoarse + 1] first pass-2 tile of each bucket
   uint32_t* tbk = nullptr;   // [pass-2 tiles] bucket of each tile
@@ -191,7 +191,7 @@ struct SegWorkspace {
   ull* boff = nullptr;       // [n big sectors] its first key in `big`
   ull* bcur = nullptr;       // [n big sectors] pass-2 cursors
   ull* bpre = nullptr;       // [2][big_cap] first CTA of each big sector (main, pc passes)
-  ull big_cap = 0, n_bigsec = 0, n_big_keys = 0, n_normal = 0;
+  ull big_cap = 0, n_bigsec = 0, n_big_keys = 0, n_normal = 0, n_chunks = 0;
   ull* chunk_ctr = nullptr;  // persistent chunk kernel: chunks handed out
   // per-kernel timers (created by the caller): before coarse, after coarse,
   // after fine, after chunk, after big; ran[] says which intervals ran
