@@ -227,7 +227,7 @@ static __device__ __noinline__ void instr_flush(uint32_t* s_ikey, ull* s_ival, u
 constexpr int kRingChunks = 8;          // fast kernel: per-warp record ring of 8 x 32 records (4 KB)
 constexpr int kAhead = 6;               // chunks in flight ahead of the current one (cp.async)
 constexpr uint32_t kShortView = 8;      // instructions shorter than this are packed for the general kernel
-constexpr size_t kWarpCache = 10 * 16;  // fast kernel: four window-cache entries (4 x 2 uint4) + pc-id cache (2 uint4)
+constexpr size_t kWarpCache = 12 * 16;  // four window-cache entries (4 x 2 uint4) + pc-id cache (view kernel: 8 sites in 4 uint4)
 constexpr int kDeferBuf = 32;           // fast kernel: deferred-view descriptors staged per warp
 // + 32 words of merge scratch (lane decoder)
 constexpr size_t kOffScratch = kStage * sizeof(ull) + kRingChunks * 32 * 16 + kWarpCache + kDeferBuf * sizeof(ull);

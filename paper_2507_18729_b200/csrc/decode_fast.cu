@@ -64,15 +64,16 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
   // occupancy limit): window entries e = 0..3 as {H, blo, bn, sbase},
   // {tail_s, tail_m, oid, -} at wc[2e], wc[2e + 1] (four: SpMV's col / val / x
   // loads alternate between three objects); site -> pc id cache
-  // {site0, id0, site1, id1} {site2, id2, site3, id3} at wc[8], wc[9]
+  // {site0, id0, site1, id1} ... {site6, id6, site7, id7} at wc[8..11] (the
+  // stencil's six loads and store cycle through six pcs)
   uint4* const wc = ring + kRingChunks * 32;
   if (lane < 4) {
     wc[2 * lane] = make_uint4(0xFFFFFFFFu, 0, 0, 0);
     wc[2 * lane + 1] = make_uint4(1, 0xFFu, 0xFFFFFFFFu, 0);
   }
-  if (lane == 0) wc[8] = wc[9] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
+  if (lane < 4) wc[8 + lane] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
   uint32_t win_rr = 0, pc_rr = 0;  // round-robin replacement (uniform)
-  DeferBuf dq{reinterpret_cast<ull*>(wc + 10), 0};
+  DeferBuf dq{reinterpret_cast<ull*>(wc + 12), 0};
   __syncwarp();
 
   uint32_t lane_mapped = 0, lane_unmapped = 0;  // this lane's word counts for cur_launch
@@ -239,9 +240,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
         }
         uint32_t pcid = 0;
         if (a.track_pc) {
-          // four cached sites (uniform): lane e < 4 tests entry e
+          // eight cached sites (uniform): lane e < 8 tests entry e
           const uint32_t* const pcw = reinterpret_cast<const uint32_t*>(wc + 8);
-          const unsigned ph = __ballot_sync(FULL, (lane < 4) && pcw[2 * (lane & 3)] == w0);
+          const unsigned ph = __ballot_sync(FULL, (lane < 8) && pcw[2 * (lane & 7)] == w0);
           if (ph) {
             pcid = pcw[2 * (__ffs(ph) - 1) + 1];
           } else {
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_kernel(DecodeArgs
               reinterpret_cast<uint32_t*>(wc + 8)[2 * pc_rr] = w0;
               reinterpret_cast<uint32_t*>(wc + 8)[2 * pc_rr + 1] = id;
             }
-            pc_rr = (pc_rr + 1) & 3u;
+            pc_rr = (pc_rr + 1) & 7u;
             __syncwarp();
             pcid = __shfl_sync(FULL, id, 0);
           }

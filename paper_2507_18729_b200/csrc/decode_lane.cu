@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
   }
   if (lane == 0) wc[8] = wc[9] = make_uint4(0xFFFFFFFFu, 0, 0xFFFFFFFFu, 0);
   uint32_t win_rr = 0, pc_rr = 0;  // round-robin replacement (uniform)
-  DeferBuf dq{reinterpret_cast<ull*>(wc + 10), 0};
+  DeferBuf dq{reinterpret_cast<ull*>(wc + 12), 0};
   uint32_t* const scr = reinterpret_cast<uint32_t*>(sm.warp + wib * kWarpRegion + kOffScratch);  // merge scratch
   __syncwarp();
 
