@@ -101,6 +101,20 @@ __device__ __forceinline__ void group_merge(ull prefix, uint32_t& mask, bool& ha
   __syncwarp();
 }
 
+// same with the groups given: grp = the lanes holding a key equal to this
+// lane's (computed by the caller's match, restricted to lanes that have one)
+__device__ __forceinline__ void group_merge_grp(unsigned grp, uint32_t& mask, bool& has, uint32_t* scr, int lane) {
+  if (!__any_sync(FULL, has && grp != (1u << lane))) return;
+  const int ldr = __ffs(grp) - 1;
+  if (has && ldr == lane) scr[lane] = mask;
+  __syncwarp();
+  if (has && ldr != lane) atomicOr(&scr[ldr], mask);
+  __syncwarp();
+  if (has && ldr == lane) mask = scr[lane];
+  has = has && ldr == lane;
+  __syncwarp();
+}
+
 // same on 32-bit sector ids (fast path: launch/warp are uniform)
 // (g < 2^31 where has: the previous lane's g is shuffled as kNoG when it has no key)
 __device__ __forceinline__ void adjacent_merge32(uint32_t g, uint32_t& mask, bool& has, int lane) {

@@ -142,6 +142,13 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
       const uint32_t z0 = __shfl_sync(FULL, z, 0), w0 = __shfl_sync(FULL, w, 0), l0 = __shfl_sync(FULL, l2s, 0);
       const bool one = hb == 1u && __ballot_sync(FULL, act & ((z != z0) | (w != w0) | (l2s != l0))) == 0;
       const bool bcast = one && __ballot_sync(FULL, act & (x != x0)) == 0;
+      // a window of several instructions of one source warp: one match over
+      // (site, sector offset) groups equal keys (the merge: launch, warp and
+      // window are uniform, the site fixes the pc id, the offset the sector)
+      // and equal sectors of an instruction (the statistics); 0 = not taken
+      unsigned grp = 0;
+      if (!one && __ballot_sync(FULL, act & (z != z0)) == 0)
+        grp = __match_any_sync(FULL, act ? (((ull)w << 32) | (x >> 5)) : (0xFFFFFFFF80000000ull | (ull)lane));
       // ---- window interval of each lane's sector (four uniform entries) ----
       uint32_t blo = 0, bn = 0, sbase = 0, tail_s = 1, tail_m = 0xFFu;
       int oid = -1;
@@ -251,6 +258,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
           has = has && lane == 0;  // the run of equal sectors is the whole window
         } else if (one) {
           adjacent_merge32(g, mk, has, lane);  // one instruction: warp, launch and pc are uniform
+        } else if (grp) {
+          group_merge_grp(grp & __ballot_sync(FULL, has), mk, has, scr, lane);
         } else {
           group_merge(pre, mk, has, scr, lane);
         }
@@ -311,7 +320,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, MINB) decode_lane_kernel(Decod
             const uint32_t omn = __shfl_down_sync(FULL, mn, d), omx = __shfl_down_sync(FULL, mx, d);
             if (lane + d < e0) { mn = omn < mn ? omn : mn; mx = omx > mx ? omx : mx; }
           }
-          const unsigned m = __match_any_sync(FULL, act ? (x >> 5) : (0xF8000000u | (uint32_t)lane));
+          // (an instruction's records share the site: grp & segm = its lanes on this sector)
+          const unsigned m = grp ? grp : __match_any_sync(FULL, act ? (x >> 5) : (0xF8000000u | (uint32_t)lane));
           const uint32_t distinct = __popc(__ballot_sync(FULL, act && (__ffs(m & segm) - 1 == lane)) & segm);
           mis = distinct > ((ull)(mx - mn) + 1 + 31) / 32;  // (valid at lane s0: its instruction's values)
         }
