@@ -90,6 +90,19 @@ def test_random_traces(seed, dedup):
         compare(orc, th, t)
 
 
+@pytest.mark.parametrize("n_pcs", [8, 9])
+def test_random_traces_pc_count_boundary(n_pcs):
+    """SEGMENT's per-pc path switches at 8 pc ids in the job (byte masks and a
+    direct bin table up to 8, a second hash set above): both sides, with a
+    launch-filtered rebuild."""
+    t = tg.random_trace(n=40000, seed=11 + n_pcs, n_warps=400, n_launches=1, n_pcs=n_pcs)
+    t.meta["launches"] = 1
+    for lf in (oracle.ALL_LAUNCHES, 0):
+        orc, th = run_both(t, dedup=3, launch_filter=lf)
+        compare(orc, th, t)
+        assert th.stats()["n_pcs"] == n_pcs
+
+
 @pytest.mark.parametrize("dist", ["bimodal", "uniform"])
 @pytest.mark.parametrize("dedup", [1, 2, 3])
 def test_random_hot(dist, dedup):
