@@ -9,8 +9,18 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a tool (nsys) attaches
+
 #include "shard.cuh"
 #include "thermo_internal.cuh"
+
+namespace {
+// one NVTX range per ABI call (SURVEY §5 tracing: nsys timelines per call)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 using namespace thermo;
 
@@ -616,6 +626,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
 }
 
 thermo_status thermo_register_objects(thermo_ctx* ctx, const thermo_object* objs, size_t n) {
+  NvtxRange nvtx_("thermo_register_objects");
   thermo_status st = pre(ctx);
   if (st) return st;
   if (ctx->state != 0) return fail(ctx, THERMO_ESTATE, "objects already registered");
@@ -777,6 +788,7 @@ thermo_status thermo_reset(thermo_ctx* ctx) {
 }
 
 thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, size_t n) {
+  NvtxRange nvtx_("thermo_ingest_trace");
   thermo_status st = pre(ctx);
   if (st) return st;
   if (ctx->state < 1) return fail(ctx, THERMO_ESTATE, "register objects first");
@@ -869,6 +881,7 @@ thermo_status thermo_ingest_trace(thermo_ctx* ctx, const thermo_record* recs, si
 }
 
 thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record* recs, size_t n) {
+  NvtxRange nvtx_("thermo_ingest_warp_trace");
   thermo_status st = pre(ctx);
   if (st) return st;
   if (ctx->state < 1) return fail(ctx, THERMO_ESTATE, "register objects first");
@@ -959,6 +972,7 @@ thermo_status thermo_ingest_warp_trace(thermo_ctx* ctx, const thermo_warp_record
 }
 
 thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32_t launch_filter) {
+  NvtxRange nvtx_("thermo_build_heatmap");
   thermo_status st = pre(ctx);
   if (st) return st;
   // (sharded: a rank may hold an empty slice; build is collective)
@@ -1314,6 +1328,7 @@ thermo_status thermo_query_per_pc(thermo_ctx* ctx, thermo_granularity g, thermo_
 
 thermo_status thermo_classify(thermo_ctx* ctx, const thermo_params* params, thermo_indicators* out, size_t cap,
                               size_t* n_out) {
+  NvtxRange nvtx_("thermo_classify");
   thermo_status st = pre(ctx);
   if (st) return st;
   if (ctx->state != 3) return fail(ctx, THERMO_ESTATE, "build the heat map first");
