@@ -708,10 +708,11 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     }
     distinct += nent;
     __syncthreads();
-    // the chunk owns its sectors: plain stores of the nonzero rows
+    // the chunk owns its sectors: plain stores of every row, zeros included
+    // (the build does not clear the dense rows on this path; a big sector's
+    // row is zero here and its passes add to it afterwards)
     for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
       const uint32_t* cg = cnt + j * 5;
-      if (cg[4] == 0) continue;
       const ull g = s0 + j;
       sc[g] = cg[4];
       uint4 lo, hi;

@@ -998,8 +998,6 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
   cudaStream_t s = ctx->stream;
   CK(cudaEventRecord(ctx->ev0, s));
   const ull l0 = ctx->launches;
-  CK(cudaMemsetAsync(ctx->d_wc, 0, 8 * ctx->S_own * sizeof(uint32_t), s));
-  CK(cudaMemsetAsync(ctx->d_sc, 0, ctx->S_own * sizeof(uint32_t), s));
   CK(cudaMemsetAsync(ctx->d_hist, 0, n * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(ctx->d_pchist, 0, (size_t)ctx->cfg.max_pcs * 2 * kLevels * 8, s));
   CK(cudaMemsetAsync(&ctx->d_ctr->distinct_pairs, 0, 2 * sizeof(ull), s));
@@ -1015,6 +1013,10 @@ thermo_status thermo_build_heatmap(thermo_ctx* ctx, thermo_granularity g, uint32
       mode = THERMO_DEDUP_DENSE;
     else
       mode = ctx->S_own <= (1ull << 30) ? THERMO_DEDUP_SEGMENT : THERMO_DEDUP_HASH;
+  }
+  if (mode != THERMO_DEDUP_SEGMENT) {  // (SEGMENT's chunk kernel writes every row, zeros included)
+    CK(cudaMemsetAsync(ctx->d_wc, 0, 8 * ctx->S_own * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(ctx->d_sc, 0, ctx->S_own * sizeof(uint32_t), s));
   }
   const KeyLayout kl = ctx->kl;
   cudaError_t e = cudaSuccess;
