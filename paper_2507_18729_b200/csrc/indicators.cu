@@ -87,7 +87,7 @@ __device__ ull block_prev_last(ull last_or_none, ull* s_w) {
 // mode 0: sums + votes; mode 1: verify count of gaps == candidate
 __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorArgs a, int mode) {
   __shared__ ull s_w[kIndThreads / 32];
-  __shared__ ull s_red[kIndThreads / 32][12];
+  __shared__ ull s_red[kIndThreads / 32][13];
   const uint32_t tile = blockIdx.x;
   const uint32_t o = (uint32_t)a.tile_obj[tile];
   const ull g0 = a.tile_first[tile], g1 = a.tile_end[tile];
@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
       le1 += x <= P.smem_cap ? 1 : 0;
       if (last != kNone) {
         const ull gap = wl - last;
-        if (mode == 0) vote_add(vt, gap); else verify += gap == cand ? 1 : 0;
+        if (mode == 0) vote_add(vt, gap);
+        verify += gap == (mode == 0 ? 1ull : cand) ? 1 : 0;  // (mode 0: the gaps of 1, exactly)
       } else {
         first = wl;
       }
@@ -180,7 +181,8 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   const ull prev = block_prev_last(last, s_w);
   if (first != kNone && prev != kNone) {
     const ull gap = first - prev;
-    if (mode == 0) vote_add(vt, gap); else verify += gap == cand ? 1 : 0;
+    if (mode == 0) vote_add(vt, gap);
+    verify += gap == (mode == 0 ? 1ull : cand) ? 1 : 0;
   }
   // the tile's first gap (crossing the previous tile) in verify mode
   if (mode == 1 && first != kNone && prev == kNone) {
@@ -210,12 +212,13 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     s2lo = nlo;
   }
   vt = warp_vote(vt);
+  verify = warp_sum(verify);
   const ull tfirst = warp_min(first);
   const ull tlast = warp_max(last == kNone ? 0 : last + 1);
   if (lane == 0) {
     ull* r = s_red[w];
     r[0] = T; r[1] = TW; r[2] = hot; r[3] = fs; r[4] = sumx; r[5] = le1; r[6] = maxsec;
-    r[7] = s2lo; r[8] = s2hi; r[9] = vt.c; r[10] = vt.n; r[11] = tfirst;
+    r[7] = s2lo; r[8] = s2hi; r[9] = vt.c; r[10] = vt.n; r[11] = tfirst; r[12] = verify;
     s_w[w] = tlast;
   }
   __syncthreads();
@@ -223,10 +226,11 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     ull acc[12] = {0};
     acc[11] = kNone;
     Vote bv{0, 0};
-    ull bl = 0;
+    ull bl = 0, ones = 0;
     u128 s2 = 0;
     for (int i = 0; i < kIndThreads / 32; ++i) {
       const ull* r = s_red[i];
+      ones += r[12];
       for (int f = 0; f < 6; ++f) acc[f] += r[f];
       acc[6] = r[6] > acc[6] ? r[6] : acc[6];
       s2 += ((u128)r[8] << 64) | r[7];
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     ti[2] = bv.c;
     ti[3] = bv.n;
     ti[4] = acc[1];
+    ti[5] = ones;
   }
 }
 
@@ -298,9 +303,53 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
   if (threadIdx.x == 0) {
     Vote v{0, 0};
     for (int i = 0; i < 8; ++i) v = vote_merge(v, Vote{s_vc[i], s_vn[i]});
+    s_vc[0] = v.c;
+    s_vn[0] = v.n;
+  }
+  __syncthreads();
+  const ull x = s_vc[0], xn = s_vn[0];
+  // An upper bound on the candidate's gap count, from the tile summaries: a
+  // Boyer-Moore summary (c, n) of N values was formed by cancelling pairs of
+  // different values, so a value v occurs at most (N + n) / 2 times if v == c
+  // and n > 0, else at most (N - n) / 2; each cross-tile gap counts 1 if it
+  // equals the candidate.  When twice the bound is at most the object's gap
+  // count, no gap value can hold a strict majority: the verify scan is
+  // skipped (F_CANDCNT = 0) and no dominant gap is reported, as with the count
+  // A candidate of 1 (every word after the previous one: the contiguous
+  // pattern) needs no verify scan either: the tiles counted their gaps of 1
+  // exactly (tile_info[5]), plus the cross-tile gaps of 1 -- F_VERIFY directly
+  // (rank 0's copy: the sharded mode sums the ranks' verify counts)
+  ull ub = 0, ng = 0, n1 = 0;
+  if (xn) {
+    for (uint32_t t = t0 + threadIdx.x; t < t1; t += 256) {
+      const ull* ti = a.tile_info + (ull)t * kTileInfo;
+      const ull G = ti[4] ? ti[4] - 1 : 0;  // the tile's own gaps (touched words - 1)
+      const ull c = ti[2], n = ti[3];
+      ub += (n && c == x) ? (G + n) / 2 : (G - n) / 2;
+      ng += G;
+      n1 += ti[5];
+      const ull first = ti[0], prev = a.tile_prev[t];
+      if (first != kNone && prev != kNone) {
+        ++ng;
+        ub += first - prev == x ? 1 : 0;
+        n1 += first - prev == 1 ? 1 : 0;
+      }
+    }
+  }
+  ub = warp_sum(ub);
+  ng = warp_sum(ng);
+  n1 = warp_sum(n1);
+  __syncthreads();
+  if (lane == 0) { s_w[w] = ub; s_vn[w] = ng; s_vc[w] = n1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ull U = 0, N = 0, N1 = 0;
+    for (int i = 0; i < 8; ++i) { U += s_w[i]; N += s_vn[i]; N1 += s_vc[i]; }
     ull* ind = a.ind + (ull)o * kIndFields;
-    ind[F_CAND] = v.n ? v.c : 0;
-    ind[F_CANDCNT] = v.n;
+    const bool possible = xn && 2 * U > N;
+    ind[F_CAND] = possible ? x : 0;
+    ind[F_CANDCNT] = possible && x != 1 ? xn : 0;  // 0: no verify scan of this object
+    if (possible && x == 1) ind[F_VERIFY] = a.rank == 0 ? N1 : 0;
   }
 }
 

@@ -260,12 +260,12 @@ struct IndicatorArgs {
   uint32_t max_launches, launch_filter;
   thermo_params prm;
   ull* ind;                  // [n][kIndFields] accumulators
-  ull* tile_info;            // [n_tiles][kTileInfo] first touched, last touched, cand, cnt, touched words
+  ull* tile_info;            // [n_tiles][kTileInfo] first touched, last touched, cand, cnt, touched words, gaps of 1
   ull* tile_prev;            // [n_tiles] last touched word before the tile (or ~0)
   uint32_t rank, nranks;     // sharded mode: tiles of other ranks are skipped
 };
 constexpr int kIndFields = 24;
-constexpr int kTileInfo = 5;
+constexpr int kTileInfo = 6;
 enum IndField {
   F_NWORDS, F_NSECTORS, F_T, F_TW, F_HOT, F_FS, F_SUMX, F_SUMX2_LO, F_SUMX2_HI, F_LE1, F_MAXSEC,
   F_INSTRS, F_MIS, F_GAPS, F_DOMGAP, F_DOMCNT, F_LABELS, F_CAND, F_CANDCNT, F_VERIFY, F_PAD0,
