@@ -90,6 +90,31 @@ def test_random_traces(seed, dedup):
         compare(orc, th, t)
 
 
+def _gap_trace(pattern, n_words, reps):
+    """One warp reads words w of a 4-byte array whenever pattern[w % len] is
+    set, 32 lanes per instruction: the touched words' gaps repeat the
+    pattern's (e.g. 1, 2, 1, 2 ...)."""
+    objects = [(0x500000, 4 * n_words, 0, 0, "gaps")]
+    words = [w for w in range(n_words) if pattern[w % len(pattern)]][:reps]
+    n = (len(words) + 31) // 32 * 32
+    addr = torch.tensor(words + [words[-1]] * (n - len(words)), dtype=torch.int64).reshape(-1, 32) * 4 + 0x500000
+    act = torch.arange(n).reshape(-1, 32) < len(words)
+    rec = tg.from_instructions(addr, act, 0, 0x700, 0, 2)
+    return tg.Trace("gaps", objects, rec, meta=dict(warps=1, launches=1))
+
+
+@pytest.mark.parametrize("pattern,reps", [((1, 1, 0), 20001), ((1, 1, 0), 20000), ((1, 0, 1, 1, 0, 0), 30001),
+                                          ((1,) * 7 + (0,), 50000), ((1, 0, 0), 40000)])
+def test_dominant_gap_majority_boundary(pattern, reps):
+    """The dominant gap needs a strict majority of the gaps: gaps 1, 2
+    alternating (1 holds exactly half, or one more than half), a gap of 1 in
+    3 of 5, gaps of 1 in 6 of 7 (the first pass's exact count of 1-gaps), and
+    all gaps 3 (the verify scan) -- against the oracle on every indicator field."""
+    t = _gap_trace(pattern, 3 * reps, reps)
+    orc, th = run_both(t)
+    compare(orc, th, t)
+
+
 @pytest.mark.parametrize("n_pcs", [8, 9])
 def test_random_traces_pc_count_boundary(n_pcs):
     """SEGMENT's per-pc path switches at 8 pc ids in the job (byte masks and a
