@@ -259,16 +259,17 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
 
 // one block per object: order the object's tiles, add the cross-tile gaps to
 // the vote, merge the tile votes, record each tile's predecessor word
-__global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, const uint32_t* obj_tile0) {
-  __shared__ ull s_w[8];
-  __shared__ ull s_vc[8], s_vn[8];
+constexpr int kStitchT = 1024;  // a block per object walks its tiles in order, 1024 at a time
+__global__ void __launch_bounds__(kStitchT) indicator_stitch_kernel(IndicatorArgs a, const uint32_t* obj_tile0) {
+  __shared__ ull s_w[kStitchT / 32];
+  __shared__ ull s_vc[kStitchT / 32], s_vn[kStitchT / 32];
   __shared__ ull s_carry;
   const uint32_t o = blockIdx.x;
   const uint32_t t0 = obj_tile0[o], t1 = obj_tile0[o + 1];
   if (threadIdx.x == 0) s_carry = kNone;
   __syncthreads();
   Vote vt{0, 0};
-  for (uint32_t base = t0; base < t1; base += 256) {
+  for (uint32_t base = t0; base < t1; base += kStitchT) {
     const uint32_t t = base + threadIdx.x;
     ull first = kNone, last = kNone;
     Vote tv{0, 0};
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
     __syncthreads();
     if (threadIdx.x == 0) {
       ull m = 0;
-      for (int i = 0; i < 8; ++i) m = s_w[i] > m ? s_w[i] : m;
+      for (int i = 0; i < kStitchT / 32; ++i) m = s_w[i] > m ? s_w[i] : m;
       if (m) s_carry = m - 1;
     }
     __syncthreads();
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
   __syncthreads();
   if (threadIdx.x == 0) {
     Vote v{0, 0};
-    for (int i = 0; i < 8; ++i) v = vote_merge(v, Vote{s_vc[i], s_vn[i]});
+    for (int i = 0; i < kStitchT / 32; ++i) v = vote_merge(v, Vote{s_vc[i], s_vn[i]});
     s_vc[0] = v.c;
     s_vn[0] = v.n;
   }
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
   // (rank 0's copy: the sharded mode sums the ranks' verify counts)
   ull ub = 0, ng = 0, n1 = 0;
   if (xn) {
-    for (uint32_t t = t0 + threadIdx.x; t < t1; t += 256) {
+    for (uint32_t t = t0 + threadIdx.x; t < t1; t += kStitchT) {
       const ull* ti = a.tile_info + (ull)t * kTileInfo;
       const ull G = ti[4] ? ti[4] - 1 : 0;  // the tile's own gaps (touched words - 1)
       const ull c = ti[2], n = ti[3];
@@ -344,7 +345,7 @@ __global__ void __launch_bounds__(256) indicator_stitch_kernel(IndicatorArgs a, 
   __syncthreads();
   if (threadIdx.x == 0) {
     ull U = 0, N = 0, N1 = 0;
-    for (int i = 0; i < 8; ++i) { U += s_w[i]; N += s_vn[i]; N1 += s_vc[i]; }
+    for (int i = 0; i < kStitchT / 32; ++i) { U += s_w[i]; N += s_vn[i]; N1 += s_vc[i]; }
     ull* ind = a.ind + (ull)o * kIndFields;
     const bool possible = xn && 2 * U > N;
     ind[F_CAND] = possible ? x : 0;
@@ -436,7 +437,7 @@ void launch_indicator_stitch(const IndicatorArgs& a, cudaStream_t s) {
   // obj_tile0: first tile of each object, derived from tile_obj on the host side
   // and stored right after tile_prev (see thermo_api.cu)
   const uint32_t* obj_tile0 = reinterpret_cast<const uint32_t*>(a.tile_prev + a.n_tiles);
-  indicator_stitch_kernel<<<a.obj.n, 256, 0, s>>>(a, obj_tile0);
+  indicator_stitch_kernel<<<a.obj.n, kStitchT, 0, s>>>(a, obj_tile0);
 }
 
 void launch_indicator_finalize(const IndicatorArgs& a, cudaStream_t s) {
