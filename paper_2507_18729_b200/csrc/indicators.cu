@@ -124,7 +124,23 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
   // no surviving vote: no gap holds a majority, the verify count is not needed
   if (mode == 1 && a.ind[(ull)o * kIndFields + F_CANDCNT] == 0) return;
 
-  ull T = 0, TW = 0, hot = 0, fs = 0, sumx = 0, le1 = 0, maxsec = 0, verify = 0;
+  // Boyer-Moore summaries of the gaps inside one sector, by its touched-word
+  // mask: the gaps between consecutive set bits of m, voted in order (any
+  // pairing summary keeps a strict majority as its candidate, and the later
+  // count / bounds are exact): s_bm[m] = candidate << 4 | count
+  __shared__ uint8_t s_bm[256];
+  {
+    const uint32_t m = threadIdx.x & 255u;
+    uint32_t c = 0, n = 0;
+    for (uint32_t r = m; r & (r - 1); r &= r - 1) {
+      const uint32_t gap = (uint32_t)(__ffs(r & (r - 1)) - __ffs(r));
+      if (n == 0) { c = gap; n = 1; } else if (c == gap) ++n; else --n;
+    }
+    if (threadIdx.x < 256) s_bm[m] = (uint8_t)((c << 4) | n);
+  }
+  __syncthreads();
+  uint32_t T = 0, TW = 0, hot = 0, fs = 0, le1 = 0, maxsec = 0;
+  ull sumx = 0, verify = 0;
   u128 sumx2 = 0;
   Vote vt{0, 0};
   ull first = kNone, last = kNone;
@@ -138,6 +154,7 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
     lo_n = reinterpret_cast<const uint4*>(word_cnt + 8 * gs)[0];
     hi_n = reinterpret_cast<const uint4*>(word_cnt + 8 * gs)[1];
   }
+  const uint32_t smem_cap = (uint32_t)(P.smem_cap < 0xFFFFFFFFull ? P.smem_cap : 0xFFFFFFFFull);
   for (int i = 0; i < kSecPerThread; ++i) {
     const ull g = gs + i;
     if (g >= g1) break;
@@ -149,33 +166,55 @@ __global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorAr
       hi_n = reinterpret_cast<const uint4*>(word_cnt + 8 * (g + 1))[1];
     }
     const uint32_t xs[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    ull mw = 0;
     const ull wl0 = (g - soff) * 8;
+    // the object's words of this sector (its partial last sector, G9)
+    const uint32_t vm = wl0 + 8 <= nw ? 0xFFu : (wl0 >= nw ? 0u : (1u << (uint32_t)(nw - wl0)) - 1u);
+    uint32_t mw = 0, tm = 0, lm = 0;
+    ull s1 = 0;
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-      const ull wl = wl0 + b;
-      if (wl >= nw) break;
-      const uint32_t x = xs[b];
+      const uint32_t x = ((vm >> b) & 1u) ? xs[b] : 0u;
       mw = x > mw ? x : mw;
-      if (x == 0) continue;
-      ++TW;
-      sumx += x;
-      sumx2 += (u128)x * x;
-      le1 += x <= P.smem_cap ? 1 : 0;
-      if (last != kNone) {
-        const ull gap = wl - last;
+      tm |= (x != 0u) << b;
+      lm |= (x != 0u && x <= smem_cap) << b;
+      s1 += x;
+    }
+    if (tm) {
+      TW += __popc(tm);
+      le1 += __popc(lm);
+      sumx += s1;
+      if (mw < (1u << 30)) {  // 8 squares below 2^63: one 64-bit sum per sector
+        ull s2 = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) s2 += ((vm >> b) & 1u) ? (ull)xs[b] * xs[b] : 0ull;
+        sumx2 += s2;
+      } else {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) sumx2 += ((vm >> b) & 1u) ? (u128)((ull)xs[b] * xs[b]) : (u128)0;
+      }
+      const ull wf = wl0 + (uint32_t)(__ffs(tm) - 1);
+      if (last != kNone) {  // the gap from the previous touched word of this thread
+        const ull gap = wf - last;
         if (mode == 0) vote_add(vt, gap);
         verify += gap == (mode == 0 ? 1ull : cand) ? 1 : 0;  // (mode 0: the gaps of 1, exactly)
       } else {
-        first = wl;
+        first = wf;
       }
-      last = wl;
+      if (mode == 0) {  // the gaps inside the sector: their summary, their 1s
+        const uint32_t e = s_bm[tm];
+        if (e & 15u) vt = vote_merge(vt, Vote{(ull)(e >> 4), (ull)(e & 15u)});
+        verify += __popc(tm & (tm >> 1));
+      } else if (cand < 8) {
+        for (uint32_t r = tm; r & (r - 1); r &= r - 1)
+          verify += (ull)(__ffs(r & (r - 1)) - __ffs(r)) == cand ? 1 : 0;
+      }
+      last = wl0 + (uint32_t)(31 - __clz(tm));
     }
     if (c == 0) continue;
     ++T;
     maxsec = c > maxsec ? c : maxsec;
-    if (c >= P.theta_hot && P.alpha_den * c <= P.alpha_num * mw) ++hot;
-    if (P.beta_den * c >= P.beta_num * mw && c >= P.fs_min) ++fs;
+    if (c >= P.theta_hot && P.alpha_den * c <= P.alpha_num * (ull)mw) ++hot;
+    if (P.beta_den * c >= P.beta_num * (ull)mw && c >= P.fs_min) ++fs;
   }
   // gap from the previous touched word in this tile (another thread)
   const ull prev = block_prev_last(last, s_w);
