@@ -147,11 +147,16 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const ull base = (ull)blockIdx.x * kScanBlock + (ull)threadIdx.x * 8;
   uint32_t v[8];
+  if (base + 8 <= n) {  // two 16-byte loads (32-byte aligned)
+    const uint4 a0 = reinterpret_cast<const uint4*>(in + base)[0], a1 = reinterpret_cast<const uint4*>(in + base)[1];
+    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = base + k < n ? in[base + k] : 0u;
+  }
   Sum3 t{0, 0, 0};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const ull j = base + k;
-    v[k] = j < n ? in[j] : 0u;
     const Sum3 q = sum3_of(v[k]);
     t.nl += q.nl; t.bs += q.bs; t.bk += q.bk;
   }
@@ -162,6 +167,7 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
   for (int k = 0; k < w; ++k) { pre.nl += ws[0][k]; pre.bs += ws[1][k]; pre.bk += ws[2][k]; }
   pre.nl += incl.nl - t.nl; pre.bs += incl.bs - t.bs; pre.bk += incl.bk - t.bk;
   uint32_t vprev = (base > 0 && base - 1 < n) ? in[base - 1] : 0u;  // the previous sector's keys
+  uint32_t dd[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const ull j = base + k;
@@ -178,11 +184,11 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
       }
       const bool big = v[k] >= (uint32_t)kSegCap;
       if (big) {
-        dst[j] = 0x80000000u | (uint32_t)pre.bs;
+        dd[k] = 0x80000000u | (uint32_t)pre.bs;
         bg[pre.bs] = j;
         boff[pre.bs] = pre.bk;
       } else {
-        dst[j] = (uint32_t)c;
+        dd[k] = (uint32_t)c;
       }
       if ((j & (kGroup - 1)) == 0) {
         gpre[3 * (j / kGroup)] = pre.nl;
@@ -193,6 +199,14 @@ __global__ void seg_scan_apply(const uint32_t* __restrict__ in, ull n, const ull
     const Sum3 q = sum3_of(v[k]);
     pre.nl += q.nl; pre.bs += q.bs; pre.bk += q.bk;
     vprev = v[k];
+  }
+  if (base + 8 <= n) {
+    reinterpret_cast<uint4*>(dst + base)[0] = make_uint4(dd[0], dd[1], dd[2], dd[3]);
+    reinterpret_cast<uint4*>(dst + base)[1] = make_uint4(dd[4], dd[5], dd[6], dd[7]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (base + k < n) dst[base + k] = dd[k];
   }
 }
 
@@ -922,39 +936,51 @@ __device__ __forceinline__ uint32_t big_table_bits(uint32_t keys_per_pass) {
 
 // passes of every big sector: pre[i] = first CTA of sector i (pre[n] = total);
 // kind 0: main-key passes ceil(K / fill), kind 1: pc passes ceil(min(K, npc) / fill)
-__global__ void seg_big_plan_kernel(const ull* __restrict__ boff, const ull* __restrict__ tot, ull npc,
-                                    ull* __restrict__ pre_main, ull* __restrict__ pre_pc) {
-  __shared__ ull carry[2];
-  __shared__ ull wsum[2][kSegWarps];
+constexpr int kPlanT = 1024;  // seg_big_plan_kernel threads: each scans a contiguous run of big sectors
+__global__ void __launch_bounds__(kPlanT) seg_big_plan_kernel(const ull* __restrict__ boff, const ull* __restrict__ tot,
+                                                              ull npc, ull* __restrict__ pre_main,
+                                                              ull* __restrict__ pre_pc) {
+  __shared__ ull ws[2][kPlanT / 32];
   const ull nbs = tot[1];
-  if (threadIdx.x < 2) carry[threadIdx.x] = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (ull b0 = 0; b0 < nbs; b0 += kSegThreads) {
-    const ull i = b0 + threadIdx.x;
-    ull v0 = 0, v1 = 0;
-    if (i < nbs) {
-      const ull K = (i + 1 < nbs ? boff[i + 1] : tot[2]) - boff[i];
-      v0 = (K + kBigFill - 1) / kBigFill;
-      const ull kp = K < npc ? K : npc;
-      // one-pass sectors bin their pc ids in the main kernel (counts final there)
-      v1 = v0 == 1 ? 0 : (kp + kBigFill - 1) / kBigFill;
-    }
-    ull i0 = v0, i1 = v1;
-    for (int d = 1; d < 32; d <<= 1) {
-      const ull a = __shfl_up_sync(GFULL, i0, d), b = __shfl_up_sync(GFULL, i1, d);
-      if (lane >= d) { i0 += a; i1 += b; }
-    }
-    if (lane == 31) { wsum[0][w] = i0; wsum[1][w] = i1; }
-    __syncthreads();
-    ull p0 = carry[0], p1 = carry[1];
-    for (int k = 0; k < w; ++k) { p0 += wsum[0][k]; p1 += wsum[1][k]; }
-    if (i < nbs) { pre_main[i] = p0 + i0 - v0; pre_pc[i] = p1 + i1 - v1; }
-    __syncthreads();
-    if (threadIdx.x == kSegThreads - 1) { carry[0] = p0 + i0; carry[1] = p1 + i1; }
-    __syncthreads();
+  const ull per = (nbs + kPlanT - 1) / kPlanT;
+  const ull i0 = (ull)threadIdx.x * per, i1 = i0 + per < nbs ? i0 + per : nbs;
+  auto passes = [&](ull i, ull& v0, ull& v1) {
+    const ull K = (i + 1 < nbs ? boff[i + 1] : tot[2]) - boff[i];
+    v0 = (K + kBigFill - 1) / kBigFill;
+    const ull kp = K < npc ? K : npc;
+    // one-pass sectors bin their pc ids in the main kernel (counts final there)
+    v1 = v0 == 1 ? 0 : (kp + kBigFill - 1) / kBigFill;
+  };
+  ull t0 = 0, t1 = 0;
+  for (ull i = i0; i < i1; ++i) {
+    ull v0, v1;
+    passes(i, v0, v1);
+    t0 += v0;
+    t1 += v1;
   }
-  if (threadIdx.x == 0) { pre_main[nbs] = carry[0]; pre_pc[nbs] = carry[1]; }
+  ull c0 = t0, c1 = t1;  // inclusive warp scans
+  for (int d = 1; d < 32; d <<= 1) {
+    const ull a0 = __shfl_up_sync(GFULL, c0, d), a1 = __shfl_up_sync(GFULL, c1, d);
+    if (lane >= d) { c0 += a0; c1 += a1; }
+  }
+  if (lane == 31) { ws[0][w] = c0; ws[1][w] = c1; }
+  __syncthreads();
+  ull p0 = c0 - t0, p1 = c1 - t1, all0 = 0, all1 = 0;
+  for (int k = 0; k < kPlanT / 32; ++k) {
+    if (k < w) { p0 += ws[0][k]; p1 += ws[1][k]; }
+    all0 += ws[0][k];
+    all1 += ws[1][k];
+  }
+  for (ull i = i0; i < i1; ++i) {
+    ull v0, v1;
+    passes(i, v0, v1);
+    pre_main[i] = p0;
+    pre_pc[i] = p1;
+    p0 += v0;
+    p1 += v1;
+  }
+  if (threadIdx.x == 0) { pre_main[nbs] = all0; pre_pc[nbs] = all1; }
 }
 
 // CTA t -> (big sector i, pass p): pre[i] <= t < pre[i + 1]
@@ -1271,7 +1297,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
   if (ws.n_bigsec) {
     const ull* tot = reinterpret_cast<ull*>(ws.maxc) + 1;
     const ull npc = pc_hist ? (1ull << kl.P) : 0ull;
-    seg_big_plan_kernel<<<1, kSegThreads, 0, s>>>(ws.boff, tot, npc, ws.bpre, ws.bpre + ws.big_cap);
+    seg_big_plan_kernel<<<1, kPlanT, 0, s>>>(ws.boff, tot, npc, ws.bpre, ws.bpre + ws.big_cap);
     // CTAs: at most one per kBigFill keys plus one per sector
     const ull grid = ws.n_big_keys / kBigFill + ws.n_bigsec + 1;
     const size_t bsm = ((size_t)kBigSlots + kSegWarps * kBigWBuf) * sizeof(ull);
