@@ -11,4 +11,5 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/e
 timeout 900 python bench.py --workload sgemm --only --format warp --no-cpu-baseline > gpurun_out/ev_bench_warp.json 2> gpurun_out/ev_bench_warp.err; echo rc=$?
 W=spmv bash scripts/gpu_r2_ncu_decode.sh
 W=spmv bash scripts/gpu_r2_ncu_count.sh
+W=sgemm bash scripts/gpu_r2_ncu_view.sh
 for P in 1 2 4 8; do timeout 900 python bench.py --workload synthetic --local-shards $P --steps 2 --warmup 1 > gpurun_out/ev_shards_P$P.json 2> gpurun_out/ev_shards_P$P.err; echo rc=$?; done
