@@ -842,8 +842,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
 // the sector's distinct pc ids (split the same way) and bins them at the
 // sector's and words' levels (G11).  All CTAs run in parallel: a CTA re-reads
 // its sector's keys (L2-resident) instead of one CTA looping over P passes.
-constexpr int kBigSlots = 8192;          // 64 KB table
-constexpr uint32_t kBigFill = 6144;      // keys per pass (load <= 3/4)
+constexpr int kBigSlots = 4096;          // 32 KB table
+constexpr uint32_t kBigFill = 3072;      // keys per pass (load <= 3/4)
 __device__ __forceinline__ uint32_t big_pass_of(ull id, uint32_t P) {
   return P <= 1 ? 0u : __umulhi((uint32_t)((id * 0xD6E8FEB86659FD93ull) >> 32), P);
 }
