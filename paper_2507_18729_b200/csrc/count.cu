@@ -184,13 +184,15 @@ __device__ __forceinline__ uint32_t obj_of_sector(const ull* soff, uint32_t n, u
   return lo;
 }
 
-__device__ __forceinline__ void agg_add(uint32_t* s_hist, ull* g_hist, bool use_smem, uint32_t bin, bool has) {
+// w: every lane of the call adds w to its bin
+__device__ __forceinline__ void agg_add(uint32_t* s_hist, ull* g_hist, bool use_smem, uint32_t bin, bool has,
+                                        uint32_t w = 1u) {
   const uint32_t key = has ? bin : 0xFFFFFFFFu;
   const unsigned m = __match_any_sync(CFULL, key);
   const int lane = threadIdx.x & 31;
   if (has && (__ffs(m) - 1) == lane) {
-    if (use_smem) atomicAdd(&s_hist[bin], (uint32_t)__popc(m));
-    else atomicAdd(&g_hist[bin], (ull)__popc(m));
+    if (use_smem) atomicAdd(&s_hist[bin], w * (uint32_t)__popc(m));
+    else atomicAdd(&g_hist[bin], (ull)w * __popc(m));
   }
 }
 
@@ -242,10 +244,19 @@ __global__ void __launch_bounds__(256) object_hist_kernel(const uint32_t* __rest
     const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     // bins aggregated over the warp's lanes (match_any), one atomic per distinct bin
     agg_add(s_hist, hist, use_smem, (o * 2 + 1) * kLevels + (in ? level_of(c) : 0), in);
+    // a sector whose 8 words (all the object's) share one level adds 8 to one
+    // bin: one aggregation for those lanes instead of eight
+    const uint32_t lw0 = level_of(x[0]);
+    bool same8 = in && wl0 + 8 <= nwo;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const bool hw = in && wl0 + b < nwo;
-      agg_add(s_hist, hist, use_smem, (o * 2) * kLevels + (hw ? level_of(x[b]) : 0), hw);
+    for (int b = 1; b < 8; ++b) same8 = same8 && level_of(x[b]) == lw0;
+    agg_add(s_hist, hist, use_smem, (o * 2) * kLevels + (same8 ? lw0 : 0), same8, 8u);
+    if (__any_sync(CFULL, in && !same8)) {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const bool hw = in && !same8 && wl0 + b < nwo;
+        agg_add(s_hist, hist, use_smem, (o * 2) * kLevels + (hw ? level_of(x[b]) : 0), hw);
+      }
     }
   }
   if (use_smem) {
