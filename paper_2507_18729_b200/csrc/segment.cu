@@ -605,41 +605,6 @@ __device__ __forceinline__ void chunk_insert_regs(ull* tab, uint16_t* list, uint
   }
 }
 
-// one insert pass over the chunk's keys seg[k0, k0 + nk): id = (sector - s0) <<
-// A | (key >> B) & M, mask = the key's low 8 bits.  Each warp takes 32 x kIns
-// consecutive keys per iteration, all loads in flight before the inserts
-constexpr int kIns = 4;
-__device__ __forceinline__ void chunk_insert_pass(ull* tab, uint16_t* list, uint32_t* nlist, const ull* __restrict__ seg,
-                                                  ull k0, uint32_t nk, ull s0, const KeyLayout& kl, uint32_t filter,
-                                                  uint32_t A, uint32_t B, ull M) {
-  const int lane = threadIdx.x & 31;
-  unsigned lt;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
-  for (uint32_t wb = (threadIdx.x >> 5) * 32u * kIns; wb < nk; wb += (uint32_t)kSegThreads * kIns) {
-    ull kk[kIns];
-#pragma unroll
-    for (int u = 0; u < kIns; ++u) {
-      const uint32_t i = wb + u * 32u + lane;
-      kk[u] = i < nk ? seg[k0 + i] : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < kIns; ++u) {
-      const ull k = kk[u];
-      bool ok = wb + u * 32u + lane < nk;
-      if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
-      uint32_t slot = 0;
-      const bool nw = ok && hset_or(tab, ((key_g(k, kl) - s0) << A) | ((k >> B) & M), (uint32_t)k & 0xFFu, slot);
-      const unsigned b = __ballot_sync(GFULL, nw);
-      if (b) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(nlist, (uint32_t)__popc(b));
-        base = __shfl_sync(GFULL, base, 0);
-        if (nw) list[base + __popc(b & lt)] = (uint16_t)slot;
-      }
-    }
-  }
-}
-
 // chunk c owns the sectors [cs0[c], cs0[c + 1]) (at most kChunkSec); their
 // keys are seg[cko[c], cko[c + 1]), fewer than 2 kSegCap.  (a) distinct
 // (sector, launch, warp) with OR-ed masks in a shared-memory hash set ->
