@@ -568,6 +568,30 @@ __device__ __forceinline__ bool hset_or(ull* tab, ull id, uint32_t m, uint32_t& 
   }
 }
 
+// the same insert reporting what it added (the pass-(a) counts form as the
+// entries do): 0x100 | m for a new entry (*slot), else the mask bits the
+// entry gained (exact: bits only accumulate; the OR returns the old mask)
+__device__ __forceinline__ uint32_t hset_or_new(ull* tab, ull id, uint32_t m, uint32_t& slot) {
+  const uint32_t hx = (uint32_t)((id * 0x9E3779B97F4A7C15ull) >> 32);
+  uint32_t h = __umulhi(hx, (uint32_t)kHSlots);
+  const ull v = (id << 8) | m;
+  for (;;) {
+    ull cur = tab[h];
+    if (cur == kHEmpty) {
+      cur = atomicCAS(&tab[h], kHEmpty, v);
+      if (cur == kHEmpty) {
+        slot = h;
+        return 0x100u | m;
+      }
+    }
+    if ((cur >> 8) == id) {
+      if (((uint32_t)cur & m) == m) return 0u;
+      return m & ~atomicOr(reinterpret_cast<uint32_t*>(&tab[h]), m);
+    }
+    h = h + 1 == (uint32_t)kHSlots ? 0u : h + 1;
+  }
+}
+
 // the chunk's keys, held in registers for both insert passes: thread t holds
 // keys t, t + 256, ... (a chunk holds < 2 kSegCap = 16 x 256 keys)
 constexpr int kKPT = 2 * kSegCap / kSegThreads;
@@ -595,6 +619,47 @@ __device__ __forceinline__ void chunk_insert_regs(ull* tab, uint16_t* list, uint
     if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
     uint32_t slot = 0;
     const bool nw = ok && hset_or(tab, ((key_g(k, kl) - s0) << A) | ((k >> B) & M), (uint32_t)k & 0xFFu, slot);
+    const unsigned b = __ballot_sync(GFULL, nw);
+    if (b) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(nlist, (uint32_t)__popc(b));
+      base = __shfl_sync(GFULL, base, 0);
+      if (nw) list[base + __popc(b & lt)] = (uint16_t)slot;
+    }
+  }
+}
+
+// pass (a) over the chunk's keys kk: id = (sector - s0) << LW | (launch, warp),
+// OR-ed masks; each insert adds what it created to the sector's counters in
+// cnt ([sector][5]: words (2b, 2b+1) as u16 pairs, the sector count): a new
+// entry is a new warp of the sector, each bit it gains a new (warp, word)
+// (P:328 flush); new slots appended to `list` (for clearing)
+__device__ __forceinline__ void chunk_insert_count(ull* tab, uint16_t* list, uint32_t* nlist, const ull (&kk)[kKPT],
+                                                   uint32_t nk, ull s0, const KeyLayout& kl, uint32_t filter,
+                                                   uint32_t LW, uint32_t RS, ull M, uint32_t* cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;  // (uniform)
+#pragma unroll
+  for (int j = 0; j < kKPT; ++j) {
+    if ((uint32_t)j >= jmax) break;
+    const ull k = kk[j];
+    bool ok = j * kSegThreads + threadIdx.x < nk;
+    if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
+    uint32_t slot = 0, r = 0;
+    if (ok) {
+      const uint32_t gl = (uint32_t)(key_g(k, kl) - s0);
+      r = hset_or_new(tab, ((ull)gl << LW) | ((k >> RS) & M), (uint32_t)k & 0xFFu, slot);
+      uint32_t* cg = cnt + gl * 5;
+      if (r & 0x100u) atomicAdd(&cg[4], 1u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t add = ((r >> (2 * q)) & 1u) | (((r >> (2 * q + 1)) & 1u) << 16);
+        if (add) atomicAdd(&cg[q], add);
+      }
+    }
+    const bool nw = (r & 0x100u) != 0;
     const unsigned b = __ballot_sync(GFULL, nw);
     if (b) {
       uint32_t base = 0;
@@ -664,27 +729,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     // ---- (a) distinct (sector, launch, warp) ----
     ull kk[kKPT];
     chunk_load(kk, seg, k0, nk);
-    chunk_insert_regs(tab, list, &s_n[0], kk, nk, s0, kl, filter, LW, RS, lwmask);
+    chunk_insert_count(tab, list, &s_n[0], kk, nk, s0, kl, filter, LW, RS, lwmask, cnt);
     __syncthreads();
     const uint32_t nent = s_n[0];
-    for (uint32_t base = threadIdx.x & ~31u; base < nent; base += kSegThreads) {  // warp-uniform trip count
-      const uint32_t i = base + lane;
-      const bool occ = i < nent;
-      const ull v = occ ? tab[list[i]] : kHEmpty;
-      const uint32_t gl = occ ? (uint32_t)(v >> (8 + LW)) : 0xFFFFFFFFu;
-      const uint32_t m = occ ? (uint32_t)v & 0xFFu : 0u;
-      const unsigned peers = __match_any_sync(GFULL, gl);
-      uint32_t cb[8];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) cb[b] = __popc(__ballot_sync(GFULL, (m >> b) & 1u) & peers);
-      if (occ && lane == __ffs(peers) - 1) {
-        uint32_t* cg = cnt + gl * 5;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (cb[2 * j] | cb[2 * j + 1]) atomicAdd(&cg[j], cb[2 * j] | (cb[2 * j + 1] << 16));
-        atomicAdd(&cg[4], (uint32_t)__popc(peers));
-      }
-    }
     distinct += nent;
     __syncthreads();
     // the chunk owns its sectors: plain stores of every row, zeros included
