@@ -1016,10 +1016,12 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
                                                              uint32_t filter, uint32_t* __restrict__ wc,
                                                              uint32_t* __restrict__ sc,
                                                              const uint32_t* __restrict__ site_of,
-                                                             ull* __restrict__ pc_hist, DevCounters* ctr) {
+                                                             ull* __restrict__ pc_hist, DevCounters* ctr,
+                                                             uint32_t few_pcs, uint32_t* __restrict__ bpcm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ull* tab = reinterpret_cast<ull*>(smem_raw);  // [kBigSlots], then [warps][kBigWBuf] compaction buffers
   __shared__ uint32_t s_cnt[9];
+  __shared__ uint32_t s_pcm[2];  // few_pcs: the pass's (pc, word) bytes (pc q: byte q)
   const ull nbs = tot[1];
   ull i;
   uint32_t p, P;
@@ -1030,14 +1032,22 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
   const uint32_t LW = kl.L + kl.W, RS = 8 + kl.P;
   const ull lwmask = (1ull << LW) - 1;
   if (threadIdx.x < 9) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 2) s_pcm[threadIdx.x] = 0;
   const uint32_t tb = big_table_bits((K + P - 1) / P + 64);
+  // few_pcs: each key ORs its word mask into its pc's byte of a register
+  // (pc ids < 8), so the per-pc facts need no second pass over the keys
+  ull pm = 0;
   const int T = 1 << tb;
   for (int j = threadIdx.x; j < T; j += kSegThreads) tab[j] = kHEmpty;
   __syncthreads();
+  auto insert = [&](ull k) {
+    if (!big_or(tab, tb, (k >> RS) & lwmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+    if (few_pcs) pm |= (ull)((uint32_t)k & 0xFFu) << (8 * ((uint32_t)(k >> 8) & 7u));
+  };
   if (P == 1) {
     big_for_keys(big, b0, K, [&](ull k) {
       if (filter != THERMO_ALL_LAUNCHES && key_launch(k, kl) != filter) return;
-      if (!big_or(tab, tb, (k >> RS) & lwmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
+      insert(k);
     });
   } else {
     big_for_kept(
@@ -1046,9 +1056,14 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
           return (filter == THERMO_ALL_LAUNCHES || key_launch(k, kl) == filter) &&
                  big_pass_of((k >> RS) & lwmask, P) == p;
         },
-        [&](ull k) {
-          if (!big_or(tab, tb, (k >> RS) & lwmask, (uint32_t)k & 0xFFu)) atomicAdd(&ctr->hash_fail, 1ull);
-        });
+        insert);
+  }
+  if (few_pcs) {
+    for (int d = 16; d; d >>= 1) pm |= __shfl_xor_sync(GFULL, pm, d);
+    if ((threadIdx.x & 31) == 0 && pm) {
+      atomicOr(&s_pcm[0], (uint32_t)pm);
+      atomicOr(&s_pcm[1], (uint32_t)(pm >> 32));
+    }
   }
   __syncthreads();
   uint32_t cw[8] = {0, 0, 0, 0, 0, 0, 0, 0}, cs = 0;
@@ -1074,6 +1089,25 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_kernel(const ull* __restr
     // several passes of one sector add up (the dense arrays start at 0)
     atomicAdd(threadIdx.x == 8 ? &sc[g] : &wc[8 * g + threadIdx.x], s_cnt[threadIdx.x]);
     if (threadIdx.x == 8) atomicAdd(&ctr->distinct_pairs, (ull)s_cnt[8]);
+  }
+  if (few_pcs) {
+    // the (pc, word) bytes: binned here for a one-pass sector (its counts are
+    // final), OR-ed into the sector's slot for several passes (binned by
+    // seg_big_pcbin_kernel once every pass has added its counts)
+    if (P != 1) {
+      if (threadIdx.x < 2 && s_pcm[threadIdx.x]) atomicOr(&bpcm[2 * i + threadIdx.x], s_pcm[threadIdx.x]);
+      return;
+    }
+    if (threadIdx.x < 8) {
+      const uint32_t q = threadIdx.x, m = (s_pcm[q >> 2] >> (8 * (q & 3))) & 0xFFu;
+      if (m) {
+        atomicAdd(&pc_hist[(q * 2 + 1) * kLevels + level_of_g(s_cnt[8])], 1ull);
+        for (uint32_t r = m; r; r &= r - 1)
+          atomicAdd(&pc_hist[(q * 2) * kLevels + level_of_g(s_cnt[__ffs(r) - 1])], 1ull);
+        atomicAdd(&ctr->distinct_pc, 1ull);
+      }
+    }
+    return;
   }
   if (P != 1 || !pc_hist || !kl.P) return;
   // ---- one-pass sector: its counts are final here, so its distinct pc ids
@@ -1160,6 +1194,32 @@ __global__ void __launch_bounds__(kSegThreads) seg_big_pc_kernel(const ull* __re
   if ((threadIdx.x & 31) == 0 && npc) atomicAdd(&ctr->distinct_pc, (ull)npc);
 }
 
+// few_pcs, big sectors of several passes: their (pc, word) bytes against the
+// final counts (one thread per big sector)
+__global__ void seg_big_pcbin_kernel(const ull* __restrict__ pre, const ull* __restrict__ bg,
+                                     const ull* __restrict__ tot, const uint32_t* __restrict__ bpcm,
+                                     const uint32_t* __restrict__ wc, const uint32_t* __restrict__ sc,
+                                     ull* __restrict__ pc_hist, DevCounters* ctr) {
+  const ull i = (ull)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tot[1] || pre[i + 1] - pre[i] <= 1) return;
+  const ull g = bg[i];
+  const uint32_t p0 = bpcm[2 * i], p1 = bpcm[2 * i + 1];
+  if ((p0 | p1) == 0) return;
+  uint32_t w[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) w[b] = wc[8 * g + b];
+  const uint32_t ls = level_of_g(sc[g]);
+  ull npc = 0;
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t m = ((q < 4 ? p0 : p1) >> (8 * (q & 3))) & 0xFFu;
+    if (!m) continue;
+    ++npc;
+    atomicAdd(&pc_hist[(q * 2 + 1) * kLevels + ls], 1ull);
+    for (uint32_t r = m; r; r &= r - 1) atomicAdd(&pc_hist[(q * 2) * kLevels + level_of_g(w[__ffs(r) - 1])], 1ull);
+  }
+  atomicAdd(&ctr->distinct_pc, npc);
+}
+
 static size_t segment_chunk_smem() {
   return (size_t)kHSlots * sizeof(ull) + ((size_t)kHWin * 5 + 2 * kPcBins) * sizeof(uint32_t) +
          2 * kSegCap * sizeof(uint16_t);
@@ -1214,13 +1274,15 @@ cudaError_t segment_prepare(const ull* keys, ull n, KeyLayout kl, ull nsec, SegW
   // the sectors holding >= kSegCap of the n keys
   const ull nbig_cap = std::min<ull>(nsec, n / kSegCap) + 2;
   if (ws.big_cap < nbig_cap) {
-    cudaFree(ws.bg); cudaFree(ws.boff); cudaFree(ws.bcur); cudaFree(ws.bpre);
+    cudaFree(ws.bg); cudaFree(ws.boff); cudaFree(ws.bcur); cudaFree(ws.bpre); cudaFree(ws.bpcm);
     ws.bg = ws.boff = ws.bcur = ws.bpre = nullptr;
+    ws.bpcm = nullptr;
     ws.big_cap = 0;
     if ((e = cudaMalloc(&ws.bg, nbig_cap * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.boff, nbig_cap * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.bcur, nbig_cap * sizeof(ull)))) return e;
     if ((e = cudaMalloc(&ws.bpre, 2 * nbig_cap * sizeof(ull)))) return e;
+    if ((e = cudaMalloc(&ws.bpcm, 2 * nbig_cap * sizeof(uint32_t)))) return e;
     ws.big_cap = nbig_cap;
   }
   const ull ngroups = (nsec + kGroup - 1) / kGroup;
@@ -1315,10 +1377,16 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     const size_t bsm = ((size_t)kBigSlots + kSegWarps * kBigWBuf) * sizeof(ull);
     smem_optin((const void*)seg_big_kernel, (int)bsm);
     smem_optin((const void*)seg_big_pc_kernel, (int)bsm);
+    const uint32_t few = pc_hist && kl.P && n_pc <= kFewPcs ? 1u : 0u;
+    if (few) cudaMemsetAsync(ws.bpcm, 0, 2 * ws.n_bigsec * sizeof(uint32_t), s);
     seg_big_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre, kl, filter, wc, sc,
-                                                             site_of, pc_hist, ctr);
+                                                             site_of, pc_hist, ctr, few, ws.bpcm);
     ws.launches += 2;
-    if (pc_hist && kl.P) {
+    if (few) {
+      seg_big_pcbin_kernel<<<(unsigned)((ws.n_bigsec + 255) / 256), 256, 0, s>>>(ws.bpre, ws.bg, tot, ws.bpcm, wc, sc,
+                                                                                pc_hist, ctr);
+      ws.launches += 1;
+    } else if (pc_hist && kl.P) {
       seg_big_pc_kernel<<<(unsigned)grid, kSegThreads, bsm, s>>>(big, ws.boff, ws.bg, tot, ws.bpre + ws.big_cap,
                                                                   kl, filter, wc, sc, site_of, pc_hist, ctr);
       ws.launches += 1;

@@ -599,7 +599,7 @@ thermo_status thermo_destroy(thermo_ctx* ctx) {
                   ctx->swpc.alt, ctx->swpc.status, ctx->swpc.hist, ctx->swpc.counters, ctx->seg.cnt, ctx->seg.cko, ctx->seg.cur,
                   ctx->seg.bsum, ctx->seg.maxc, ctx->seg.cs0, ctx->seg.dst, ctx->seg.gpre, ctx->seg.cb,
                   ctx->seg.cstart, ctx->seg.cinfo, ctx->seg.ccur, ctx->seg.tpre, ctx->seg.tbk, ctx->seg.tmp, ctx->seg.bg,
-                  ctx->seg.boff, ctx->seg.bcur, ctx->seg.bpre, ctx->seg.chunk_ctr, ctx->d_stage[0],
+                  ctx->seg.boff, ctx->seg.bcur, ctx->seg.bpre, ctx->seg.bpcm, ctx->seg.chunk_ctr, ctx->d_stage[0],
                   ctx->d_stage[1], ctx->d_pcmap, ctx->d_site_glob, ctx->d_tmp, ctx->d_red, ctx->d_instr_g,
                   ctx->d_launch_g, ctx->d_acc, ctx->d_spill, ctx->d_wctr, ctx->d_wstage[0], ctx->d_wstage[1]};
   for (void* b : bufs) dfree(b);

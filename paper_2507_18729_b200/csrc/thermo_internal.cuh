@@ -191,6 +191,7 @@ struct SegWorkspace {
   ull* boff = nullptr;       // [n big sectors] its first key in `big`
   ull* bcur = nullptr;       // [n big sectors] pass-2 cursors
   ull* bpre = nullptr;       // [2][big_cap] first CTA of each big sector (main, pc passes)
+  uint32_t* bpcm = nullptr;  // [big_cap][2] <= 8 pc ids: each big sector's (pc, word) bytes, OR-ed by its passes
   ull big_cap = 0, n_bigsec = 0, n_big_keys = 0, n_normal = 0, n_chunks = 0;
   ull* chunk_ctr = nullptr;  // persistent chunk kernel: chunks handed out
   // per-kernel timers (created by the caller): before coarse, after coarse,
