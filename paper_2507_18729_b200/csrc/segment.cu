@@ -633,14 +633,12 @@ __device__ __forceinline__ void chunk_insert_regs(ull* tab, uint16_t* list, uint
 // OR-ed masks; each insert adds what it created to the sector's counters in
 // cnt ([sector][5]: words (2b, 2b+1) as u16 pairs, the sector count): a new
 // entry is a new warp of the sector, each bit it gains a new (warp, word)
-// (P:328 flush); new slots appended to `list` (for clearing)
-__device__ __forceinline__ void chunk_insert_count(ull* tab, uint16_t* list, uint32_t* nlist, const ull (&kk)[kKPT],
-                                                   uint32_t nk, ull s0, const KeyLayout& kl, uint32_t filter,
-                                                   uint32_t LW, uint32_t RS, ull M, uint32_t* cnt) {
-  const int lane = threadIdx.x & 31;
-  unsigned lt;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+// (P:328 flush); returns the entries this thread created
+__device__ __forceinline__ uint32_t chunk_insert_count(ull* tab, const ull (&kk)[kKPT], uint32_t nk, ull s0,
+                                                       const KeyLayout& kl, uint32_t filter, uint32_t LW, uint32_t RS,
+                                                       ull M, uint32_t* cnt) {
   const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;  // (uniform)
+  uint32_t fresh = 0;  // entries this thread created
 #pragma unroll
   for (int j = 0; j < kKPT; ++j) {
     if ((uint32_t)j >= jmax) break;
@@ -659,15 +657,9 @@ __device__ __forceinline__ void chunk_insert_count(ull* tab, uint16_t* list, uin
         if (add) atomicAdd(&cg[q], add);
       }
     }
-    const bool nw = (r & 0x100u) != 0;
-    const unsigned b = __ballot_sync(GFULL, nw);
-    if (b) {
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(nlist, (uint32_t)__popc(b));
-      base = __shfl_sync(GFULL, base, 0);
-      if (nw) list[base + __popc(b & lt)] = (uint16_t)slot;
-    }
+    fresh += (r >> 8) & 1u;
   }
+  return fresh;
 }
 
 // chunk c owns the sectors [cs0[c], cs0[c + 1]) (at most kChunkSec); their
@@ -709,7 +701,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
   } else {
     for (int i = threadIdx.x; i < kPcBins; i += kSegThreads) { tbin[i] = 0xFFFFFFFFu; tcnt[i] = 0; }
   }
-  ull distinct = 0, distinct_pc = 0;  // thread 0's running totals
+  ull distinct = 0, distinct_pc = 0;  // this thread's running totals (distinct_pc: thread 0's on the hashed path)
   for (;;) {
     __syncthreads();  // the previous chunk is done with s_c, s_n and its table slots
     if (threadIdx.x == 0) {
@@ -729,10 +721,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     // ---- (a) distinct (sector, launch, warp) ----
     ull kk[kKPT];
     chunk_load(kk, seg, k0, nk);
-    chunk_insert_count(tab, list, &s_n[0], kk, nk, s0, kl, filter, LW, RS, lwmask, cnt);
+    distinct += chunk_insert_count(tab, kk, nk, s0, kl, filter, LW, RS, lwmask, cnt);
     __syncthreads();
-    const uint32_t nent = s_n[0];
-    distinct += nent;
     __syncthreads();
     // the chunk owns its sectors: plain stores of every row, zeros included
     // (the build does not clear the dense rows on this path; a big sector's
@@ -747,7 +737,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
       reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
       reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
     }
-    for (uint32_t i = threadIdx.x; i < nent; i += kSegThreads) tab[list[i]] = kHEmpty;  // only the used slots
+    for (uint32_t i = threadIdx.x; i < (uint32_t)kHSlots; i += kSegThreads) tab[i] = kHEmpty;  // (a)'s entries
     if (!pc_hist) continue;  // (uniform)
     __syncthreads();
     if (few_pcs) {
@@ -826,7 +816,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < npc; i += kSegThreads) tab[list[i]] = kHEmpty;
   }
-  if (threadIdx.x == 0 && distinct) atomicAdd(&ctr->distinct_pairs, distinct);
+  for (int d = 16; d; d >>= 1) distinct += __shfl_xor_sync(GFULL, distinct, d);
+  if (lane == 0 && distinct) atomicAdd(&ctr->distinct_pairs, distinct);
   for (int d = 16; d; d >>= 1) distinct_pc += __shfl_xor_sync(GFULL, distinct_pc, d);
   if (lane == 0 && distinct_pc) atomicAdd(&ctr->distinct_pc, distinct_pc);
   if (pc_hist) {
