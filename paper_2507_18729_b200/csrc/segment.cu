@@ -737,16 +737,17 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
       reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
       reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
     }
-    for (uint32_t i = threadIdx.x; i < (uint32_t)kHSlots; i += kSegThreads) tab[i] = kHEmpty;  // (a)'s entries
+    // (a)'s entries cleared; with few pc ids the first win slots become the
+    // zeroed (sector, pc) byte masks of (b') at the same time
+    const uint32_t pcz = (few_pcs && pc_hist) ? (uint32_t)win : 0u;
+    for (uint32_t i = threadIdx.x; i < (uint32_t)kHSlots; i += kSegThreads) tab[i] = i < pcz ? 0ull : kHEmpty;
     if (!pc_hist) continue;  // (uniform)
     __syncthreads();
     if (few_pcs) {
       // ---- (b') the chunk's (sector, pc) word masks as bytes: pcm[2 j + pc / 4]
       // byte pc % 4 = OR of the masks of sector s0 + j's keys of that pc, in the
       // (now clear) first win u64 slots of the table ----
-      uint32_t* const pcm = reinterpret_cast<uint32_t*>(tab);
-      for (uint32_t j = threadIdx.x; j < 2 * (uint32_t)win; j += kSegThreads) pcm[j] = 0;
-      __syncthreads();
+      uint32_t* const pcm = reinterpret_cast<uint32_t*>(tab);  // (zeroed with the table clear)
       const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;
 #pragma unroll
       for (int j = 0; j < kKPT; ++j) {
