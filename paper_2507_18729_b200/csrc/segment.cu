@@ -633,10 +633,12 @@ __device__ __forceinline__ void chunk_insert_regs(ull* tab, uint16_t* list, uint
 // OR-ed masks; each insert adds what it created to the sector's counters in
 // cnt ([sector][5]: words (2b, 2b+1) as u16 pairs, the sector count): a new
 // entry is a new warp of the sector, each bit it gains a new (warp, word)
-// (P:328 flush); returns the entries this thread created
+// (P:328 flush); with pcm (<= 8 pc ids), each key also ORs its word mask into
+// the (sector, pc) byte pcm[2 (sector - s0) + pc / 4] byte pc % 4; returns the
+// entries this thread created
 __device__ __forceinline__ uint32_t chunk_insert_count(ull* tab, const ull (&kk)[kKPT], uint32_t nk, ull s0,
                                                        const KeyLayout& kl, uint32_t filter, uint32_t LW, uint32_t RS,
-                                                       ull M, uint32_t* cnt) {
+                                                       ull M, uint32_t* cnt, uint32_t* pcm) {
   const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;  // (uniform)
   uint32_t fresh = 0;  // entries this thread created
 #pragma unroll
@@ -655,6 +657,10 @@ __device__ __forceinline__ uint32_t chunk_insert_count(ull* tab, const ull (&kk)
       for (int q = 0; q < 4; ++q) {
         const uint32_t add = ((r >> (2 * q)) & 1u) | (((r >> (2 * q + 1)) & 1u) << 16);
         if (add) atomicAdd(&cg[q], add);
+      }
+      if (pcm) {  // <= 8 pc ids: the key's word mask into its (sector, pc) byte
+        const uint32_t pcid = (uint32_t)(k >> 8) & 7u;
+        atomicOr(&pcm[2 * gl + (pcid >> 2)], ((uint32_t)k & 0xFFu) << (8 * (pcid & 3u)));
       }
     }
     fresh += (r >> 8) & 1u;
@@ -716,13 +722,17 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
     const ull k0 = cko[c];
     const uint32_t nk = (uint32_t)(cko[c + 1] - k0);  // < 2 kSegCap
     const ull win = s1 - s0;  // <= kChunkSec <= kHWin: the chunk's rows are counted in shared memory
+    // few pc ids: the (sector, pc) byte masks live in the list region (the
+    // hashed per-pc pass's, unused then)
+    uint32_t* const pcm = (few_pcs && pc_hist) ? reinterpret_cast<uint32_t*>(list) : nullptr;
     for (uint32_t i = threadIdx.x; i < (uint32_t)win * 5; i += kSegThreads) cnt[i] = 0;
+    if (pcm)
+      for (uint32_t i = threadIdx.x; i < 2 * (uint32_t)win; i += kSegThreads) pcm[i] = 0;
     __syncthreads();
     // ---- (a) distinct (sector, launch, warp) ----
     ull kk[kKPT];
     chunk_load(kk, seg, k0, nk);
-    distinct += chunk_insert_count(tab, kk, nk, s0, kl, filter, LW, RS, lwmask, cnt);
-    __syncthreads();
+    distinct += chunk_insert_count(tab, kk, nk, s0, kl, filter, LW, RS, lwmask, cnt, pcm);
     __syncthreads();
     // the chunk owns its sectors: plain stores of every row, zeros included
     // (the build does not clear the dense rows on this path; a big sector's
@@ -737,30 +747,11 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
       reinterpret_cast<uint4*>(wc + 8 * g)[0] = lo;
       reinterpret_cast<uint4*>(wc + 8 * g)[1] = hi;
     }
-    // (a)'s entries cleared; with few pc ids the first win slots become the
-    // zeroed (sector, pc) byte masks of (b') at the same time
-    const uint32_t pcz = (few_pcs && pc_hist) ? (uint32_t)win : 0u;
-    for (uint32_t i = threadIdx.x; i < (uint32_t)kHSlots; i += kSegThreads) tab[i] = i < pcz ? 0ull : kHEmpty;
+    for (uint32_t i = threadIdx.x; i < (uint32_t)kHSlots; i += kSegThreads) tab[i] = kHEmpty;  // (a)'s entries
     if (!pc_hist) continue;  // (uniform)
-    __syncthreads();
-    if (few_pcs) {
-      // ---- (b') the chunk's (sector, pc) word masks as bytes: pcm[2 j + pc / 4]
-      // byte pc % 4 = OR of the masks of sector s0 + j's keys of that pc, in the
-      // (now clear) first win u64 slots of the table ----
-      uint32_t* const pcm = reinterpret_cast<uint32_t*>(tab);  // (zeroed with the table clear)
-      const uint32_t jmax = (nk + kSegThreads - 1) / kSegThreads;
-#pragma unroll
-      for (int j = 0; j < kKPT; ++j) {
-        if ((uint32_t)j >= jmax) break;
-        const ull k = kk[j];
-        bool ok = j * kSegThreads + threadIdx.x < nk;
-        if (filter != THERMO_ALL_LAUNCHES) ok = ok && key_launch(k, kl) == filter;
-        if (ok) {
-          const uint32_t gl = (uint32_t)(key_g(k, kl) - s0), pcid = (uint32_t)(k >> 8) & 7u;
-          atomicOr(&pcm[2 * gl + (pcid >> 2)], ((uint32_t)k & 0xFFu) << (8 * (pcid & 3u)));
-        }
-      }
-      __syncthreads();
+    if (pcm) {
+      // ---- (b') the chunk's (sector, pc) word-mask bytes (filled by pass (a))
+      // binned at the sectors' and words' levels ----
       uint32_t npcs = 0;
       for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) {
         const uint32_t p0 = pcm[2 * j], p1 = pcm[2 * j + 1];
@@ -782,10 +773,9 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_chunk_kernel(const ull* __
         }
       }
       distinct_pc += npcs;  // (per thread: summed below)
-      __syncthreads();
-      for (uint32_t j = threadIdx.x; j < (uint32_t)win; j += kSegThreads) tab[j] = kHEmpty;
       continue;
     }
+    __syncthreads();
     // ---- (b) distinct (sector, pc id) -> per-pc level histograms ----
     chunk_insert_regs(tab, list, &s_n[1], kk, nk, s0, kl, filter, kl.P, 8, pmask);
     __syncthreads();
