@@ -85,7 +85,7 @@ __device__ ull block_prev_last(ull last_or_none, ull* s_w) {
 }
 
 // mode 0: sums + votes; mode 1: verify count of gaps == candidate
-__global__ void __launch_bounds__(kIndThreads) indicator_tile_kernel(IndicatorArgs a, int mode) {
+__global__ void __launch_bounds__(kIndThreads, 4) indicator_tile_kernel(IndicatorArgs a, int mode) {
   __shared__ ull s_w[kIndThreads / 32];
   __shared__ ull s_red[kIndThreads / 32][13];
   const uint32_t tile = blockIdx.x;
