@@ -257,7 +257,9 @@ constexpr int kCoarse = 1024;
 constexpr int kPT = 512;                 // partition threads (16 warps: two CTAs fill an SM's 32 warps)
 constexpr int kPPer = 8;                 // keys per thread
 constexpr int kPTile = kPT * kPPer;      // 4096 keys per tile
-constexpr int kFineBins = 4096;          // pass-2 destinations per bucket (more: direct scatter)
+constexpr int kFPer = 4;                 // pass 2: keys per thread
+constexpr int kFTile = kPT * kFPer;      // pass-2 tile (2048 keys): smaller tiles, three CTAs per SM
+constexpr int kFineBins = 2048;          // pass-2 destinations per bucket (more: direct scatter)
 
 // block-wide exclusive scan of cnt[0, nbins) into excl (nbins <= kFineBins), returns the total
 __device__ __forceinline__ uint32_t block_excl_scan(const uint32_t* cnt, uint32_t* excl, uint32_t nbins,
@@ -322,8 +324,8 @@ struct PartSmem {
   uint32_t cnt[kFineBins];
   uint32_t excl[kFineBins];
   ull base[kFineBins];
-  ull stage[kPTile];
-  uint16_t sd[kPTile];  // pass 2: the staged key's destination
+  ull stage[kFTile];
+  uint16_t sd[kFTile];  // pass 2: the staged key's destination
   uint32_t wsum[kPT / 32];
 };
 
@@ -399,7 +401,7 @@ __global__ void seg_tiles_kernel(const ull* __restrict__ tot, uint32_t ncoarse, 
     const uint32_t b = b0 + threadIdx.x;
     ull v = 0;
     if (b < ncoarse) {
-      v = (cstart[b + 1] - cstart[b] + kPTile - 1) / kPTile;
+      v = (cstart[b + 1] - cstart[b] + kFTile - 1) / kFTile;
       ccur[b] = cstart[b];
     }
     ull incl = v;
@@ -427,7 +429,7 @@ __global__ void seg_tilemap_kernel(const ull* __restrict__ tpre, uint32_t ncoars
 }
 
 // pass 2: tile t of coarse bucket b -> its chunks (out) and big sectors (big)
-__global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict__ tmp, KeyLayout kl,
+__global__ void __launch_bounds__(kPT, 3) seg_fine_kernel(const ull* __restrict__ tmp, KeyLayout kl,
                                                        uint32_t ncoarse, const ull* __restrict__ cstart,
                                                        const ull* __restrict__ cinfo, const ull* __restrict__ tpre,
                                                        const uint32_t* __restrict__ tbk,
@@ -442,23 +444,23 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   const ull t = blockIdx.x;
   if (t >= tpre[ncoarse]) return;
   const uint32_t b = tbk[t];  // bucket b: tpre[b] <= t < tpre[b + 1]
-  const ull k0 = cstart[b] + (t - tpre[b]) * kPTile;
-  const ull k1 = k0 + kPTile < cstart[b + 1] ? k0 + kPTile : cstart[b + 1];
+  const ull k0 = cstart[b] + (t - tpre[b]) * kFTile;
+  const ull k1 = k0 + kFTile < cstart[b + 1] ? k0 + kFTile : cstart[b + 1];
   const ull nl0 = cinfo[3 * b], nl1 = cinfo[3 * b + 3];
   const ull bs0 = cinfo[3 * b + 1], bs1 = cinfo[3 * b + 4];
   // the bucket's chunks lie in [chunk_of(nl0, g0), chunk_of(nl1, g1)] (monotone)
   const ull c_lo = chunk_of(nl0, cinfo[3 * b + 2]);
   const uint32_t nbn = nl1 > nl0 ? (uint32_t)(chunk_of(nl1, cinfo[3 * b + 5]) - c_lo + 1) : 0u;  // chunk bins
   const uint32_t nbins = nbn + (uint32_t)(bs1 - bs0);
-  ull k[kPPer];
-  uint32_t d[kPPer];  // destination, ~0 = none; below kFineBins bins: | rank << 16
+  ull k[kFPer];
+  uint32_t d[kFPer];  // destination, ~0 = none; below kFineBins bins: | rank << 16
 #pragma unroll
-  for (int u = 0; u < kPPer; ++u) {
+  for (int u = 0; u < kFPer; ++u) {
     const ull i = k0 + (ull)u * kPT + threadIdx.x;
     k[u] = i < k1 ? tmp[i] : 0ull;
   }
 #pragma unroll
-  for (int u = 0; u < kPPer; ++u) {
+  for (int u = 0; u < kFPer; ++u) {
     const ull i = k0 + (ull)u * kPT + threadIdx.x;
     uint32_t dd = 0xFFFFFFFFu;
     if (i < k1) {
@@ -471,7 +473,7 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
     // too many destinations for one tile's histogram: per-key cursor atomics
     // (warp-aggregated), written directly
 #pragma unroll
-    for (int u = 0; u < kPPer; ++u) {
+    for (int u = 0; u < kFPer; ++u) {
       const unsigned peers = __match_any_sync(GFULL, d[u]);
       const int ldr = __ffs(peers) - 1;
       ull p0 = 0;
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   // rank within the destination: one shared atomic per key (order within a
   // destination is free)
 #pragma unroll
-  for (int u = 0; u < kPPer; ++u)
+  for (int u = 0; u < kFPer; ++u)
     if (d[u] != 0xFFFFFFFFu) d[u] |= atomicAdd(&sm.cnt[d[u]], 1u) << 16;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nbins; i += kPT)
@@ -497,7 +499,7 @@ __global__ void __launch_bounds__(kPT, 2) seg_fine_kernel(const ull* __restrict_
   const uint32_t tot = block_excl_scan(sm.cnt, sm.excl, nbins, sm.wsum);
   // stage in destination order (with each key's destination), then write runs
 #pragma unroll
-  for (int u = 0; u < kPPer; ++u)
+  for (int u = 0; u < kFPer; ++u)
     if (d[u] != 0xFFFFFFFFu) {
       const uint32_t dd = d[u] & 0xFFFFu;
       const uint32_t q = sm.excl[dd] + (d[u] >> 16);
@@ -1318,7 +1320,7 @@ cudaError_t segment_count(const ull* keys, ull n, ull* out, ull* big, KeyLayout 
     const unsigned g1 = (unsigned)std::min<ull>((n + kPTile - 1) / kPTile, (ull)num_sms * 2);
     seg_coarse_kernel<<<g1, kPT, csm, s>>>(keys, n, kl, ws.cb, ws.ncoarse, ws.ccur, ws.tmp);
     if (ws.ev[1]) cudaEventRecord(ws.ev[1], s);
-    const ull g2 = (n + kPTile - 1) / kPTile + ws.ncoarse;  // >= the tiles of all buckets
+    const ull g2 = (n + kFTile - 1) / kFTile + ws.ncoarse;  // >= the tiles of all buckets
     if (ws.tbk_cap < g2) {
       cudaFree(ws.tbk);
       ws.tbk = nullptr;
