@@ -72,12 +72,23 @@ __global__ void seg_scan_reduce(const uint32_t* __restrict__ in, ull n, ull* __r
   const ull base = (ull)blockIdx.x * kScanBlock;
   Sum3 t{0, 0, 0};
   uint32_t mx = 0;
-  for (int i = threadIdx.x; i < kScanBlock; i += kSegThreads) {
+  // 16-byte loads: thread t reads counts [4 t, 4 t + 4) and [1024 + 4 t, ...)
+  for (int i = threadIdx.x * 4; i < kScanBlock; i += kSegThreads * 4) {
     const ull j = base + i;
-    const uint32_t v = j < n ? in[j] : 0u;
-    const Sum3 q = sum3_of(v);
-    t.nl += q.nl; t.bs += q.bs; t.bk += q.bk;
-    mx = v > mx ? v : mx;
+    uint32_t v[4];
+    if (j + 4 <= n) {
+      const uint4 q4 = *reinterpret_cast<const uint4*>(in + j);
+      v[0] = q4.x; v[1] = q4.y; v[2] = q4.z; v[3] = q4.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = j + k < n ? in[j + k] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const Sum3 q = sum3_of(v[k]);
+      t.nl += q.nl; t.bs += q.bs; t.bk += q.bk;
+      mx = v[k] > mx ? v[k] : mx;
+    }
   }
   for (int d = 16; d; d >>= 1) {
     t.nl += __shfl_xor_sync(GFULL, t.nl, d);
