@@ -879,7 +879,7 @@ __device__ __forceinline__ bool big_or(ull* tab, uint32_t tb, ull id, uint32_t m
 // f(key) over big[b0, b0 + K), kBigUnroll loads in flight per thread (the
 // keys are re-read from L2 by each pass of the sector: latency-bound with one
 // load at a time)
-constexpr int kBigUnroll = 8;
+constexpr int kBigUnroll = 4;
 template <typename F>
 __device__ __forceinline__ void big_for_keys(const ull* __restrict__ big, ull b0, uint32_t K, F f) {
   for (uint32_t base = 0; base < K; base += kSegThreads * kBigUnroll) {
