@@ -94,6 +94,16 @@ CASES = [
 ]
 
 
+def _one_sector():
+    # one 32-byte sector read by 60 k warps (a multi-pass big sector on its owner
+    # rank, the other ranks' keys reaching it through the exchange)
+    from tests.test_gpu_parity import _one_sector_trace
+    return _one_sector_trace()
+
+
+CASES.append(_one_sector)
+
+
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("dedup", [1, 2, 3])
 @pytest.mark.parametrize("i", range(len(CASES)))
